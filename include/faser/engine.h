@@ -1,0 +1,270 @@
+/*
+ * faser/engine.h — C ABI of the B200-native FASER speculative-decoding data path.
+ *
+ * The reference (`/root/reference/proj/core`, C++20, CPU only) exposes the path as an
+ * in-process C++ class API. Every entry point below names the reference interface it
+ * replaces (file:line). Conventions:
+ *   - plain pointers + sizes, caller-owned HOST buffers unless a name says `_dev`;
+ *   - reference exceptions map to status codes (std::invalid_argument -> FASER_EINVAL,
+ *     std::logic_error -> FASER_EILLEGAL_STATE, errors.hpp:8-18 -> ECONFIG/EPARSE/EFIT);
+ *   - the message of the mapped exception is returned by faser_last_error();
+ *   - the library never falls back to CPU: if the CUDA kernels cannot run the call fails
+ *     with FASER_ECUDA.
+ */
+#ifndef FASER_ENGINE_H
+#define FASER_ENGINE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FASER_ABI_VERSION 1
+/* Largest speculative length a request may be assigned in one round (S = {1..10} in the
+ * reference, drafter.hpp:16). Bounds per-request outcome arrays. */
+#define FASER_MAX_SPEC 32
+/* Largest layer count the per-layer exit-threshold table covers. */
+#define FASER_MAX_LAYERS 128
+
+typedef enum faser_status {
+  FASER_OK = 0,
+  FASER_EINVAL = 1,         /* std::invalid_argument */
+  FASER_EILLEGAL_STATE = 2, /* std::logic_error: draft/commit on done request, stale outcome */
+  FASER_ECONFIG = 3,        /* specsim::ConfigError */
+  FASER_EPARSE = 4,         /* specsim::ParseError */
+  FASER_EFIT = 5,           /* specsim::FitError */
+  FASER_ECUDA = 6,          /* device missing / kernel failure (never silently degraded) */
+  FASER_ENCCL = 7,
+  FASER_ENOMEM = 8,
+  FASER_ECAPACITY = 9       /* engine slot / sequence capacity exceeded */
+} faser_status;
+
+/* ---------------------------------------------------------------- model descriptors */
+
+/* LayeredToyLM::Params (toylm.hpp:42-51). `divergence` is eta of draft_next. */
+typedef struct faser_toy_params {
+  uint64_t seed;
+  int32_t vocab;
+  int32_t layers;
+  int32_t order;
+  int32_t reserved0;
+  double divergence;
+  uint64_t noise_seed;
+  double logit_scale;
+  double noise_scale;
+} faser_toy_params;
+
+/* ExitPolicy (exitctl.hpp:14-22). */
+typedef struct faser_exit_policy {
+  int32_t l_init;
+  int32_t k_init;
+  int32_t k_final;
+} faser_exit_policy;
+
+/* GatePlan (exitctl.hpp:60-67): gated layers are [first_layer, stop_layer). */
+typedef struct faser_gate_plan {
+  int32_t first_layer;
+  int32_t stop_layer;
+  double s_eff;
+} faser_gate_plan;
+
+/* GateEntry (exitctl.hpp:24-28). */
+typedef struct faser_gate_entry {
+  int32_t spec_length;
+  int32_t reserved0;
+  double accept_estimate;
+} faser_gate_entry;
+
+/* OverlapPlan (overlap.hpp:11-17). */
+typedef struct faser_overlap_plan {
+  int32_t enabled;
+  int32_t chunk;
+  double r;
+  double predicted_ms;
+  double serial_ms;
+} faser_overlap_plan;
+
+/* PiecewiseLatencyParams (latmodel.hpp:32-38); stage: 0 draft, 1 target, 2 ee_check, 3 prune. */
+typedef struct faser_latency_params {
+  int32_t stage;
+  int32_t reserved0;
+  double knee, a1, gamma1, a2, gamma2, c0, c1, c2;
+} faser_latency_params;
+
+/* LatencyModel (latmodel.hpp:92-113). */
+typedef struct faser_latency_model {
+  faser_latency_params draft, target, ee_check, prune;
+} faser_latency_model;
+
+/* VerifyOutcome (sdcore.hpp:59-77), flattened: optionals become has_* flags. */
+typedef struct faser_verify_outcome {
+  int32_t submitted;
+  int32_t accepted_count;
+  int32_t has_recovery;
+  int32_t recovery_token;
+  int32_t has_pruned;
+  int32_t pruned_index; /* pruned_at->first  */
+  int32_t pruned_layer; /* pruned_at->second */
+  int32_t gate_layers;
+  double full_layers_run;
+  int32_t false_prune;
+  int32_t n_prune_layers;
+  int32_t prune_layers[FASER_MAX_SPEC];
+  int64_t base_len;
+} faser_verify_outcome;
+
+/* ------------------------------------------------- stateless batched toy-model kernels
+ * Ragged batch convention: request i's context (prompt ++ committed) is
+ * tokens[offsets[i] .. offsets[i+1]), offsets has n+1 entries. */
+
+/* LayeredToyLM::final_and_noise (toylm.cpp:42-54) per row -> z_final/z_noise [n][vocab]. */
+faser_status faser_toy_final_and_noise(const faser_toy_params* model, int32_t n,
+                                       const int32_t* tokens, const int64_t* offsets,
+                                       double* z_final, double* z_noise);
+
+/* LayeredToyLM::target_logits (toylm.cpp:56-67) per row at layers[i] -> z [n][vocab]. */
+faser_status faser_toy_target_logits(const faser_toy_params* model, int32_t n,
+                                     const int32_t* tokens, const int64_t* offsets,
+                                     const int32_t* layers, double* z);
+
+/* LayeredToyLM::target_next / draft_next (toylm.cpp:69-85) per row -> out[n]. */
+faser_status faser_toy_target_next(const faser_toy_params* model, int32_t n,
+                                   const int32_t* tokens, const int64_t* offsets, int32_t* out);
+faser_status faser_toy_draft_next(const faser_toy_params* model, int32_t n,
+                                  const int32_t* tokens, const int64_t* offsets, int32_t* out);
+
+/* SpeculativeEngine::draft_tokens (sdcore.cpp:45-59) per request.
+ * s[i] >= 1, remaining[i] = max_out - |committed| >= 1 (else EILLEGAL_STATE, "done").
+ * out [n][FASER_MAX_SPEC], out_len[n]. */
+faser_status faser_toy_draft_tokens(const faser_toy_params* model, int32_t n,
+                                    const int32_t* tokens, const int64_t* offsets,
+                                    const int32_t* s, const int32_t* remaining,
+                                    int32_t* out, int32_t* out_len);
+
+/* SpeculativeEngine::full_verify (sdcore.cpp:61-81) when gate == NULL, else
+ * SpeculativeEngine::verify_with_early_exit (sdcore.cpp:83-180) with `policy`/`gate`.
+ * committed_len[i] = |req.committed| (for exempt positions), exempt[i] = req.exempt_position.
+ * k_table (may be NULL) overrides policy->k_at: k_table[layer] for layer in [0, layers]. */
+faser_status faser_toy_verify(const faser_toy_params* model, int32_t n, const int32_t* tokens,
+                              const int64_t* offsets, const int32_t* committed_len,
+                              const int32_t* exempt, const int32_t* drafted,
+                              const int32_t* drafted_len, const faser_exit_policy* policy,
+                              const faser_gate_plan* gate, faser_verify_outcome* out);
+
+/* ------------------------------------------------------------ stateful serving engine
+ * Replaces the missing serving loop's use of SpeculativeEngine + Request (sdcore.hpp:39-116,
+ * SPEC.md:541-563): requests are submitted (iteration-boundary admission), every
+ * faser_step() runs draft -> verify(+early exit) -> accept -> commit for all live requests
+ * on the GPU and returns one faser_round_result per live request. */
+
+enum { FASER_MODEL_TOY = 0, FASER_MODEL_LLAMA = 1 };
+/* AblationMode (config.hpp:16). */
+enum { FASER_MODE_VSD = 0, FASER_MODE_VSD_AD = 1, FASER_MODE_VSD_AD_EE = 2, FASER_MODE_FULL = 3 };
+
+typedef struct faser_model_desc {
+  int32_t kind; /* FASER_MODEL_TOY */
+  int32_t reserved0;
+  faser_toy_params toy;
+} faser_model_desc;
+
+typedef struct faser_engine_cfg {
+  int32_t device;
+  int32_t max_batch;       /* B_max, config.hpp:50 (256) */
+  int32_t max_seq_len;     /* prompt + max_out capacity per request */
+  int32_t mode;            /* FASER_MODE_*: EE modes use verify_with_early_exit */
+  int32_t default_spec_length; /* fixed_spec_len, config.hpp:51 (4) */
+  int32_t exempt_rule;     /* 1: exempt = committed_before + pruned_at.first for one round */
+  faser_exit_policy exit_policy;
+  int32_t max_pending;     /* capacity of the submitted-not-admitted queue */
+  int32_t pending_tokens;  /* device staging arena for submitted prompts (tokens) */
+} faser_engine_cfg;
+
+typedef struct faser_step_plan {
+  faser_gate_plan gate;         /* used in EE modes; inactive gate == full verify semantics */
+  int32_t use_k_table;          /* 1: k_table[layer] replaces exit_policy.k_at */
+  int32_t k_table[FASER_MAX_LAYERS + 1];
+  faser_overlap_plan overlap;   /* FULL mode: chunked draft/verify co-execution */
+} faser_step_plan;
+
+typedef struct faser_round_result {
+  int64_t req_id;
+  int32_t spec_length;       /* k_i used this round */
+  int32_t drafted;           /* tokens drafted (<= k_i: budget / EOS stop) */
+  faser_verify_outcome outcome;
+  int32_t committed;         /* tokens committed this round (SpeculativeEngine::commit) */
+  int32_t done;
+  int32_t exempt_position;   /* value for the next round */
+  int32_t n_committed_total;
+  int32_t tokens[FASER_MAX_SPEC + 1]; /* the tokens committed this round */
+} faser_round_result;
+
+typedef struct faser_engine faser_engine;
+
+faser_status faser_engine_create(const faser_model_desc* model, const faser_engine_cfg* cfg,
+                                 faser_engine** out);
+void faser_engine_destroy(faser_engine* e);
+/* Message of the last failing call on `e` (or of the last failed create when e == NULL). */
+const char* faser_last_error(const faser_engine* e);
+
+faser_status faser_submit(faser_engine* e, int64_t req_id, const int32_t* prompt, int32_t len,
+                          int32_t max_out);
+/* Controller -> engine (AdaptiveDrafter::assign_lengths output, drafter.hpp:105-107). */
+faser_status faser_set_spec_lengths(faser_engine* e, const int64_t* req_ids, const int32_t* k,
+                                    int32_t n);
+/* Requests that the next faser_step() will run, in batch order (admits pending ones). */
+faser_status faser_live_requests(faser_engine* e, int64_t* req_ids, int32_t cap, int32_t* n);
+faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_round_result* out,
+                        int32_t cap, int32_t* n_out);
+faser_status faser_get_committed(faser_engine* e, int64_t req_id, int32_t* buf, int32_t cap,
+                                 int32_t* n);
+/* Drops a finished request's host state (its slot is already free once done). */
+faser_status faser_release(faser_engine* e, int64_t req_id);
+/* Number of live + pending requests. */
+int32_t faser_pending_work(const faser_engine* e);
+/* Device time (ms, CUDA events on the engine stream) of the last faser_step: draft lane,
+ * verify lane and whole step. */
+faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, float* verify_ms,
+                                    float* step_ms);
+/* Bytes the last faser_step copied host->device (step plan + admissions) and
+ * device->host (round results). */
+faser_status faser_last_step_bytes(const faser_engine* e, int64_t* h2d, int64_t* d2h);
+/* The engine's CUDA stream (cudaStream_t) so a caller can record events around steps. */
+void* faser_engine_stream(const faser_engine* e);
+/* Kernel launches issued by this engine since creation (evidence counter). */
+int64_t faser_kernel_launches(const faser_engine* e);
+
+/* ABI self-description: FASER_ABI_VERSION and sizeof() of every struct above, in
+ * declaration order (toy_params, exit_policy, gate_plan, gate_entry, overlap_plan,
+ * latency_params, latency_model, verify_outcome, model_desc, engine_cfg, step_plan,
+ * round_result). Writes min(n, 12) entries. */
+int32_t faser_abi_version(void);
+faser_status faser_abi_struct_sizes(int64_t* out, int32_t n);
+
+/* ------------------------------------------------- host-side controllers (scalar math)
+ * exitctl.cpp / overlap.cpp / latmodel.cpp restated natively; no device work. */
+
+/* ExitPolicy::k_at (exitctl.cpp:9-17) for layer = 0..num_layers -> table[num_layers+1]. */
+faser_status faser_k_table(const faser_exit_policy* policy, int32_t num_layers, int32_t* table);
+/* LatencyModel::default_ground_truth (latmodel.cpp:396-403). */
+void faser_default_latency_model(faser_latency_model* out);
+/* eval_latency (latmodel.cpp:32-62); stage 0..3. */
+faser_status faser_eval_latency(const faser_latency_model* m, int32_t stage, double b, double s,
+                                double r, double* out_ms);
+/* make_gate_plan (exitctl.cpp:70-82); models NULL = default ground truth. */
+faser_status faser_make_gate_plan(const faser_exit_policy* policy, const faser_gate_entry* batch,
+                                  int32_t n, double b, double r, const faser_latency_model* models,
+                                  int32_t num_layers, faser_gate_plan* out);
+/* plan_overlap (overlap.cpp:23-42). */
+faser_status faser_plan_overlap(int32_t s, int32_t b, const faser_latency_model* models,
+                                const double* r_grid, int32_t n_r, faser_overlap_plan* out);
+
+/* Deterministic workload inputs (workload.cpp:116-122): synth_prompt. */
+faser_status faser_synth_prompt(uint64_t seed, int32_t index, int32_t len, int32_t vocab,
+                                int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASER_ENGINE_H */

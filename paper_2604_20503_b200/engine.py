@@ -1,0 +1,260 @@
+"""Python mirror of the C ABI (include/faser/engine.h) over ``libfaser_b200.so``.
+
+Names follow the reference's C++ API so tests read like the reference's own:
+  * ``LayeredToyLM``      — toylm.hpp:40-87 (final_and_noise, target_logits, target_next,
+                            draft_next), batched over a ragged set of prefixes;
+  * ``SpeculativeEngine`` — sdcore.hpp:81-116 (draft_tokens, full_verify,
+                            verify_with_early_exit), batched over requests;
+  * ``ServingEngine``     — the stateful submit/step engine that replaces the serving loop.
+Every call runs the CUDA kernels; if the library (or a GPU) is missing the call raises —
+there is no CPU fallback anywhere in this package.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+_LIB = None
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfaser_b200.so")
+
+
+class FaserError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{abi.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib():
+    """Load the product library (raises if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.faser_last_error.restype = C.c_char_p
+        L.faser_last_error.argtypes = [C.c_void_p]
+        L.faser_kernel_launches.restype = C.c_int64
+        L.faser_kernel_launches.argtypes = [C.c_void_p]
+        L.faser_pending_work.restype = C.c_int32
+        L.faser_pending_work.argtypes = [C.c_void_p]
+        L.faser_engine_stream.restype = C.c_void_p
+        L.faser_engine_stream.argtypes = [C.c_void_p]
+        L.faser_engine_destroy.argtypes = [C.c_void_p]
+        L.faser_engine_destroy.restype = None
+        _LIB = L
+    return _LIB
+
+
+def _check(rc, engine=None):
+    if rc != 0:
+        msg = lib().faser_last_error(engine)
+        raise FaserError(rc, msg.decode() if msg else "")
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _ragged(rows):
+    off = np.zeros(len(rows) + 1, np.int64)
+    for i, r in enumerate(rows):
+        off[i + 1] = off[i] + len(r)
+    flat = np.zeros(max(int(off[-1]), 1), np.int32)
+    for i, r in enumerate(rows):
+        flat[off[i]:off[i + 1]] = r
+    return flat, off
+
+
+class LayeredToyLM:
+    """GPU LayeredToyLM (toylm.hpp:40-87); every method takes a list of prefixes."""
+
+    def __init__(self, params=None):
+        self.params = params if params is not None else abi.ToyParams.default()
+
+    @property
+    def vocab_size(self):
+        return self.params.vocab
+
+    @property
+    def eos_token(self):
+        return self.params.vocab - 1
+
+    def final_and_noise(self, prefixes):
+        tok, off = _ragged(prefixes)
+        V = self.params.vocab
+        zf = np.zeros((len(prefixes), V), np.float64)
+        zn = np.zeros_like(zf)
+        _check(lib().faser_toy_final_and_noise(C.byref(self.params), len(prefixes), _ptr(tok),
+                                               _ptr(off), _ptr(zf), _ptr(zn)))
+        return zf, zn
+
+    def target_logits(self, prefixes, layers):
+        tok, off = _ragged(prefixes)
+        lay = np.ascontiguousarray(np.broadcast_to(layers, (len(prefixes),)), np.int32)
+        z = np.zeros((len(prefixes), self.params.vocab), np.float64)
+        _check(lib().faser_toy_target_logits(C.byref(self.params), len(prefixes), _ptr(tok),
+                                              _ptr(off), _ptr(lay), _ptr(z)))
+        return z
+
+    def _next(self, fn, prefixes):
+        tok, off = _ragged(prefixes)
+        out = np.zeros(len(prefixes), np.int32)
+        _check(fn(C.byref(self.params), len(prefixes), _ptr(tok), _ptr(off), _ptr(out)))
+        return out
+
+    def target_next(self, prefixes):
+        return self._next(lib().faser_toy_target_next, prefixes)
+
+    def draft_next(self, prefixes):
+        return self._next(lib().faser_toy_draft_next, prefixes)
+
+
+class SpeculativeEngine:
+    """GPU SpeculativeEngine (sdcore.hpp:81-116), batched: request i is described by its
+    context (prompt ++ committed), |committed| and exempt_position."""
+
+    def __init__(self, model):
+        self.model = model
+
+    def draft_tokens(self, contexts, s, remaining):
+        tok, off = _ragged(contexts)
+        n = len(contexts)
+        s = np.ascontiguousarray(np.broadcast_to(s, (n,)), np.int32)
+        rem = np.ascontiguousarray(np.broadcast_to(remaining, (n,)), np.int32)
+        out = np.zeros((n, abi.MAX_SPEC), np.int32)
+        ol = np.zeros(n, np.int32)
+        _check(lib().faser_toy_draft_tokens(C.byref(self.model.params), n, _ptr(tok), _ptr(off),
+                                            _ptr(s), _ptr(rem), _ptr(out), _ptr(ol)))
+        return [out[i, :ol[i]].tolist() for i in range(n)]
+
+    def _verify(self, contexts, drafted, committed_len, exempt, policy, gate):
+        tok, off = _ragged(contexts)
+        n = len(contexts)
+        cl = np.ascontiguousarray(np.broadcast_to(committed_len, (n,)), np.int32)
+        ex = np.ascontiguousarray(np.broadcast_to(exempt, (n,)), np.int32)
+        d = np.zeros((n, abi.MAX_SPEC), np.int32)
+        dl = np.zeros(n, np.int32)
+        for i, r in enumerate(drafted):
+            d[i, :len(r)] = r
+            dl[i] = len(r)
+        out = (abi.VerifyOutcome * max(n, 1))()
+        pol = policy or abi.ExitPolicy.default()
+        _check(lib().faser_toy_verify(C.byref(self.model.params), n, _ptr(tok), _ptr(off), _ptr(cl),
+                                      _ptr(ex), _ptr(d), _ptr(dl), C.byref(pol),
+                                      C.byref(gate) if gate is not None else None, out))
+        return list(out[:n])
+
+    def full_verify(self, contexts, drafted):
+        return self._verify(contexts, drafted, 0, -1, None, None)
+
+    def verify_with_early_exit(self, contexts, drafted, policy, gate, committed_len, exempt=-1):
+        return self._verify(contexts, drafted, committed_len, exempt, policy, gate)
+
+
+def default_engine_cfg(**kw):
+    cfg = abi.EngineCfg(device=0, max_batch=256, max_seq_len=4096, mode=abi.MODE_VSD,
+                        default_spec_length=4, exempt_rule=1,
+                        exit_policy=abi.ExitPolicy.default(), max_pending=1 << 20,
+                        pending_tokens=1 << 24)
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+def k_table(policy, num_layers):
+    t = (C.c_int32 * (abi.MAX_LAYERS + 1))()
+    _check(lib().faser_k_table(C.byref(policy), num_layers, t))
+    return t
+
+
+def make_gate_plan(policy, entries, b, r, num_layers, models=None):
+    arr = (abi.GateEntry * max(len(entries), 1))()
+    for i, (s, a) in enumerate(entries):
+        arr[i].spec_length = s
+        arr[i].accept_estimate = a
+    g = abi.GatePlan()
+    _check(lib().faser_make_gate_plan(C.byref(policy), arr, len(entries), C.c_double(b),
+                                      C.c_double(r), C.byref(models) if models else None,
+                                      num_layers, C.byref(g)))
+    return g
+
+
+class ServingEngine:
+    """Stateful GPU engine: submit() requests, step() one draft->verify->commit round."""
+
+    def __init__(self, model_params=None, cfg=None, **cfg_kw):
+        self.h = None
+        self.params = model_params if model_params is not None else abi.ToyParams.default()
+        self.cfg = cfg if cfg is not None else default_engine_cfg(**cfg_kw)
+        desc = abi.ModelDesc(kind=abi.MODEL_TOY, toy=self.params)
+        h = C.c_void_p()
+        _check(lib().faser_engine_create(C.byref(desc), C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        self._res = (abi.RoundResult * self.cfg.max_batch)()
+        self.plan = abi.StepPlan()
+        self.plan.gate = abi.GatePlan(self.cfg.exit_policy.l_init, self.cfg.exit_policy.l_init, 1.0)
+
+    def close(self):
+        if self.h:
+            lib().faser_engine_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def submit(self, req_id, prompt, max_out):
+        p = np.ascontiguousarray(prompt, np.int32)
+        _check(lib().faser_submit(self.h, C.c_int64(req_id), _ptr(p), len(p), max_out), self.h)
+
+    def set_spec_lengths(self, ids, ks):
+        ids = np.ascontiguousarray(ids, np.int64)
+        ks = np.ascontiguousarray(ks, np.int32)
+        _check(lib().faser_set_spec_lengths(self.h, _ptr(ids), _ptr(ks), len(ids)), self.h)
+
+    def live_requests(self):
+        buf = np.zeros(self.cfg.max_batch, np.int64)
+        n = C.c_int32()
+        _check(lib().faser_live_requests(self.h, _ptr(buf), len(buf), C.byref(n)), self.h)
+        return buf[:n.value].tolist()
+
+    def set_gate(self, gate):
+        self.plan.gate = gate
+
+    def step(self):
+        n = C.c_int32()
+        _check(lib().faser_step(self.h, C.byref(self.plan), self._res, self.cfg.max_batch,
+                                C.byref(n)), self.h)
+        return self._res[:n.value]
+
+    def committed(self, req_id, cap=1 << 16):
+        buf = np.zeros(cap, np.int32)
+        n = C.c_int32()
+        _check(lib().faser_get_committed(self.h, C.c_int64(req_id), _ptr(buf), cap, C.byref(n)),
+               self.h)
+        return buf[:n.value].tolist()
+
+    def pending_work(self):
+        return lib().faser_pending_work(self.h)
+
+    def last_step_timing(self):
+        a, b, c = C.c_float(), C.c_float(), C.c_float()
+        _check(lib().faser_last_step_timing(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def last_step_bytes(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().faser_last_step_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def stream_ptr(self):
+        return lib().faser_engine_stream(self.h)
+
+    def kernel_launches(self):
+        return lib().faser_kernel_launches(self.h)
