@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define FASER_ABI_VERSION 1
+#define FASER_ABI_VERSION 2
 /* Largest speculative length a request may be assigned in one round (S = {1..10} in the
  * reference, drafter.hpp:16). Bounds per-request outcome arrays. */
 #define FASER_MAX_SPEC 32
@@ -162,10 +162,24 @@ enum { FASER_MODEL_TOY = 0, FASER_MODEL_LLAMA = 1 };
 /* AblationMode (config.hpp:16). */
 enum { FASER_MODE_VSD = 0, FASER_MODE_VSD_AD = 1, FASER_MODE_VSD_AD_EE = 2, FASER_MODE_FULL = 3 };
 
+/* Llama-style random-init bf16 model (configs 3-5; no reference implementation exists, see
+ * SURVEY.md section 8c). Weights are a pure function of (seed, tensor, index), regenerated
+ * bit-identically by the CPU oracle (oracle/llama_oracle.c). bigram_scale / embed_noise set
+ * the acceptance-tunable construction (embedding(t) = bigram_scale * W_lm[g(t)] + noise). */
+typedef struct faser_llama_shape {
+  int32_t d_model, layers, n_heads, n_kv_heads, head_dim, ffn, vocab, reserved0;
+  double rope_theta, rms_eps;
+  double bigram_scale, embed_noise, init_std;
+  uint64_t seed;
+} faser_llama_shape;
+
 typedef struct faser_model_desc {
-  int32_t kind; /* FASER_MODEL_TOY */
+  int32_t kind; /* FASER_MODEL_TOY or FASER_MODEL_LLAMA */
   int32_t reserved0;
-  faser_toy_params toy;
+  faser_toy_params toy;       /* FASER_MODEL_TOY */
+  faser_llama_shape draft;    /* FASER_MODEL_LLAMA */
+  faser_llama_shape target;   /* FASER_MODEL_LLAMA */
+  uint32_t bigram_a, bigram_b; /* successor map g(t) = (a*t + b) mod vocab shared by both */
 } faser_model_desc;
 
 typedef struct faser_engine_cfg {
@@ -178,6 +192,10 @@ typedef struct faser_engine_cfg {
   faser_exit_policy exit_policy;
   int32_t max_pending;     /* capacity of the submitted-not-admitted queue */
   int32_t pending_tokens;  /* device staging arena for submitted prompts (tokens) */
+  int32_t max_spec_length; /* LLAMA: largest k_i a step may use (verify row capacity); 0 = 16 */
+  int32_t prefill_rows;    /* LLAMA: rows per prefill forward chunk; 0 = 8192 */
+  int32_t debug_capture;   /* LLAMA: 1 = keep per-stage logits of the last step for validation */
+  int32_t reserved1;
 } faser_engine_cfg;
 
 typedef struct faser_step_plan {
@@ -234,10 +252,24 @@ void* faser_engine_stream(const faser_engine* e);
 /* Kernel launches issued by this engine since creation (evidence counter). */
 int64_t faser_kernel_launches(const faser_engine* e);
 
+/* LLAMA validation mode (cfg.debug_capture = 1): logits of the last step's verify forward.
+ * stage = 0: final logits of the surviving rows; stage = l (1..L-1): the gated-layer logits
+ * (LM head on RMSNorm of the layer-l residual) of the rows tested at layer l.
+ * Writes min(rows, cap_rows) rows of `vocab` floats and, per row, (req_id, j) into row_ids
+ * [2*rows] (row j of a request predicts its drafted[j]). Returns the row count in *rows and
+ * FASER_EINVAL if the stage was not evaluated in the last step. */
+faser_status faser_debug_verify_logits(faser_engine* e, int32_t stage, float* logits,
+                                       int64_t* row_ids, int32_t cap_rows, int32_t* rows);
+/* Drafted tokens of the last step per live request (batch order), [n][FASER_MAX_SPEC]. */
+faser_status faser_debug_drafted(faser_engine* e, int32_t* drafted, int32_t cap, int32_t* n);
+/* Page table row of a live request: KV page ids backing positions [0, 64*n). */
+faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* pages, int32_t cap,
+                                  int32_t* n);
+
 /* ABI self-description: FASER_ABI_VERSION and sizeof() of every struct above, in
  * declaration order (toy_params, exit_policy, gate_plan, gate_entry, overlap_plan,
  * latency_params, latency_model, verify_outcome, model_desc, engine_cfg, step_plan,
- * round_result). Writes min(n, 12) entries. */
+ * round_result, llama_shape). Writes min(n, 13) entries. */
 int32_t faser_abi_version(void);
 faser_status faser_abi_struct_sizes(int64_t* out, int32_t n);
 

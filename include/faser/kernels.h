@@ -1,0 +1,29 @@
+/*
+ * faser/kernels.h — kernel-level C ABI of the B200 data path (device pointers, caller's
+ * stream). The serving engine (engine.h) drives the same launchers; these entry points
+ * exist so each kernel can be checked against its oracle and timed in isolation.
+ * All pointers are device pointers; `stream` is a cudaStream_t (NULL = legacy stream).
+ * Status codes as in engine.h; a missing GPU is FASER_ECUDA (never a CPU fallback).
+ */
+#ifndef FASER_KERNELS_H
+#define FASER_KERNELS_H
+
+#include <stdint.h>
+
+#include "faser/engine.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* out[t][n] = sum_k w[n][k] * x[t][k]; w bf16 [n_out][k], x bf16 [t][k], out fp32 [t][n_out].
+ * tcgen05 swap-AB GEMM (verify K2 / draft K1 projections). splits = 0 picks the engine's
+ * split-K heuristic. n_out % 128 == 0, k % 64 == 0. */
+faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,
+                               int32_t t, int32_t k, int32_t splits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASER_KERNELS_H */

@@ -84,8 +84,18 @@ class VerifyOutcome(C.Structure):
                 tuple(self.prune_layers[:self.n_prune_layers]), self.base_len)
 
 
+class LlamaShape(C.Structure):
+    """faser_llama_shape: Llama-style random-init bf16 model (configs 3-5)."""
+    _fields_ = [(n, C.c_int32) for n in ("d_model", "layers", "n_heads", "n_kv_heads", "head_dim",
+                                         "ffn", "vocab", "reserved0")] + [
+        (n, C.c_double) for n in ("rope_theta", "rms_eps", "bigram_scale", "embed_noise",
+                                  "init_std")] + [("seed", C.c_uint64)]
+
+
 class ModelDesc(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("reserved0", C.c_int32), ("toy", ToyParams)]
+    _fields_ = [("kind", C.c_int32), ("reserved0", C.c_int32), ("toy", ToyParams),
+                ("draft", LlamaShape), ("target", LlamaShape), ("bigram_a", C.c_uint32),
+                ("bigram_b", C.c_uint32)]
 
 
 class EngineCfg(C.Structure):
@@ -93,6 +103,8 @@ class EngineCfg(C.Structure):
         ("device", C.c_int32), ("max_batch", C.c_int32), ("max_seq_len", C.c_int32),
         ("mode", C.c_int32), ("default_spec_length", C.c_int32), ("exempt_rule", C.c_int32),
         ("exit_policy", ExitPolicy), ("max_pending", C.c_int32), ("pending_tokens", C.c_int32),
+        ("max_spec_length", C.c_int32), ("prefill_rows", C.c_int32), ("debug_capture", C.c_int32),
+        ("reserved1", C.c_int32),
     ]
 
 

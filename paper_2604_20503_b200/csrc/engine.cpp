@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "faser/engine.h"
+#include "llama_engine.cuh"
 #include "toy_kernels.cuh"
 
 namespace faser {
@@ -159,6 +160,7 @@ using namespace faser;
 
 // ------------------------------------------------------------------------------ engine
 struct faser_engine {
+  faser::LlamaEngine* llama = nullptr;  // model kind LLAMA: the transformer path
   faser_engine_cfg cfg{};
   faser_toy_params toy{};
   ToyDev m{};
@@ -191,6 +193,7 @@ struct faser_engine {
   std::vector<int32_t> free_slots;
 
   ~faser_engine() {
+    if (llama) faser::llama_engine_destroy(llama);
     if (stream) cudaStreamSynchronize(stream);
     for (auto& kv : reqs)
       if (kv.second.d_prompt) cudaFree(kv.second.d_prompt);
@@ -218,6 +221,7 @@ struct faser_engine {
 extern "C" {
 
 const char* faser_last_error(const faser_engine* e) {
+  if (e && e->llama) return faser::llama_last_error(e->llama);
   return e ? e->err.c_str() : g_last_error.c_str();
 }
 
@@ -226,6 +230,20 @@ faser_status faser_engine_create(const faser_model_desc* model, const faser_engi
   if (!out) return FASER_EINVAL;
   *out = nullptr;
   faser_engine* e = nullptr;
+  if (model && cfg && model->kind == FASER_MODEL_LLAMA) {
+    faser_status lst = FASER_OK;
+    const char* msg = "";
+    faser::LlamaEngine* le = faser::llama_engine_create(model, cfg, &lst, &msg);
+    if (!le) {
+      g_last_error = msg;
+      return lst;
+    }
+    e = new faser_engine();
+    e->llama = le;
+    e->cfg = *cfg;
+    *out = e;
+    return FASER_OK;
+  }
   faser_status st = guarded(nullptr, [&] {
     if (!model || !cfg) throw Fail{FASER_EINVAL, "null model or cfg"};
     if (model->kind != FASER_MODEL_TOY)
@@ -273,6 +291,7 @@ void faser_engine_destroy(faser_engine* e) { delete e; }
 faser_status faser_submit(faser_engine* e, int64_t req_id, const int32_t* prompt, int32_t len,
                           int32_t max_out) {
   if (!e) return FASER_EINVAL;
+  if (e->llama) return faser::llama_submit(e->llama, req_id, prompt, len, max_out);
   return guarded(&e->err, [&] {
     if (!prompt || len < 1) throw Fail{FASER_EINVAL, "prompt must be non-empty"};
     if (max_out < 0) throw Fail{FASER_EINVAL, "max_out must be >= 0"};
@@ -301,6 +320,7 @@ faser_status faser_submit(faser_engine* e, int64_t req_id, const int32_t* prompt
 faser_status faser_set_spec_lengths(faser_engine* e, const int64_t* req_ids, const int32_t* k,
                                     int32_t n) {
   if (!e) return FASER_EINVAL;
+  if (e->llama) return faser::llama_set_spec_lengths(e->llama, req_ids, k, n);
   return guarded(&e->err, [&] {
     for (int i = 0; i < n; ++i) {
       if (k[i] < 1 || k[i] > FASER_MAX_SPEC)
@@ -314,6 +334,7 @@ faser_status faser_set_spec_lengths(faser_engine* e, const int64_t* req_ids, con
 
 faser_status faser_live_requests(faser_engine* e, int64_t* req_ids, int32_t cap, int32_t* n) {
   if (!e || !n) return FASER_EINVAL;
+  if (e->llama) return faser::llama_live_requests(e->llama, req_ids, cap, n);
   return guarded(&e->err, [&] {
     e->admit_pending();
     *n = static_cast<int32_t>(e->live.size());
@@ -322,12 +343,14 @@ faser_status faser_live_requests(faser_engine* e, int64_t* req_ids, int32_t cap,
 }
 
 int32_t faser_pending_work(const faser_engine* e) {
+  if (e && e->llama) return faser::llama_pending_work(e->llama);
   return e ? static_cast<int32_t>(e->live.size() + e->pending.size()) : 0;
 }
 
 faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_round_result* out,
                         int32_t cap, int32_t* n_out) {
   if (!e || !n_out) return FASER_EINVAL;
+  if (e->llama) return faser::llama_step(e->llama, plan, out, cap, n_out);
   return guarded(&e->err, [&] {
     CK(cudaSetDevice(e->cfg.device));
     e->admit_pending();
@@ -422,6 +445,7 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
 faser_status faser_get_committed(faser_engine* e, int64_t req_id, int32_t* buf, int32_t cap,
                                  int32_t* n) {
   if (!e || !n) return FASER_EINVAL;
+  if (e->llama) return faser::llama_get_committed(e->llama, req_id, buf, cap, n);
   return guarded(&e->err, [&] {
     auto it = e->reqs.find(req_id);
     if (it == e->reqs.end()) throw Fail{FASER_EINVAL, "unknown request id"};
@@ -433,6 +457,7 @@ faser_status faser_get_committed(faser_engine* e, int64_t req_id, int32_t* buf, 
 
 faser_status faser_release(faser_engine* e, int64_t req_id) {
   if (!e) return FASER_EINVAL;
+  if (e->llama) return faser::llama_release(e->llama, req_id);
   return guarded(&e->err, [&] {
     auto it = e->reqs.find(req_id);
     if (it == e->reqs.end()) throw Fail{FASER_EINVAL, "unknown request id"};
@@ -444,22 +469,53 @@ faser_status faser_release(faser_engine* e, int64_t req_id) {
 faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, float* verify_ms,
                                     float* step_ms) {
   if (!e) return FASER_EINVAL;
+  if (e->llama) {
+    faser::llama_last_step_timing(e->llama, draft_ms, verify_ms, step_ms);
+    return FASER_OK;
+  }
   if (draft_ms) *draft_ms = e->t_draft;
   if (verify_ms) *verify_ms = e->t_verify;
   if (step_ms) *step_ms = e->t_step;
   return FASER_OK;
 }
 
-int64_t faser_kernel_launches(const faser_engine* e) { return e ? e->launches : 0; }
+int64_t faser_kernel_launches(const faser_engine* e) {
+  if (e && e->llama) return faser::llama_launches(e->llama);
+  return e ? e->launches : 0;
+}
 
 faser_status faser_last_step_bytes(const faser_engine* e, int64_t* h2d, int64_t* d2h) {
   if (!e) return FASER_EINVAL;
+  if (e->llama) {
+    faser::llama_last_step_bytes(e->llama, h2d, d2h);
+    return FASER_OK;
+  }
   if (h2d) *h2d = e->h2d_bytes;
   if (d2h) *d2h = e->d2h_bytes;
   return FASER_OK;
 }
 
-void* faser_engine_stream(const faser_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+void* faser_engine_stream(const faser_engine* e) {
+  if (e && e->llama) return faser::llama_stream(e->llama);
+  return e ? static_cast<void*>(e->stream) : nullptr;
+}
+
+faser_status faser_debug_verify_logits(faser_engine* e, int32_t stage, float* logits, int64_t* row_ids,
+                                       int32_t cap_rows, int32_t* rows) {
+  if (!e || !rows) return FASER_EINVAL;
+  if (!e->llama) return FASER_EINVAL;
+  return faser::llama_debug_verify_logits(e->llama, stage, logits, row_ids, cap_rows, rows);
+}
+
+faser_status faser_debug_drafted(faser_engine* e, int32_t* drafted, int32_t cap, int32_t* n) {
+  if (!e || !n || !e->llama) return FASER_EINVAL;
+  return faser::llama_debug_drafted(e->llama, drafted, cap, n);
+}
+
+faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n) {
+  if (!e || !n || !e->llama) return FASER_EINVAL;
+  return faser::llama_debug_kv_pages(e->llama, req_id, pages, cap, n);
+}
 
 // --------------------------------------------------------------- stateless batched toy ops
 

@@ -1,0 +1,111 @@
+// llama.cuh — device layout + launchers for the Llama-style draft/target pair (configs 3-5).
+//
+// The reference has no transformer: its "draft/target pair" is LayeredToyLM.
+// For configs 3-5 the build supplies random-init bf16 Llama-shaped models whose weights are a
+// pure function of (seed, tensor tag, element index) so that the CPU fp32 oracle
+// (oracle/llama_oracle.c) regenerates exactly the same bf16 values. Acceptance is made
+// tunable by a "bigram" construction (the analogue of the toy's eta, toylm.cpp:76-85): the
+// embedding of token t is bigram_scale * W_lm[g(t)] + noise, with g(t) = (a*t + b) mod V
+// shared by both models, so both models lean towards g(x) and agree when the layer stack does
+// not override it.
+//
+// HBM layout (per engine):
+//   weights   : per model, one bf16 arena; per layer [wqkv | wo | wgu | wd] row-major
+//               (K-major for the swap-AB GEMM). wgu interleaves gate/up in 64-row groups.
+//   KV pages  : per model, [layer][page][kv_head][K|V][P=64][head_dim] bf16; a request's
+//               page table maps position -> page (shared across layers).
+//   rows      : ragged batch of the current forward (slot, position, token per row) +
+//               per-request (first row, n rows); n_rows lives in device memory so early-exit
+//               compaction can shrink it without a host round trip.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "faser/engine.h"
+
+namespace faser {
+
+constexpr int kPage = 64;  // tokens per KV page
+
+struct LlamaShape {
+  int d, layers, n_q, n_kv, hd, ffn, vocab;
+  float rope_theta, eps;
+  float bigram_scale, embed_noise, init_std;
+  uint64_t seed;
+  int qkv_out() const { return (n_q + 2 * n_kv) * hd; }
+};
+
+// Element generator shared with the oracle: Irwin-Hall(4) on 16-bit lanes of a SplitMix64
+// hash, scaled and rounded to bf16 (exact IEEE ops only, so CPU and GPU agree bit-for-bit).
+__host__ __device__ inline uint64_t lm_mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// Tensor tags (per model, per layer): tag = kind * 4096 + layer.
+enum : uint32_t { kTagLm = 1, kTagEmbNoise = 2, kTagQkv = 3, kTagO = 4, kTagGate = 5, kTagUp = 6, kTagDown = 7 };
+
+struct LayerW {
+  const __nv_bfloat16* wqkv;  // [qkv_out][d]
+  const __nv_bfloat16* wo;    // [d][n_q*hd]
+  const __nv_bfloat16* wgu;   // [2*ffn][d], 64-row groups: gate j0..j0+63, up j0..j0+63, ...
+  const __nv_bfloat16* wd;    // [d][ffn]
+};
+
+// Ragged batch of one forward pass (device arrays; capacity rows_cap / req_cap).
+struct RowsDev {
+  int* n_rows;     // [1] live rows (shrinks under early-exit compaction)
+  int* row_req;    // [rows] request index within this forward
+  int* row_pos;    // [rows] absolute position of the row's input token
+  int* row_tok;    // [rows] input token id
+  int* row_j;      // [rows] index of the row within its request (drafted position)
+  int* req_first;  // [reqs] first row (compacted order)
+  int* req_n;      // [reqs] rows of the request
+  int* req_slot;   // [reqs] engine slot (page table row)
+  int* req_pos0;   // [reqs] position of the request's first row
+};
+
+struct KvDev {
+  __nv_bfloat16* pool;  // [layers][pages][n_kv][2][kPage][hd]
+  const int* ptab;      // [slots][max_pages]
+  int max_pages;
+  int64_t layer_stride;  // elements per layer
+};
+
+// ------------------------------------------------------------------ launchers
+cudaError_t lm_init_matrix(__nv_bfloat16* w, int64_t n, uint64_t seed, uint32_t tag, float std,
+                           cudaStream_t s);
+// wgu in the interleaved order (gate rows tagged kTagGate, up rows kTagUp, both [ffn][d]).
+cudaError_t lm_init_gate_up(__nv_bfloat16* wgu, int ffn, int d, uint64_t seed, uint32_t tag_layer,
+                            float std, cudaStream_t s);
+// emb[t] = bf16(bigram_scale * lm[g(t)] + noise(t))
+cudaError_t lm_init_embedding(__nv_bfloat16* emb, const __nv_bfloat16* lm, const LlamaShape& m,
+                              uint32_t ga, uint32_t gb, cudaStream_t s);
+
+// x[r] = emb[row_tok[r]] (fp32 residual) and xn[r] = bf16(rmsnorm(x[r])) (gamma = 1).
+cudaError_t lm_embed_norm(const LlamaShape& m, const __nv_bfloat16* emb, RowsDev rows, int rows_cap,
+                          float* x, __nv_bfloat16* xn, cudaStream_t s);
+// qkv = sum of split partials; RoPE(q,k) at row_pos; q -> qbuf bf16 [rows][n_q*hd];
+// k,v appended to the paged cache of `layer`.
+cudaError_t lm_qkv_rope_append(const LlamaShape& m, const float* ws, int splits, int t_stride,
+                               RowsDev rows, int rows_cap, const float2* rope, KvDev kv, int layer,
+                               __nv_bfloat16* qbuf, cudaStream_t s);
+// Causal attention of every row over its request's paged KV (GQA packed, mma.sync bf16).
+cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req,
+                         int max_ctx, KvDev kv, int layer, const __nv_bfloat16* qbuf,
+                         __nv_bfloat16* obuf, float* scratch, size_t scratch_bytes, cudaStream_t s);
+// x += sum of split partials (fp32 residual), xn = bf16(rmsnorm(x)).
+cudaError_t lm_residual_norm(const LlamaShape& m, const float* ws, int splits, int t_stride,
+                             RowsDev rows, int rows_cap, float* x, __nv_bfloat16* xn, cudaStream_t s);
+// h = bf16(silu(gate) * up) from the interleaved gate/up partials.
+cudaError_t lm_swiglu(const LlamaShape& m, const float* ws, int splits, int t_stride, RowsDev rows,
+                      int rows_cap, __nv_bfloat16* h, cudaStream_t s);
+// logits[r][v] = sum of split partials (in place into split 0), argmax (lowest id on ties).
+cudaError_t lm_logits_argmax(int vocab, float* ws, int splits, int t_stride, RowsDev rows,
+                             int rows_cap, int* argmax_out, cudaStream_t s);
+
+}  // namespace faser

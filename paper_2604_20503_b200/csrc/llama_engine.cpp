@@ -1,0 +1,1000 @@
+// llama_engine.cpp — host engine of the Llama-style speculative-decoding path (configs 3-5).
+//
+// Replaces the reference's SpeculativeEngine + Request loop (sdcore.hpp:39-116, driven by the
+// missing serving loop SPEC.md:541-563) for transformer draft/target pairs:
+//   submit()  -> pending queue; admitted at the next step (iteration-boundary admission,
+//                B_max slots), prompt copied to HBM, both models prefilled (rows 0..len-2).
+//   step()    -> ragged draft loop (step t runs the requests with min(k_i, remaining) > t,
+//                one tcgen05 forward per step, sorted by k' so step t's rows are a prefix),
+//                one verify forward over sum(k') rows with per-layer early-exit compaction,
+//                fused accept + commit, ONE D2H of the round results, page release past the
+//                committed length (KV rollback).
+// Device memory: both models' weights (bf16), one page pool per model sharing one page table
+// (draft and target cache the same positions), activations sized for max_batch x max_spec.
+// Every failing CUDA call surfaces as FASER_ECUDA; there is no CPU fallback.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "faser/engine.h"
+#include "llama.cuh"
+#include "llama_engine.cuh"
+#include "llama_step.cuh"
+#include "tc_gemm.cuh"
+
+namespace faser {
+namespace {
+
+struct LFail {
+  faser_status st;
+  std::string msg;
+};
+
+#define LCK(call)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw LFail{FASER_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};      \
+  } while (0)
+
+struct Mem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  Mem() = default;
+  Mem(const Mem&) = delete;
+  Mem& operator=(const Mem&) = delete;
+  ~Mem() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b) {
+    bytes = b;
+    LCK(cudaMalloc(&p, b ? b : 16));
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+LlamaShape shape_of(const faser_llama_shape& s) {
+  LlamaShape m{};
+  m.d = s.d_model;
+  m.layers = s.layers;
+  m.n_q = s.n_heads;
+  m.n_kv = s.n_kv_heads;
+  m.hd = s.head_dim;
+  m.ffn = s.ffn;
+  m.vocab = s.vocab;
+  m.rope_theta = static_cast<float>(s.rope_theta);
+  m.eps = static_cast<float>(s.rms_eps);
+  m.bigram_scale = static_cast<float>(s.bigram_scale);
+  m.embed_noise = static_cast<float>(s.embed_noise);
+  m.init_std = static_cast<float>(s.init_std);
+  m.seed = s.seed;
+  return m;
+}
+
+void validate_shape(const faser_llama_shape& s, const char* which) {
+  auto bad = [&](const char* why) { throw LFail{FASER_EINVAL, std::string(which) + ": " + why}; };
+  if (s.d_model <= 0 || s.d_model % 128) bad("d_model must be a positive multiple of 128");
+  if (s.layers < 1 || s.layers > FASER_MAX_LAYERS) bad("layers out of range");
+  if (s.head_dim != 64 && s.head_dim != 128) bad("head_dim must be 64 or 128");
+  if (s.n_heads < 1 || s.n_kv_heads < 1 || s.n_heads % s.n_kv_heads) bad("n_heads must be a multiple of n_kv_heads");
+  if ((s.n_heads + 2 * s.n_kv_heads) * s.head_dim % 128) bad("qkv width must be a multiple of 128");
+  if ((s.n_heads * s.head_dim) % 128) bad("n_heads*head_dim must be a multiple of 128");
+  if (s.ffn <= 0 || s.ffn % 64) bad("ffn must be a positive multiple of 64");
+  if (s.vocab < 2 || s.vocab % 128) bad("vocab must be a multiple of 128");
+  if (!(s.rms_eps > 0) || !(s.rope_theta > 0) || !(s.init_std > 0)) bad("eps/theta/std must be > 0");
+}
+
+// ------------------------------------------------------------------ one model on device
+struct LmModel {
+  LlamaShape sh{};
+  Mem arena;
+  __nv_bfloat16* lm = nullptr;
+  __nv_bfloat16* emb = nullptr;
+  std::vector<LayerW> lw;
+  GemmOperand op_lm;
+  std::vector<GemmOperand> op_qkv, op_o, op_gu, op_d;
+  Mem kv;
+  int64_t kv_layer_stride = 0;
+  Mem rope;  // float2 [max_pos][hd/2]
+
+  void build(const LlamaShape& s, uint32_t ga, uint32_t gb, int n_pages, int max_pos, cudaStream_t st) {
+    sh = s;
+    const int64_t d = s.d, qkv = s.qkv_out(), qd = static_cast<int64_t>(s.n_q) * s.hd, F = s.ffn, V = s.vocab;
+    const int64_t per_layer = qkv * d + d * qd + 2 * F * d + d * F;
+    const int64_t total = 2 * V * d + per_layer * s.layers;
+    arena.alloc(total * 2);
+    __nv_bfloat16* p = arena.as<__nv_bfloat16>();
+    lm = p;
+    emb = p + V * d;
+    p += 2 * V * d;
+    LCK(lm_init_matrix(lm, V * d, s.seed, kTagLm * 4096u, s.init_std, st));
+    LCK(lm_init_embedding(emb, lm, s, ga, gb, st));
+    for (int l = 0; l < s.layers; ++l) {
+      LayerW w;
+      __nv_bfloat16* wqkv = p;
+      p += qkv * d;
+      __nv_bfloat16* wo = p;
+      p += d * qd;
+      __nv_bfloat16* wgu = p;
+      p += 2 * F * d;
+      __nv_bfloat16* wd = p;
+      p += d * F;
+      LCK(lm_init_matrix(wqkv, qkv * d, s.seed, kTagQkv * 4096u + l, s.init_std, st));
+      LCK(lm_init_matrix(wo, d * qd, s.seed, kTagO * 4096u + l, s.init_std, st));
+      LCK(lm_init_gate_up(wgu, s.ffn, s.d, s.seed, l, s.init_std, st));
+      LCK(lm_init_matrix(wd, d * F, s.seed, kTagDown * 4096u + l, s.init_std, st));
+      w.wqkv = wqkv;
+      w.wo = wo;
+      w.wgu = wgu;
+      w.wd = wd;
+      lw.push_back(w);
+      GemmOperand a, b, c, e;
+      LCK(make_weight_operand(&a, wqkv, static_cast<int>(qkv), s.d));
+      LCK(make_weight_operand(&b, wo, s.d, static_cast<int>(qd)));
+      LCK(make_weight_operand(&c, wgu, 2 * s.ffn, s.d));
+      LCK(make_weight_operand(&e, wd, s.d, s.ffn));
+      op_qkv.push_back(a);
+      op_o.push_back(b);
+      op_gu.push_back(c);
+      op_d.push_back(e);
+    }
+    LCK(make_weight_operand(&op_lm, lm, s.vocab, s.d));
+    kv_layer_stride = static_cast<int64_t>(n_pages) * s.n_kv * 2 * kPage * s.hd;
+    kv.alloc(static_cast<size_t>(kv_layer_stride) * s.layers * 2);
+    LCK(cudaMemsetAsync(kv.p, 0, kv.bytes, st));  // stale pages must be finite (masked P*V)
+    // RoPE table (rotate-half), computed in double on the host; the oracle uses the same formula.
+    const int half = s.hd / 2;
+    std::vector<float> tab(static_cast<size_t>(max_pos) * half * 2);
+    for (int pos = 0; pos < max_pos; ++pos)
+      for (int i = 0; i < half; ++i) {
+        const double inv = 1.0 / std::pow(static_cast<double>(s.rope_theta), (2.0 * i) / s.hd);
+        const double a = pos * inv;
+        tab[(static_cast<size_t>(pos) * half + i) * 2] = static_cast<float>(std::cos(a));
+        tab[(static_cast<size_t>(pos) * half + i) * 2 + 1] = static_cast<float>(std::sin(a));
+      }
+    rope.alloc(tab.size() * 4);
+    LCK(cudaMemcpyAsync(rope.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st));
+    LCK(cudaStreamSynchronize(st));  // tab is a host temporary
+  }
+  KvDev kvdev(const int* ptab, int max_pages) const {
+    KvDev k;
+    k.pool = kv.as<__nv_bfloat16>();
+    k.ptab = ptab;
+    k.max_pages = max_pages;
+    k.layer_stride = kv_layer_stride;
+    return k;
+  }
+};
+
+// ------------------------------------------------------------------ activations of one model
+struct LmWork {
+  int rows_cap = 0;
+  Mem x, xs, xn, q, h, ws, attn, argmax, src_of;
+  size_t ws_floats = 0, attn_bytes = 0;
+  GemmOperand op_xn, op_attn, op_h;
+  // persistent row metadata (draft steps, prefill)
+  Mem meta;
+  RowsDev rows{};
+
+  void build(const LlamaShape& s, int cap, int lm_rows_cap) {
+    rows_cap = cap;
+    const int64_t d = s.d, qd = static_cast<int64_t>(s.n_q) * s.hd;
+    const int64_t xw = std::max(d, qd);
+    x.alloc(static_cast<size_t>(cap) * d * 4);
+    xs.alloc(static_cast<size_t>(cap) * d * 4);
+    xn.alloc(static_cast<size_t>(cap) * xw * 2);
+    q.alloc(static_cast<size_t>(cap) * qd * 2);
+    h.alloc(static_cast<size_t>(cap) * s.ffn * 2);
+    const int64_t nmax = std::max<int64_t>({static_cast<int64_t>(s.qkv_out()), 2ll * s.ffn, d});
+    ws_floats = std::max<size_t>(static_cast<size_t>(cap) * nmax, static_cast<size_t>(lm_rows_cap) * s.vocab);
+    ws_floats = std::max<size_t>(ws_floats, static_cast<size_t>(8) << 20);  // split-K partials
+    ws.alloc(ws_floats * 4);
+    attn_bytes = static_cast<size_t>(64) << 20;
+    attn.alloc(attn_bytes);
+    argmax.alloc(static_cast<size_t>(cap) * 4);
+    src_of.alloc(static_cast<size_t>(cap) * 4);
+    LCK(make_act_operand(&op_xn, xn.p, cap, s.d));
+    LCK(make_act_operand(&op_attn, xn.p, cap, static_cast<int>(qd)));
+    LCK(make_act_operand(&op_h, h.p, cap, s.ffn));
+    meta.alloc(static_cast<size_t>(cap) * 9 * 4 + 64);
+    int* m = meta.as<int>();
+    rows.n_rows = m;
+    m += 16;
+    rows.row_req = m;
+    m += cap;
+    rows.row_pos = m;
+    m += cap;
+    rows.row_tok = m;
+    m += cap;
+    rows.row_j = m;
+    m += cap;
+    rows.req_first = m;
+    m += cap;
+    rows.req_n = m;
+    m += cap;
+    rows.req_slot = m;
+    m += cap;
+    rows.req_pos0 = m;
+  }
+};
+
+int num_sms_dev() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ the engine
+class LlamaEngine {
+ public:
+  faser_engine_cfg cfg{};
+  faser_model_desc desc{};
+  LlamaShape dsh{}, tsh{};
+  LmModel draft, target;
+  LmWork wd, wt;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  int nsm = 148;
+  int max_spec = 16;
+  int max_seq = 0;    // slot row capacity (tokens)
+  int max_pages = 0;  // pages per slot
+  int n_pages = 0;
+  int eos = 0;
+  std::string err;
+  int64_t launches = 0, h2d = 0, d2h = 0;
+  float t_draft = 0.f, t_verify = 0.f, t_step = 0.f;
+
+  // slots
+  Mem s_tok, s_len, s_ncomm, s_maxout, s_done, s_exempt, ptab;
+  LmSlots sl{};
+  // per-request step state (sorted order), persistent
+  Mem r_drafted, r_count, r_active, r_gl, r_npl, r_pl, r_prl, r_pr, r_fail, r_truth;
+  LmReqState rq{};
+  LmReqState cur_q{};  // rq + this step's per-request arrays (slot, k, ...) in the blob
+  // step blob
+  Mem d_blob;
+  char* h_blob = nullptr;
+  size_t blob_cap = 0;
+  faser_round_result* h_res = nullptr;
+  Mem d_res;
+
+  struct Req {
+    int64_t id;
+    std::vector<int32_t> prompt, committed;
+    int32_t max_out = 0, spec = 0, slot = -1, len = 0;
+    bool done = false, admitted = false;
+    std::vector<int32_t> pages;
+  };
+  std::unordered_map<int64_t, Req> reqs;
+  std::deque<int64_t> pending;
+  std::vector<int64_t> live;
+  std::vector<int32_t> free_slots;
+  std::set<int32_t> free_pages;  // deterministic: lowest page id first
+
+  // debug capture
+  struct Stage {
+    int rows = 0;
+    std::vector<float> logits;
+    std::vector<int64_t> ids;
+  };
+  std::map<int, Stage> stages;
+  std::vector<int32_t> dbg_drafted;  // live order [n][MAX_SPEC]
+  std::vector<int64_t> step_sorted_ids;
+
+  ~LlamaEngine() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& kv : reqs) (void)kv;
+    if (h_blob) cudaFreeHost(h_blob);
+    if (h_res) cudaFreeHost(h_res);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void create(const faser_model_desc* m, const faser_engine_cfg* c) {
+    cfg = *c;
+    desc = *m;
+    validate_shape(m->draft, "draft");
+    validate_shape(m->target, "target");
+    if (m->draft.vocab != m->target.vocab) throw LFail{FASER_EINVAL, "draft and target vocab differ"};
+    if (cfg.max_batch < 1 || cfg.max_batch > 1024) throw LFail{FASER_EINVAL, "max_batch out of range [1, 1024]"};
+    if (cfg.max_seq_len < 2) throw LFail{FASER_EINVAL, "max_seq_len must be >= 2"};
+    if (cfg.mode < FASER_MODE_VSD || cfg.mode > FASER_MODE_FULL) throw LFail{FASER_EINVAL, "unknown mode"};
+    const faser_exit_policy& p = cfg.exit_policy;
+    if (p.k_init < 1 || p.k_final < 1 || p.k_final > p.k_init)
+      throw LFail{FASER_EINVAL, "exit policy thresholds must satisfy k_init >= k_final >= 1"};
+    max_spec = cfg.max_spec_length > 0 ? cfg.max_spec_length : 16;
+    if (max_spec > FASER_MAX_SPEC) throw LFail{FASER_EINVAL, "max_spec_length > FASER_MAX_SPEC"};
+    if (cfg.default_spec_length < 1 || cfg.default_spec_length > max_spec)
+      throw LFail{FASER_EINVAL, "default_spec_length out of range"};
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw LFail{FASER_ECUDA, "no CUDA device available"};
+    if (cfg.device < 0 || cfg.device >= ndev) throw LFail{FASER_EINVAL, "device index out of range"};
+    LCK(cudaSetDevice(cfg.device));
+    nsm = num_sms_dev();
+    dsh = shape_of(m->draft);
+    tsh = shape_of(m->target);
+    eos = tsh.vocab - 1;
+    LCK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    for (auto& e : ev) LCK(cudaEventCreate(&e));
+    max_seq = cfg.max_seq_len + max_spec + 2;
+    max_pages = (max_seq + kPage - 1) / kPage;
+    n_pages = cfg.max_batch * max_pages;
+    const int B = cfg.max_batch;
+    const int prefill_rows = cfg.prefill_rows > 0 ? cfg.prefill_rows : 8192;
+    const int verify_rows = B * max_spec;
+    const int cap = std::max({prefill_rows, verify_rows, cfg.max_seq_len});
+    draft.build(dsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream);
+    target.build(tsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream);
+    wd.build(dsh, cap, B);
+    wt.build(tsh, cap, verify_rows);
+    s_tok.alloc(static_cast<size_t>(B) * max_seq * 4);
+    s_len.alloc(B * 4);
+    s_ncomm.alloc(B * 4);
+    s_maxout.alloc(B * 4);
+    s_done.alloc(B * 4);
+    s_exempt.alloc(B * 4);
+    ptab.alloc(static_cast<size_t>(B) * max_pages * 4);
+    LCK(cudaMemsetAsync(ptab.p, 0, ptab.bytes, stream));
+    sl.tok = s_tok.as<int32_t>();
+    sl.len = s_len.as<int32_t>();
+    sl.ncomm = s_ncomm.as<int32_t>();
+    sl.max_out = s_maxout.as<int32_t>();
+    sl.done = s_done.as<int32_t>();
+    sl.exempt = s_exempt.as<int32_t>();
+    sl.max_seq = max_seq;
+    r_drafted.alloc(static_cast<size_t>(B) * FASER_MAX_SPEC * 4);
+    r_count.alloc(B * 4);
+    r_active.alloc(B * 4);
+    r_gl.alloc(B * 4);
+    r_npl.alloc(B * 4);
+    r_pl.alloc(static_cast<size_t>(B) * FASER_MAX_SPEC * 4);
+    r_prl.alloc(static_cast<size_t>(B) * FASER_MAX_SPEC * 4);
+    r_pr.alloc(B * 8);
+    r_fail.alloc(B * 4);
+    r_truth.alloc(static_cast<size_t>(cap) * 4);
+    rq.drafted = r_drafted.as<int32_t>();
+    rq.count = r_count.as<int32_t>();
+    rq.active = r_active.as<int32_t>();
+    rq.gate_layers = r_gl.as<int32_t>();
+    rq.n_pl = r_npl.as<int32_t>();
+    rq.pl = r_pl.as<int32_t>();
+    rq.prune_layer = r_prl.as<int32_t>();
+    rq.pr = r_pr.as<int32_t>();
+    rq.failmask = r_fail.as<uint32_t>();
+    rq.truth = r_truth.as<int32_t>();
+    // blob: request arrays (5n) + verify rows (4T + 4n + 16) + ptab triples + admits + prefill rows
+    blob_cap = static_cast<size_t>(B) * 64 + static_cast<size_t>(verify_rows) * 16 +
+               static_cast<size_t>(B) * max_pages * 12 + static_cast<size_t>(B) * sizeof(LmAdmit) +
+               static_cast<size_t>(cap) * 16 + static_cast<size_t>(B) * 16 * 2 + 4096 +
+               static_cast<size_t>(B) * cfg.max_seq_len * (4 + 16) +   // prompts + prefill rows
+               static_cast<size_t>(B) * (9 * 4 + 64);                   // per-chunk arrays
+    LCK(cudaMallocHost(reinterpret_cast<void**>(&h_blob), blob_cap));
+    d_blob.alloc(blob_cap);
+    LCK(cudaMallocHost(reinterpret_cast<void**>(&h_res), sizeof(faser_round_result) * B));
+    d_res.alloc(sizeof(faser_round_result) * B);
+    for (int s = B - 1; s >= 0; --s) free_slots.push_back(s);
+    for (int p = 0; p < n_pages; ++p) free_pages.insert(p);
+    LCK(cudaStreamSynchronize(stream));
+  }
+
+  // ---------------------------------------------------------------- forward
+  struct Fwd {
+    RowsDev rows;
+    int T = 0, n_req = 0, max_rows = 0, max_ctx = 0;
+    bool logits = false;
+    int* argmax_out = nullptr;
+    bool ee = false;
+    int gate_lo = 0, gate_hi = 0;
+    const int* k_table = nullptr;
+    bool capture = false;
+  };
+
+  int splits(int n_out, int T, int k) const { return gemm_splits_for(n_out, T, k, nsm); }
+
+  void capture_stage(int stage, const LmModel& m, const LmWork& w, const Fwd& f, int spl) {
+    LCK(cudaStreamSynchronize(stream));
+    int n = 0;
+    LCK(cudaMemcpy(&n, f.rows.n_rows, 4, cudaMemcpyDeviceToHost));
+    const int V = m.sh.vocab;
+    Stage st;
+    st.rows = n;
+    std::vector<float> part(static_cast<size_t>(n) * V);
+    st.logits.assign(static_cast<size_t>(n) * V, 0.f);
+    for (int z = 0; z < (stage == 0 ? 1 : spl); ++z) {  // stage 0 is already reduced into split 0
+      LCK(cudaMemcpy(part.data(), w.ws.as<float>() + static_cast<size_t>(z) * f.T * V,
+                     part.size() * 4, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < part.size(); ++i) st.logits[i] += part[i];
+    }
+    std::vector<int> req(n), jj(n);
+    LCK(cudaMemcpy(req.data(), f.rows.row_req, 4 * n, cudaMemcpyDeviceToHost));
+    LCK(cudaMemcpy(jj.data(), f.rows.row_j, 4 * n, cudaMemcpyDeviceToHost));
+    st.ids.resize(2 * static_cast<size_t>(n));
+    for (int r = 0; r < n; ++r) {
+      st.ids[2 * r] = step_sorted_ids[req[r]];
+      st.ids[2 * r + 1] = jj[r];
+    }
+    stages[stage] = std::move(st);
+  }
+
+  void forward(LmModel& m, LmWork& w, const Fwd& f) {
+    const LlamaShape& s = m.sh;
+    const int T = f.T;
+    if (T <= 0) return;
+    const KvDev kv = m.kvdev(ptab.as<int>(), max_pages);
+    const int qd = s.n_q * s.hd;
+    const int s_qkv = splits(s.qkv_out(), T, s.d), s_o = splits(s.d, T, qd);
+    const int s_gu = splits(2 * s.ffn, T, s.d), s_d = splits(s.d, T, s.ffn), s_lm = splits(s.vocab, T, s.d);
+    const int z_qkv = gemm_effective_splits(s.d, s_qkv), z_o = gemm_effective_splits(qd, s_o);
+    const int z_gu = gemm_effective_splits(s.d, s_gu), z_d = gemm_effective_splits(s.ffn, s_d);
+    const int z_lm = gemm_effective_splits(s.d, s_lm);
+    float* ws = w.ws.as<float>();
+    const size_t need = std::max<size_t>({static_cast<size_t>(z_qkv) * T * s.qkv_out(), static_cast<size_t>(z_o) * T * s.d,
+                                          static_cast<size_t>(z_gu) * T * 2 * s.ffn, static_cast<size_t>(z_d) * T * s.d,
+                                          f.logits || f.ee ? static_cast<size_t>(z_lm) * T * s.vocab : 0});
+    if (need > w.ws_floats) throw LFail{FASER_ECAPACITY, "GEMM workspace too small for this batch"};
+    RowsDev rows = f.rows;
+    const int* nd = rows.n_rows;
+    LCK(lm_embed_norm(s, m.emb, rows, T, w.x.as<float>(), w.xn.as<__nv_bfloat16>(), stream));
+    ++launches;
+    for (int l = 0; l < s.layers; ++l) {
+      LCK(gemm_tn(m.op_qkv[l], w.op_xn, ws, T, nd, T, s_qkv, stream));
+      LCK(lm_qkv_rope_append(s, ws, z_qkv, T, rows, T, m.rope.as<float2>(), kv, l, w.q.as<__nv_bfloat16>(), stream));
+      LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
+                       w.xn.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, stream));
+      LCK(gemm_tn(m.op_o[l], w.op_attn, ws, T, nd, T, s_o, stream));
+      LCK(lm_residual_norm(s, ws, z_o, T, rows, T, w.x.as<float>(), w.xn.as<__nv_bfloat16>(), stream));
+      LCK(gemm_tn(m.op_gu[l], w.op_xn, ws, T, nd, T, s_gu, stream));
+      LCK(lm_swiglu(s, ws, z_gu, T, rows, T, w.h.as<__nv_bfloat16>(), stream));
+      LCK(gemm_tn(m.op_d[l], w.op_h, ws, T, nd, T, s_d, stream));
+      LCK(lm_residual_norm(s, ws, z_d, T, rows, T, w.x.as<float>(), w.xn.as<__nv_bfloat16>(), stream));
+      launches += 9;
+      const int layer = l + 1;  // residual now holds the output of `layer` layers
+      if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
+        LCK(gemm_tn(m.op_lm, w.op_xn, ws, T, nd, T, s_lm, stream));
+        if (f.capture) capture_stage(layer, m, w, f, z_lm);
+        LCK(lm_exit_test(sl, cur_q, rows, ws, z_lm, static_cast<int64_t>(T) * s.vocab, s.vocab, f.k_table[layer], T, stream));
+        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), stream));
+        LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, s.eps, w.x.as<float>(), w.xs.as<float>(),
+                           w.xn.as<__nv_bfloat16>(), T, stream));
+        launches += 5;
+      }
+    }
+    if (f.logits) {
+      LCK(gemm_tn(m.op_lm, w.op_xn, ws, T, nd, T, s_lm, stream));
+      LCK(lm_logits_argmax(s.vocab, ws, z_lm, T, rows, T, f.argmax_out, stream));
+      launches += 2;
+      if (f.capture) capture_stage(0, m, w, f, 1);
+    }
+  }
+
+  // ---------------------------------------------------------------- pages
+  void ensure_pages(Req& r, int upto_pos) {  // positions [0, upto_pos] backed
+    const int need = upto_pos / kPage + 1;
+    if (need > max_pages) throw LFail{FASER_ECAPACITY, "sequence exceeds page capacity"};
+    while (static_cast<int>(r.pages.size()) < need) {
+      if (free_pages.empty()) throw LFail{FASER_ENOMEM, "KV page pool exhausted"};
+      const int p = *free_pages.begin();
+      free_pages.erase(free_pages.begin());
+      pend_triples.push_back(r.slot);
+      pend_triples.push_back(static_cast<int>(r.pages.size()));
+      pend_triples.push_back(p);
+      r.pages.push_back(p);
+    }
+  }
+  void release_pages_beyond(Req& r, int keep_pages) {
+    while (static_cast<int>(r.pages.size()) > keep_pages) {
+      free_pages.insert(r.pages.back());
+      r.pages.pop_back();
+    }
+  }
+  std::vector<int> pend_triples;
+
+  void admit_pending() {
+    while (!pending.empty() && static_cast<int>(live.size()) < cfg.max_batch && !free_slots.empty()) {
+      const int64_t id = pending.front();
+      pending.pop_front();
+      Req& r = reqs.at(id);
+      r.slot = free_slots.back();
+      free_slots.pop_back();
+      live.push_back(id);
+    }
+  }
+
+  // ---------------------------------------------------------------- step
+  template <class T>
+  T* carve(size_t& off, size_t n) {
+    off = (off + 15) & ~size_t(15);
+    T* p = reinterpret_cast<T*>(h_blob + off);
+    off += sizeof(T) * n;
+    if (off > blob_cap) throw LFail{FASER_ECAPACITY, "step blob overflow"};
+    return p;
+  }
+  template <class T>
+  T* dev_of(const T* host) const {
+    return reinterpret_cast<T*>(d_blob.as<char>() + (reinterpret_cast<const char*>(host) - h_blob));
+  }
+
+  void step(const faser_step_plan* plan, faser_round_result* out, int cap, int* n_out) {
+    LCK(cudaSetDevice(cfg.device));
+    admit_pending();
+    const int n = static_cast<int>(live.size());
+    *n_out = n;
+    if (n == 0) return;
+    if (cap < n) throw LFail{FASER_ECAPACITY, "result capacity smaller than live batch"};
+    const int L = tsh.layers;
+    stages.clear();
+    pend_triples.clear();
+
+    // ---- admissions (prompt -> slot row) + prefill rows
+    struct Pre {
+      int req_idx;  // index into live
+      int rows;
+    };
+    std::vector<LmAdmit> admits;
+    std::vector<int64_t> newly;
+    for (int i = 0; i < n; ++i) {
+      Req& r = reqs.at(live[i]);
+      if (r.admitted) continue;
+      newly.push_back(r.id);
+    }
+    // ---- per request k' and ordering
+    struct Ent {
+      int live_idx, k;
+    };
+    std::vector<Ent> ents(n);
+    int kmax = 0, total = 0, maxctx = 0;
+    for (int i = 0; i < n; ++i) {
+      Req& r = reqs.at(live[i]);
+      const int remaining = r.max_out - static_cast<int>(r.committed.size());
+      int k = std::min(r.spec, remaining);
+      k = std::min(k, max_spec);
+      if (k < 1) throw LFail{FASER_EILLEGAL_STATE, "draft on a finished request"};
+      ents[i] = {i, k};
+    }
+    std::stable_sort(ents.begin(), ents.end(), [](const Ent& a, const Ent& b) { return a.k > b.k; });
+    for (int i = 0; i < n; ++i) {
+      Req& r = reqs.at(live[ents[i].live_idx]);
+      kmax = std::max(kmax, ents[i].k);
+      total += ents[i].k;
+      // draft & verify write positions len-1 .. len+k-2
+      ensure_pages(r, r.len + ents[i].k - 2);
+      maxctx = std::max(maxctx, r.len - 1 + ents[i].k);
+    }
+    if (total > wt.rows_cap) throw LFail{FASER_ECAPACITY, "verify rows exceed capacity"};
+
+    // ---- lay out the blob
+    size_t off = 0;
+    int32_t* b_slot = carve<int32_t>(off, n);
+    int32_t* b_k = carve<int32_t>(off, n);
+    int32_t* b_spec = carve<int32_t>(off, n);
+    int32_t* b_live = carve<int32_t>(off, n);
+    int64_t* b_id = carve<int64_t>(off, n);
+    int32_t* v_nrows = carve<int32_t>(off, 4);
+    int32_t* v_row_req = carve<int32_t>(off, total);
+    int32_t* v_row_pos = carve<int32_t>(off, total);
+    int32_t* v_row_tok = carve<int32_t>(off, total);
+    int32_t* v_row_j = carve<int32_t>(off, total);
+    int32_t* v_first = carve<int32_t>(off, n);
+    int32_t* v_n = carve<int32_t>(off, n);
+    int32_t* v_rslot = carve<int32_t>(off, n);
+    int32_t* v_pos0 = carve<int32_t>(off, n);
+    step_sorted_ids.resize(n);
+    {
+      int row = 0;
+      for (int i = 0; i < n; ++i) {
+        Req& r = reqs.at(live[ents[i].live_idx]);
+        b_slot[i] = r.slot;
+        b_k[i] = ents[i].k;
+        b_spec[i] = r.spec;
+        b_live[i] = ents[i].live_idx;
+        b_id[i] = r.id;
+        step_sorted_ids[i] = r.id;
+        v_first[i] = row;
+        v_n[i] = ents[i].k;
+        v_rslot[i] = r.slot;
+        v_pos0[i] = r.len - 1;
+        for (int j = 0; j < ents[i].k; ++j, ++row) {
+          v_row_req[row] = i;
+          v_row_pos[row] = r.len - 1 + j;
+          v_row_tok[row] = 0;
+          v_row_j[row] = j;
+        }
+      }
+      v_nrows[0] = total;
+    }
+    // admissions: slot row copy + page reservation for the prompt prefix
+    for (int64_t id : newly) {
+      Req& r = reqs.at(id);
+      if (r.len >= 2) ensure_pages(r, r.len - 2);
+    }
+    int32_t* b_tr = carve<int32_t>(off, pend_triples.size());
+    std::memcpy(b_tr, pend_triples.data(), pend_triples.size() * 4);
+    const int n_tr = static_cast<int>(pend_triples.size() / 3);
+    // prompts: staged in the blob itself
+    std::vector<std::pair<int32_t*, int64_t>> prompt_at;
+    for (int64_t id : newly) {
+      Req& r = reqs.at(id);
+      int32_t* pr = carve<int32_t>(off, r.prompt.size());
+      std::memcpy(pr, r.prompt.data(), r.prompt.size() * 4);
+      prompt_at.push_back({pr, id});
+    }
+    LmAdmit* b_adm = carve<LmAdmit>(off, newly.size());
+    for (size_t i = 0; i < newly.size(); ++i) {
+      Req& r = reqs.at(newly[i]);
+      b_adm[i].src = dev_of(prompt_at[i].first);
+      b_adm[i].slot = r.slot;
+      b_adm[i].len = static_cast<int>(r.prompt.size());
+      b_adm[i].max_out = r.max_out;
+      b_adm[i].reserved = 0;
+    }
+    // prefill chunks (rows = prompt positions 0..len-2 of newly admitted requests)
+    struct Chunk {
+      int32_t *nrows, *row_req, *row_pos, *row_tok, *row_j, *first, *nn, *rslot, *pos0;
+      int T, nreq, maxrows, maxctx;
+    };
+    std::vector<Chunk> chunks;
+    {
+      const int cap_rows = std::min(wt.rows_cap, wd.rows_cap);
+      size_t i = 0;
+      while (i < newly.size()) {
+        std::vector<int64_t> grp;
+        int rows = 0;
+        while (i < newly.size()) {
+          const int rr = reqs.at(newly[i]).len - 1;
+          if (rr <= 0) {
+            ++i;
+            continue;
+          }
+          if (rows + rr > cap_rows && !grp.empty()) break;
+          grp.push_back(newly[i]);
+          rows += rr;
+          ++i;
+        }
+        if (grp.empty()) continue;
+        Chunk c;
+        c.T = rows;
+        c.nreq = static_cast<int>(grp.size());
+        c.nrows = carve<int32_t>(off, 4);
+        c.row_req = carve<int32_t>(off, rows);
+        c.row_pos = carve<int32_t>(off, rows);
+        c.row_tok = carve<int32_t>(off, rows);
+        c.row_j = carve<int32_t>(off, rows);
+        c.first = carve<int32_t>(off, grp.size());
+        c.nn = carve<int32_t>(off, grp.size());
+        c.rslot = carve<int32_t>(off, grp.size());
+        c.pos0 = carve<int32_t>(off, grp.size());
+        c.maxrows = 0;
+        c.maxctx = 0;
+        int row = 0;
+        for (size_t g = 0; g < grp.size(); ++g) {
+          Req& r = reqs.at(grp[g]);
+          const int rr = r.len - 1;
+          c.first[g] = row;
+          c.nn[g] = rr;
+          c.rslot[g] = r.slot;
+          c.pos0[g] = 0;
+          c.maxrows = std::max(c.maxrows, rr);
+          c.maxctx = std::max(c.maxctx, rr);
+          for (int j = 0; j < rr; ++j, ++row) {
+            c.row_req[row] = static_cast<int>(g);
+            c.row_pos[row] = j;
+            c.row_tok[row] = 0;
+            c.row_j[row] = j;
+          }
+        }
+        c.nrows[0] = rows;
+        chunks.push_back(c);
+      }
+    }
+    const size_t blob_bytes = off;
+    LCK(cudaMemcpyAsync(d_blob.p, h_blob, blob_bytes, cudaMemcpyHostToDevice, stream));
+    h2d = static_cast<int64_t>(blob_bytes);
+    d2h = static_cast<int64_t>(sizeof(faser_round_result)) * n;
+
+    LmReqState q = rq;
+    q.slot = dev_of(b_slot);
+    q.k = dev_of(b_k);
+    q.spec = dev_of(b_spec);
+    q.live_idx = dev_of(b_live);
+    q.req_id = dev_of(b_id);
+    cur_q = q;
+    RowsDev vrows;
+    vrows.n_rows = dev_of(v_nrows);
+    vrows.row_req = dev_of(v_row_req);
+    vrows.row_pos = dev_of(v_row_pos);
+    vrows.row_tok = dev_of(v_row_tok);
+    vrows.row_j = dev_of(v_row_j);
+    vrows.req_first = dev_of(v_first);
+    vrows.req_n = dev_of(v_n);
+    vrows.req_slot = dev_of(v_rslot);
+    vrows.req_pos0 = dev_of(v_pos0);
+
+    LCK(cudaEventRecord(ev[0], stream));
+    LCK(lm_ptab_scatter(ptab.as<int>(), max_pages, dev_of(b_tr), n_tr, stream));
+    LCK(lm_admit(sl, dev_of(b_adm), static_cast<int>(newly.size()), stream));
+    launches += (n_tr > 0) + (!newly.empty());
+    for (const Chunk& c : chunks) {
+      RowsDev pr;
+      pr.n_rows = dev_of(c.nrows);
+      pr.row_req = dev_of(c.row_req);
+      pr.row_pos = dev_of(c.row_pos);
+      pr.row_tok = dev_of(c.row_tok);
+      pr.row_j = dev_of(c.row_j);
+      pr.req_first = dev_of(c.first);
+      pr.req_n = dev_of(c.nn);
+      pr.req_slot = dev_of(c.rslot);
+      pr.req_pos0 = dev_of(c.pos0);
+      LCK(lm_prefill_tokens(sl, pr, c.T, stream));
+      ++launches;
+      Fwd f;
+      f.rows = pr;
+      f.T = c.T;
+      f.n_req = c.nreq;
+      f.max_rows = c.maxrows;
+      f.max_ctx = c.maxctx;
+      forward(draft, wd, f);
+      forward(target, wt, f);
+    }
+    // ---- draft loop
+    const bool capture = cfg.debug_capture != 0;
+    for (int t = 0; t < kmax; ++t) {
+      int nt = 0;
+      while (nt < n && ents[nt].k > t) ++nt;
+      LCK(lm_draft_prep(sl, q, wd.rows, nt, t, stream));
+      Fwd f;
+      f.rows = wd.rows;
+      f.T = nt;
+      f.n_req = nt;
+      f.max_rows = 1;
+      f.max_ctx = maxctx;
+      f.logits = true;
+      f.argmax_out = wd.argmax.as<int>();
+      forward(draft, wd, f);
+      LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, stream));
+      launches += 2;
+    }
+    LCK(cudaEventRecord(ev[1], stream));
+    // ---- verify (+ early exit) + accept/commit
+    const bool ee = cfg.mode >= FASER_MODE_VSD_AD_EE;
+    int k_table[FASER_MAX_LAYERS + 1];
+    int glo = 0, ghi = 0;
+    if (ee) {
+      faser_gate_plan g{cfg.exit_policy.l_init, cfg.exit_policy.l_init, 1.0};
+      if (plan) g = plan->gate;
+      glo = std::max(g.first_layer, 1);
+      ghi = std::min(g.stop_layer, L);
+      if (!(g.first_layer < g.stop_layer)) glo = ghi = 0;
+      if (plan && plan->use_k_table) {
+        for (int l = 0; l <= L; ++l) {
+          if (plan->k_table[l] < 1) throw LFail{FASER_EINVAL, "k must be >= 1"};
+          k_table[l] = plan->k_table[l];
+        }
+      } else if (faser_k_table(&cfg.exit_policy, L, k_table) != FASER_OK) {
+        throw LFail{FASER_EINVAL, "invalid exit policy"};
+      }
+    }
+    LCK(lm_verify_prep(sl, q, vrows, n, L, eos, total, stream));
+    {
+      Fwd f;
+      f.rows = vrows;
+      f.T = total;
+      f.n_req = n;
+      f.max_rows = kmax;
+      f.max_ctx = maxctx;
+      f.logits = true;
+      f.argmax_out = rq.truth;
+      f.ee = ee;
+      f.gate_lo = glo;
+      f.gate_hi = ghi;
+      f.k_table = k_table;
+      f.capture = capture;
+      forward(target, wt, f);
+    }
+    StepCtl ctl{n, L, eos, ee ? 1 : 0, cfg.exempt_rule};
+    LCK(lm_accept_commit(sl, q, vrows, ctl, d_res.as<faser_round_result>(), stream));
+    launches += 2;
+    LCK(cudaEventRecord(ev[2], stream));
+    LCK(cudaMemcpyAsync(h_res, d_res.p, sizeof(faser_round_result) * n, cudaMemcpyDeviceToHost, stream));
+    if (capture) {
+      std::vector<int32_t> dr(static_cast<size_t>(n) * FASER_MAX_SPEC);
+      LCK(cudaMemcpyAsync(dr.data(), rq.drafted, dr.size() * 4, cudaMemcpyDeviceToHost, stream));
+      LCK(cudaStreamSynchronize(stream));
+      dbg_drafted.assign(dr.size(), 0);
+      for (int i = 0; i < n; ++i)
+        std::memcpy(&dbg_drafted[static_cast<size_t>(ents[i].live_idx) * FASER_MAX_SPEC],
+                    &dr[static_cast<size_t>(i) * FASER_MAX_SPEC], FASER_MAX_SPEC * 4);
+    }
+    LCK(cudaStreamSynchronize(stream));
+    cudaEventElapsedTime(&t_draft, ev[0], ev[1]);
+    cudaEventElapsedTime(&t_verify, ev[1], ev[2]);
+    cudaEventElapsedTime(&t_step, ev[0], ev[2]);
+
+    // ---- host bookkeeping: commit mirror, page rollback, retire finished requests
+    for (int64_t id : newly) reqs.at(id).admitted = true;
+    std::vector<int64_t> keep;
+    keep.reserve(n);
+    for (int p = 0; p < n; ++p) {
+      const faser_round_result& rr = h_res[p];
+      Req& r = reqs.at(live[p]);
+      r.committed.insert(r.committed.end(), rr.tokens, rr.tokens + rr.committed);
+      r.len += rr.committed;
+      r.done = rr.done != 0;
+      if (r.done) {
+        release_pages_beyond(r, 0);
+        free_slots.push_back(r.slot);
+        r.slot = -1;
+      } else {
+        // the cache must hold positions [0, len-1): pages 0 .. (len-2)/64
+        release_pages_beyond(r, r.len >= 2 ? (r.len - 2) / kPage + 1 : 0);
+        keep.push_back(r.id);
+      }
+    }
+    std::memcpy(out, h_res, sizeof(faser_round_result) * n);
+    live.swap(keep);
+  }
+};
+
+// ------------------------------------------------------------------ C-side wrappers
+namespace {
+template <class F>
+faser_status lguard(LlamaEngine* e, F&& f) {
+  try {
+    f();
+    return FASER_OK;
+  } catch (const LFail& x) {
+    if (e) e->err = x.msg;
+    return x.st;
+  } catch (const std::bad_alloc&) {
+    if (e) e->err = "host allocation failed";
+    return FASER_ENOMEM;
+  }
+}
+thread_local std::string g_create_err;
+}  // namespace
+
+LlamaEngine* llama_engine_create(const faser_model_desc* model, const faser_engine_cfg* cfg,
+                                 faser_status* st, const char** msg) {
+  LlamaEngine* e = new LlamaEngine();
+  try {
+    e->create(model, cfg);
+    *st = FASER_OK;
+    return e;
+  } catch (const LFail& x) {
+    g_create_err = x.msg;
+    *st = x.st;
+  } catch (const std::bad_alloc&) {
+    g_create_err = "host allocation failed";
+    *st = FASER_ENOMEM;
+  }
+  *msg = g_create_err.c_str();
+  delete e;
+  return nullptr;
+}
+
+void llama_engine_destroy(LlamaEngine* e) { delete e; }
+const char* llama_last_error(const LlamaEngine* e) { return e->err.c_str(); }
+
+faser_status llama_submit(LlamaEngine* e, int64_t req_id, const int32_t* prompt, int32_t len, int32_t max_out) {
+  return lguard(e, [&] {
+    if (!prompt || len < 1) throw LFail{FASER_EINVAL, "prompt must be non-empty"};
+    if (max_out < 0) throw LFail{FASER_EINVAL, "max_out must be >= 0"};
+    if (e->reqs.count(req_id)) throw LFail{FASER_EINVAL, "duplicate request id"};
+    if (static_cast<int64_t>(len) + max_out > e->cfg.max_seq_len)
+      throw LFail{FASER_ECAPACITY, "prompt + max_out exceeds max_seq_len"};
+    for (int i = 0; i < len; ++i)
+      if (prompt[i] < 0 || prompt[i] >= e->tsh.vocab) throw LFail{FASER_EINVAL, "token outside vocabulary"};
+    LlamaEngine::Req r;
+    r.id = req_id;
+    r.prompt.assign(prompt, prompt + len);
+    r.max_out = max_out;
+    r.spec = e->cfg.default_spec_length;
+    r.len = len;
+    r.done = max_out == 0;
+    e->reqs.emplace(req_id, std::move(r));
+    if (max_out > 0) e->pending.push_back(req_id);
+  });
+}
+
+faser_status llama_set_spec_lengths(LlamaEngine* e, const int64_t* ids, const int32_t* k, int32_t n) {
+  return lguard(e, [&] {
+    for (int i = 0; i < n; ++i) {
+      if (k[i] < 1 || k[i] > e->max_spec) throw LFail{FASER_EINVAL, "speculative length must be in [1, max_spec_length]"};
+      auto it = e->reqs.find(ids[i]);
+      if (it == e->reqs.end()) throw LFail{FASER_EINVAL, "unknown request id"};
+      it->second.spec = k[i];
+    }
+  });
+}
+
+faser_status llama_live_requests(LlamaEngine* e, int64_t* ids, int32_t cap, int32_t* n) {
+  return lguard(e, [&] {
+    e->admit_pending();
+    *n = static_cast<int32_t>(e->live.size());
+    for (int i = 0; i < *n && i < cap; ++i) ids[i] = e->live[i];
+  });
+}
+
+faser_status llama_step(LlamaEngine* e, const faser_step_plan* plan, faser_round_result* out, int32_t cap,
+                        int32_t* n_out) {
+  return lguard(e, [&] { e->step(plan, out, cap, n_out); });
+}
+
+faser_status llama_get_committed(LlamaEngine* e, int64_t req_id, int32_t* buf, int32_t cap, int32_t* n) {
+  return lguard(e, [&] {
+    auto it = e->reqs.find(req_id);
+    if (it == e->reqs.end()) throw LFail{FASER_EINVAL, "unknown request id"};
+    const auto& c = it->second.committed;
+    *n = static_cast<int32_t>(c.size());
+    if (buf) std::memcpy(buf, c.data(), sizeof(int32_t) * std::min<size_t>(c.size(), std::max(cap, 0)));
+  });
+}
+
+faser_status llama_release(LlamaEngine* e, int64_t req_id) {
+  return lguard(e, [&] {
+    auto it = e->reqs.find(req_id);
+    if (it == e->reqs.end()) throw LFail{FASER_EINVAL, "unknown request id"};
+    if (!it->second.done) throw LFail{FASER_EILLEGAL_STATE, "release of a live request"};
+    e->reqs.erase(it);
+  });
+}
+
+int32_t llama_pending_work(const LlamaEngine* e) { return static_cast<int32_t>(e->live.size() + e->pending.size()); }
+void llama_last_step_timing(const LlamaEngine* e, float* d, float* v, float* s) {
+  if (d) *d = e->t_draft;
+  if (v) *v = e->t_verify;
+  if (s) *s = e->t_step;
+}
+void llama_last_step_bytes(const LlamaEngine* e, int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = e->h2d;
+  if (d2h) *d2h = e->d2h;
+}
+void* llama_stream(const LlamaEngine* e) { return e->stream; }
+int64_t llama_launches(const LlamaEngine* e) { return e->launches; }
+
+faser_status llama_debug_verify_logits(LlamaEngine* e, int32_t stage, float* logits, int64_t* row_ids,
+                                       int32_t cap_rows, int32_t* rows) {
+  return lguard(e, [&] {
+    auto it = e->stages.find(stage);
+    if (it == e->stages.end()) throw LFail{FASER_EINVAL, "stage not captured in the last step"};
+    const auto& st = it->second;
+    *rows = st.rows;
+    const int n = std::min(st.rows, cap_rows);
+    const size_t V = static_cast<size_t>(e->tsh.vocab);
+    if (logits) std::memcpy(logits, st.logits.data(), n * V * 4);
+    if (row_ids) std::memcpy(row_ids, st.ids.data(), static_cast<size_t>(n) * 2 * 8);
+  });
+}
+
+faser_status llama_debug_drafted(LlamaEngine* e, int32_t* drafted, int32_t cap, int32_t* n) {
+  return lguard(e, [&] {
+    const int m = static_cast<int>(e->dbg_drafted.size() / FASER_MAX_SPEC);
+    *n = m;
+    if (drafted) std::memcpy(drafted, e->dbg_drafted.data(), static_cast<size_t>(std::min(m, cap)) * FASER_MAX_SPEC * 4);
+  });
+}
+
+faser_status llama_debug_kv_pages(LlamaEngine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n) {
+  return lguard(e, [&] {
+    auto it = e->reqs.find(req_id);
+    if (it == e->reqs.end()) throw LFail{FASER_EINVAL, "unknown request id"};
+    const auto& p = it->second.pages;
+    *n = static_cast<int32_t>(p.size());
+    if (pages) std::memcpy(pages, p.data(), sizeof(int32_t) * std::min<size_t>(p.size(), std::max(cap, 0)));
+  });
+}
+
+}  // namespace faser

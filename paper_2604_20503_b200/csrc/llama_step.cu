@@ -1,0 +1,389 @@
+// llama_step.cu — control kernels of the Llama-style serving step.
+//
+//   draft prep/post      : SpeculativeEngine::draft_tokens (sdcore.cpp:45-59) as a ragged loop:
+//                          step t runs the requests whose budget min(k_i, remaining) > t.
+//   verify prep          : verify row i,j has input token ctx.back() (j = 0) or drafted[j-1]
+//                          and predicts drafted[j] (full_verify, sdcore.cpp:61-81).
+//   exit test (K4)       : token_exit_test (exitctl.cpp:56-68) on LM-head logits of the
+//                          intermediate residual: prune iff >= K(layer) ids outrank drafted[j]
+//                          (ties: lower id outranks), no Top-K materialisation.
+//   frontier (K4)        : verify_with_early_exit's per-layer scan (sdcore.cpp:111-132):
+//                          earliest failing j prunes rows j.. of that request; surviving rows are
+//                          compacted so the remaining layers' GEMM/attention tiles shrink.
+//   accept + commit (K5) : survivors exact (sdcore.cpp:134-148), force-verify of token 0
+//                          (:150-166), full_layers_run (:168-169), commit (:182-197), and the
+//                          exempt-position rule; KV "rollback" is the new context length (pages
+//                          past it are released by the host).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "llama_step.cuh"
+
+namespace faser {
+namespace {
+
+constexpr int kMS = FASER_MAX_SPEC;
+
+__global__ void draft_prep_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int t) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *rows.n_rows = n_t;
+  if (r >= n_t) return;
+  const int slot = rq.slot[r];
+  const int base = sl.len[slot] - 1;
+  const int pos = base + t;
+  rows.row_req[r] = r;
+  rows.row_pos[r] = pos;
+  rows.row_j[r] = t;
+  rows.req_first[r] = r;
+  rows.req_n[r] = 1;
+  rows.req_slot[r] = slot;
+  rows.req_pos0[r] = pos;
+  rows.row_tok[r] = t == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + base]
+                           : rq.drafted[r * kMS + t - 1];
+}
+
+__global__ void draft_post_kernel(LmReqState rq, const int* argmax, int n_t, int t) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n_t) rq.drafted[r * kMS + t] = argmax[r];
+}
+
+__global__ void verify_prep_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layers,
+                                   int eos) {
+  const int r = blockIdx.x;
+  if (r >= n) return;
+  const int slot = rq.slot[r];
+  const int k = rq.k[r];
+  const int first = rows.req_first[r];
+  const int base = sl.len[slot] - 1;
+  for (int j = threadIdx.x; j < k; j += blockDim.x)
+    rows.row_tok[first + j] = j == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + base]
+                                     : rq.drafted[r * kMS + j - 1];
+  for (int j = threadIdx.x; j < kMS; j += blockDim.x) rq.prune_layer[r * kMS + j] = layers;
+  if (threadIdx.x == 0) {
+    int count = k;
+    for (int j = 0; j < k; ++j)
+      if (rq.drafted[r * kMS + j] == eos) {  // draft_tokens stops at EOS (sdcore.cpp:56)
+        count = j + 1;
+        break;
+      }
+    rq.count[r] = count;
+    rq.active[r] = count;
+    rq.gate_layers[r] = 0;
+    rq.n_pl[r] = 0;
+    rq.pr[2 * r] = -1;
+    rq.pr[2 * r + 1] = -1;
+    rq.failmask[r] = 0u;
+  }
+}
+
+constexpr int kExitThreads = 256;
+
+__global__ void __launch_bounds__(kExitThreads) exit_test_kernel(LmSlots sl, LmReqState rq, RowsDev rows,
+                                                                 const float* __restrict__ logits, int splits,
+                                                                 int64_t split_stride, int vocab, int k_thr) {
+  __shared__ int red[kExitThreads / 32];
+  const int r = blockIdx.x;
+  if (r >= *rows.n_rows) return;
+  const int req = rows.row_req[r], j = rows.row_j[r];
+  if (j >= rq.active[req]) return;
+  const int slot = rq.slot[req];
+  if (sl.ncomm[slot] + j == sl.exempt[slot]) return;  // re-entry exemption (sdcore.cpp:118-119)
+  const int d = rq.drafted[req * kMS + j];
+  const float* z = logits + static_cast<int64_t>(r) * vocab;
+  float zd = z[d];
+  for (int s = 1; s < splits; ++s) zd += z[s * split_stride + d];
+  int cnt = 0;
+  for (int v = threadIdx.x; v < vocab; v += kExitThreads) {
+    float zv = z[v];
+    for (int s = 1; s < splits; ++s) zv += z[s * split_stride + v];
+    cnt += (zv > zd) || (zv == zd && v < d);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kExitThreads / 32; ++i) tot += red[i];
+    if (tot >= k_thr) atomicOr(&rq.failmask[req], 1u << j);
+  }
+}
+
+// One thread per request (n <= 1024), single CTA.
+__global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, int* src_of) {
+  __shared__ int scan[1024];
+  const int i = threadIdx.x;
+  int keep = 0, old_first = 0, pos0 = 0;
+  if (i < n) {
+    int act = rq.active[i];
+    old_first = rows.req_first[i];
+    pos0 = rows.req_pos0[i];
+    const int old_n = rows.req_n[i];
+    if (act > 0) {
+      rq.gate_layers[i] += 1;
+      const uint32_t live = act >= 32 ? 0xffffffffu : ((1u << act) - 1u);
+      const uint32_t f = rq.failmask[i] & live;
+      if (f) {
+        const int j = __ffs(f) - 1;
+        for (int jj = j; jj < act; ++jj) rq.prune_layer[i * kMS + jj] = layer;
+        act = j;
+        rq.active[i] = act;
+        rq.pr[2 * i] = j;
+        rq.pr[2 * i + 1] = layer;
+        rq.pl[i * kMS + rq.n_pl[i]] = layer;
+        rq.n_pl[i] += 1;
+      }
+    }
+    rq.failmask[i] = 0u;
+    keep = act > 1 ? act : 1;  // row 0 survives (force-verify, sdcore.cpp:150-166)
+    keep = keep < old_n ? keep : old_n;
+  }
+  scan[i] = keep;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    const int v = i >= off ? scan[i - off] : 0;
+    __syncthreads();
+    scan[i] += v;
+    __syncthreads();
+  }
+  const int nf = scan[i] - keep;  // exclusive prefix
+  if (i < n) {
+    rows.req_first[i] = nf;
+    rows.req_n[i] = keep;
+    for (int j = 0; j < keep; ++j) {
+      src_of[nf + j] = old_first + j;
+      rows.row_req[nf + j] = i;
+      rows.row_pos[nf + j] = pos0 + j;
+      rows.row_j[nf + j] = j;
+    }
+  }
+  if (i == blockDim.x - 1) *rows.n_rows = scan[i];
+}
+
+__global__ void gather_kernel(RowsDev rows, const int* __restrict__ src_of, int d, const float* __restrict__ x,
+                              float* __restrict__ xs) {
+  const int r = blockIdx.x;
+  if (r >= *rows.n_rows) return;
+  const float4* s = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src_of[r]) * d);
+  float4* o = reinterpret_cast<float4*>(xs + static_cast<int64_t>(r) * d);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) o[c] = s[c];
+}
+
+__global__ void scatter_back_norm_kernel(RowsDev rows, int d, float eps, const float* __restrict__ xs,
+                                         float* __restrict__ x, __nv_bfloat16* __restrict__ xn) {
+  __shared__ float red[8];
+  const int r = blockIdx.x;
+  if (r >= *rows.n_rows) return;
+  const float* s = xs + static_cast<int64_t>(r) * d;
+  float* o = x + static_cast<int64_t>(r) * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const float v = s[c];
+    o[c] = v;
+    ss += v * v;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += red[i];
+  const float inv = rsqrtf(tot / d + eps);
+  for (int c = threadIdx.x; c < d; c += blockDim.x)
+    xn[static_cast<int64_t>(r) * d + c] = __float2bfloat16_rn(s[c] * inv);
+}
+
+__global__ void accept_commit_kernel(LmSlots sl, LmReqState rq, RowsDev rows, StepCtl ctl,
+                                     faser_round_result* __restrict__ results) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= ctl.n) return;
+  const int slot = rq.slot[r];
+  const int count = rq.count[r];
+  const int L = ctl.layers;
+  const bool ee = ctl.early_exit != 0;
+  const int32_t* d = rq.drafted + r * kMS;
+  const int32_t* plr = rq.prune_layer + r * kMS;
+  const int first = rows.req_first[r];
+  const int32_t* truth = rq.truth + first;
+  int active = ee ? rq.active[r] : count;
+  int pr_j = rq.pr[2 * r], pr_l = rq.pr[2 * r + 1];
+  bool pruned = pr_j >= 0;
+  faser_round_result* rr = results + rq.live_idx[r];
+  faser_verify_outcome& o = rr->outcome;
+
+  int acc = 0, rec = -1;
+  bool mismatch = false;
+  for (int j = 0; j < active; ++j) {
+    if (d[j] == truth[j]) {
+      ++acc;
+    } else {
+      rec = truth[j];
+      mismatch = true;
+      break;
+    }
+  }
+  if (ee && active == 0) {  // progress guarantee: force-verify token 0
+    if (d[0] == truth[0]) {
+      acc = 1;
+    } else {
+      rec = truth[0];
+      mismatch = true;
+    }
+    if (count > 1) {
+      pr_j = 1;
+      pr_l = plr[1];
+    } else {
+      pruned = false;
+      pr_j = pr_l = -1;
+    }
+    active = 1;
+  }
+  double flr = 0.0;
+  if (ee) {
+    for (int j = 0; j < count; ++j) flr += (j < active) ? L : plr[j];
+  } else {
+    flr = static_cast<double>(L) * count;
+  }
+  o.submitted = count;
+  o.accepted_count = acc;
+  o.has_recovery = rec >= 0;
+  o.recovery_token = rec;
+  o.has_pruned = pruned;
+  o.pruned_index = pruned ? pr_j : -1;
+  o.pruned_layer = pruned ? pr_l : -1;
+  o.gate_layers = ee ? rq.gate_layers[r] : 0;
+  o.full_layers_run = flr;
+  // false_prune needs the full-depth argmax of the pruned row, which a pruned verify never
+  // computes (that is the saving); reported as -1 = "not evaluated" on this path.
+  o.false_prune = (pruned && !mismatch && acc == pr_j && pr_j < count) ? -1 : 0;
+  const int npl = ee ? rq.n_pl[r] : 0;
+  o.n_prune_layers = npl;
+  for (int i = 0; i < npl; ++i) o.prune_layers[i] = rq.pl[r * kMS + i];
+  const int base = sl.len[slot];
+  o.base_len = base;
+  rr->req_id = rq.req_id[r];
+  rr->spec_length = rq.spec[r];
+  rr->drafted = count;
+
+  // commit (sdcore.cpp:182-197)
+  const int ncomm0 = sl.ncomm[slot];
+  int done = sl.done[slot];
+  int nc = ncomm0, c = 0;
+  const int mo = sl.max_out[slot];
+  int32_t* out_row = sl.tok + static_cast<int64_t>(slot) * sl.max_seq + base;
+  for (int j = 0; j < acc && !done; ++j) {
+    out_row[c] = d[j];
+    rr->tokens[c++] = d[j];
+    ++nc;
+    if (d[j] == ctl.eos || nc == mo) done = 1;
+  }
+  if (rec >= 0 && !done) {
+    out_row[c] = rec;
+    rr->tokens[c++] = rec;
+    ++nc;
+    if (rec == ctl.eos || nc == mo) done = 1;
+  }
+  sl.len[slot] = base + c;
+  sl.ncomm[slot] = nc;
+  sl.done[slot] = done;
+  int ex = sl.exempt[slot];
+  if (ctl.exempt_rule) ex = pruned ? ncomm0 + pr_j : -1;
+  sl.exempt[slot] = ex;
+  rr->done = done;
+  rr->exempt_position = ex;
+  rr->n_committed_total = nc;
+  rr->committed = c;
+}
+
+__global__ void ptab_scatter_kernel(int* ptab, int max_pages, const int* tr, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ptab[static_cast<int64_t>(tr[3 * i]) * max_pages + tr[3 * i + 1]] = tr[3 * i + 2];
+}
+
+__global__ void admit_kernel(LmSlots sl, const LmAdmit* __restrict__ a, int n) {
+  const int e = blockIdx.x;
+  if (e >= n) return;
+  const LmAdmit ad = a[e];
+  int32_t* row = sl.tok + static_cast<int64_t>(ad.slot) * sl.max_seq;
+  for (int i = threadIdx.x; i < ad.len; i += blockDim.x) row[i] = ad.src[i];
+  if (threadIdx.x == 0) {
+    sl.len[ad.slot] = ad.len;
+    sl.ncomm[ad.slot] = 0;
+    sl.max_out[ad.slot] = ad.max_out;
+    sl.done[ad.slot] = 0;
+    sl.exempt[ad.slot] = -1;
+  }
+}
+
+__global__ void prefill_tokens_kernel(LmSlots sl, RowsDev rows, int rows_cap) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows_cap || r >= *rows.n_rows) return;
+  const int slot = rows.req_slot[rows.row_req[r]];
+  rows.row_tok[r] = sl.tok[static_cast<int64_t>(slot) * sl.max_seq + rows.row_pos[r]];
+}
+
+inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+cudaError_t lm_draft_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int t, cudaStream_t s) {
+  draft_prep_kernel<<<cdiv(n_t > 0 ? n_t : 1, 256), 256, 0, s>>>(sl, rq, rows, n_t, t);
+  return cudaGetLastError();
+}
+cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s) {
+  if (n_t <= 0) return cudaSuccess;
+  draft_post_kernel<<<cdiv(n_t, 256), 256, 0, s>>>(rq, argmax, n_t, t);
+  return cudaGetLastError();
+}
+cudaError_t lm_verify_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layers, int eos,
+                           int rows_cap, cudaStream_t s) {
+  (void)rows_cap;
+  if (n <= 0) return cudaSuccess;
+  verify_prep_kernel<<<n, 32, 0, s>>>(sl, rq, rows, n, layers, eos);
+  return cudaGetLastError();
+}
+cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,
+                         int64_t split_stride, int vocab, int k_thr, int rows_cap, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  exit_test_kernel<<<rows_cap, kExitThreads, 0, s>>>(sl, rq, rows, logits, splits, split_stride, vocab, k_thr);
+  return cudaGetLastError();
+}
+cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
+                                int* src_of, cudaStream_t s) {
+  (void)sl;
+  if (n <= 0) return cudaSuccess;
+  if (n > 1024) return cudaErrorInvalidValue;
+  frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, layer, src_of);
+  return cudaGetLastError();
+}
+cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, float eps, float* x, float* xs,
+                           __nv_bfloat16* xn, int rows_cap, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  gather_kernel<<<rows_cap, 256, 0, s>>>(rows, src_of, d, x, xs);
+  scatter_back_norm_kernel<<<rows_cap, 256, 0, s>>>(rows, d, eps, xs, x, xn);
+  return cudaGetLastError();
+}
+cudaError_t lm_accept_commit(LmSlots sl, LmReqState rq, RowsDev rows, StepCtl ctl,
+                             faser_round_result* results, cudaStream_t s) {
+  if (ctl.n <= 0) return cudaSuccess;
+  accept_commit_kernel<<<cdiv(ctl.n, 64), 64, 0, s>>>(sl, rq, rows, ctl, results);
+  return cudaGetLastError();
+}
+cudaError_t lm_ptab_scatter(int* ptab, int max_pages, const int* triples, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  ptab_scatter_kernel<<<cdiv(n, 256), 256, 0, s>>>(ptab, max_pages, triples, n);
+  return cudaGetLastError();
+}
+cudaError_t lm_admit(LmSlots sl, const LmAdmit* admits, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  admit_kernel<<<n, 128, 0, s>>>(sl, admits, n);
+  return cudaGetLastError();
+}
+cudaError_t lm_prefill_tokens(LmSlots sl, RowsDev rows, int rows_cap, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  prefill_tokens_kernel<<<cdiv(rows_cap, 256), 256, 0, s>>>(sl, rows, rows_cap);
+  return cudaGetLastError();
+}
+
+}  // namespace faser

@@ -1,0 +1,84 @@
+// llama_step.cuh — per-step device state of the Llama-style serving path and the launchers of
+// the small control kernels around the forwards (draft row prep, verify row prep, K4 early-exit
+// rank-count + frontier compaction, K5 fused greedy accept + commit + rollback).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "faser/engine.h"
+#include "llama.cuh"
+
+namespace faser {
+
+// Per-slot request state (SoA, HBM), the Llama analogue of SlotState.
+struct LmSlots {
+  int32_t* tok;      // [slots][max_seq] prompt ++ committed
+  int32_t* len;      // [slots] context length (prompt + committed)
+  int32_t* ncomm;    // [slots]
+  int32_t* max_out;  // [slots]
+  int32_t* done;     // [slots]
+  int32_t* exempt;   // [slots] exempt_position (-1 unset)
+  int32_t max_seq;
+};
+
+// Per-request (this step, sorted by k' descending) early-exit / draft state.
+struct LmReqState {
+  int32_t* slot;        // [n] engine slot
+  int32_t* k;           // [n] k_i' = min(k_i, remaining)
+  int32_t* spec;        // [n] controller's k_i (reported)
+  int32_t* live_idx;    // [n] position in the live (batch) order for results
+  int64_t* req_id;      // [n]
+  int32_t* drafted;     // [n][FASER_MAX_SPEC]
+  int32_t* count;       // [n] drafted length (EOS stop)
+  int32_t* active;      // [n] early-exit frontier
+  int32_t* gate_layers; // [n]
+  int32_t* n_pl;        // [n]
+  int32_t* pl;          // [n][FASER_MAX_SPEC] prune layers (VerifyOutcome::prune_layers)
+  int32_t* prune_layer; // [n][FASER_MAX_SPEC] layer at which row j was pruned (L if never)
+  int32_t* pr;          // [n][2] last pruned_at (j, layer), -1 if none
+  uint32_t* failmask;   // [n] exit-test failures at the current gated layer
+  int32_t* truth;       // [rows] final argmax per verify row (compacted order)
+};
+
+struct StepCtl {
+  int n;           // requests this step
+  int layers;      // target layers (L)
+  int eos;
+  int early_exit;  // 1: verify_with_early_exit semantics
+  int exempt_rule; // 1: exempt = committed_before + pruned_at.first for the next round
+};
+
+// draft step t: rows = sorted requests [0, n_t); row r = request r, 1 row each at position
+// len_r - 1 + t, input token = last committed (t == 0) or drafted[r][t-1].
+cudaError_t lm_draft_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int t, cudaStream_t s);
+// after draft step t: drafted[r][t] = argmax[r].
+cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s);
+// verify rows: request r has k'_r rows (host-built metadata); fills row tokens from drafted,
+// draft lengths (EOS stop) and resets the early-exit state.
+cudaError_t lm_verify_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layers, int eos,
+                           int rows_cap, cudaStream_t s);
+// K4: rank-count exit test of every live row against its drafted token at gated `layer`.
+cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,
+                         int64_t split_stride, int vocab, int k_thr, int rows_cap, cudaStream_t s);
+// K4 frontier: per request earliest failing row prunes the suffix; compacts the row set.
+// src_of[new_row] = old row; x is gathered through xs (fp32 [rows][d]) and re-normalised.
+cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
+                                int* src_of, cudaStream_t s);
+cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, float eps, float* x, float* xs,
+                           __nv_bfloat16* xn, int rows_cap, cudaStream_t s);
+// K5: greedy acceptance (+ early-exit outcome bookkeeping) + commit + exempt rule.
+cudaError_t lm_accept_commit(LmSlots sl, LmReqState rq, RowsDev rows, StepCtl ctl,
+                             faser_round_result* results, cudaStream_t s);
+// page-table scatter: ptab[slot*max_pages + idx] = page for each (slot, idx, page) triple.
+cudaError_t lm_ptab_scatter(int* ptab, int max_pages, const int* triples, int n, cudaStream_t s);
+// admission: copy prompts into the slot rows and initialise slot state.
+struct LmAdmit {
+  const int32_t* src;
+  int32_t slot, len, max_out, reserved;
+};
+cudaError_t lm_admit(LmSlots sl, const LmAdmit* admits, int n, cudaStream_t s);
+// prefill rows: tokens of the prompt prefix (positions 0..len-2) read from the slot rows.
+cudaError_t lm_prefill_tokens(LmSlots sl, RowsDev rows, int rows_cap, cudaStream_t s);
+
+}  // namespace faser

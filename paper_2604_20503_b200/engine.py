@@ -184,11 +184,15 @@ def make_gate_plan(policy, entries, b, r, num_layers, models=None):
 class ServingEngine:
     """Stateful GPU engine: submit() requests, step() one draft->verify->commit round."""
 
-    def __init__(self, model_params=None, cfg=None, **cfg_kw):
+    def __init__(self, model_params=None, cfg=None, desc=None, **cfg_kw):
+        """Toy engine from ``model_params`` (LayeredToyLM::Params), or a Llama-style engine
+        from ``desc`` (abi.ModelDesc with kind MODEL_LLAMA, see llama.py presets)."""
         self.h = None
         self.params = model_params if model_params is not None else abi.ToyParams.default()
         self.cfg = cfg if cfg is not None else default_engine_cfg(**cfg_kw)
-        desc = abi.ModelDesc(kind=abi.MODEL_TOY, toy=self.params)
+        if desc is None:
+            desc = abi.ModelDesc(kind=abi.MODEL_TOY, toy=self.params)
+        self.desc = desc
         h = C.c_void_p()
         _check(lib().faser_engine_create(C.byref(desc), C.byref(self.cfg), C.byref(h)))
         self.h = h
@@ -258,3 +262,30 @@ class ServingEngine:
 
     def kernel_launches(self):
         return lib().faser_kernel_launches(self.h)
+
+    # ---- Llama validation hooks (cfg.debug_capture = 1)
+    def debug_verify_logits(self, stage=0):
+        """(logits [rows][V] float32, ids [rows][2] = (req_id, j)) of the last step's verify
+        forward: stage 0 = final, stage l = gated layer l."""
+        V = self.desc.target.vocab
+        rows = C.c_int32()
+        _check(lib().faser_debug_verify_logits(self.h, stage, None, None, 0, C.byref(rows)), self.h)
+        n = rows.value
+        z = np.zeros((max(n, 1), V), np.float32)
+        ids = np.zeros((max(n, 1), 2), np.int64)
+        _check(lib().faser_debug_verify_logits(self.h, stage, _ptr(z), _ptr(ids), n, C.byref(rows)),
+               self.h)
+        return z[:n], ids[:n]
+
+    def debug_drafted(self):
+        n = C.c_int32()
+        buf = np.zeros((self.cfg.max_batch, abi.MAX_SPEC), np.int32)
+        _check(lib().faser_debug_drafted(self.h, _ptr(buf), self.cfg.max_batch, C.byref(n)), self.h)
+        return buf[:n.value]
+
+    def debug_kv_pages(self, req_id):
+        buf = np.zeros(4096, np.int32)
+        n = C.c_int32()
+        _check(lib().faser_debug_kv_pages(self.h, C.c_int64(req_id), _ptr(buf), len(buf), C.byref(n)),
+               self.h)
+        return buf[:n.value].tolist()

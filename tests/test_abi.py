@@ -31,13 +31,13 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_sizes_match_header():
     L = engine.lib()
-    out = (C.c_int64 * 12)()
-    assert L.faser_abi_struct_sizes(out, 12) == 0
+    out = (C.c_int64 * 13)()
+    assert L.faser_abi_struct_sizes(out, 13) == 0
     py = [abi.ToyParams, abi.ExitPolicy, abi.GatePlan, abi.GateEntry, abi.OverlapPlan,
           abi.LatencyParams, abi.LatencyModel, abi.VerifyOutcome, abi.ModelDesc, abi.EngineCfg,
-          abi.StepPlan, abi.RoundResult]
+          abi.StepPlan, abi.RoundResult, abi.LlamaShape]
     assert [C.sizeof(t) for t in py] == list(out)
-    assert L.faser_abi_version() == 1
+    assert L.faser_abi_version() == 2
 
 
 def test_library_is_sm100a_cubin():

@@ -1,0 +1,49 @@
+"""K1/K2 projection GEMM (tcgen05 + TMEM + TMA, swap-AB, split-K) vs a torch fp32 reference
+of the same op on the same bf16 operands."""
+import ctypes as C
+
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not has_gpu():
+        pytest.skip("no GPU")
+    from paper_2604_20503_b200 import engine
+    return engine.lib()
+
+
+# (n_out, T, K): the config-3/4 projection shapes at verify / draft row counts
+SHAPES = [
+    (128, 1, 64), (256, 5, 128), (2560, 20, 2048), (2048, 33, 2048), (11264, 160, 2048),
+    (2048, 64, 5632), (32000, 17, 2048), (2304, 256, 768), (768, 300, 3072), (6144, 129, 768),
+    (4096, 1280, 4096), (1024, 700, 1024),
+]
+
+
+@pytest.mark.parametrize("n_out,T,K", SHAPES)
+@pytest.mark.parametrize("splits", [0, 1])
+def test_gemm_matches_fp32(L, n_out, T, K, splits):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(n_out * 7 + T * 3 + K)
+    w = (torch.randn(n_out, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn(T, K, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.full((T, n_out), float("nan"), device="cuda", dtype=torch.float32)
+    rc = L.faser_k_gemm_bf16(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()),
+                             C.c_void_p(out.data_ptr()), n_out, T, K, splits, None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().t()
+    err = (out - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    # fp32 accumulation of exact bf16 products: only summation order differs
+    assert err <= 1e-4 * max(scale, 1.0) + 1e-3, (err, scale)
+
+
+def test_gemm_rejects_bad_shapes(L):
+    assert L.faser_k_gemm_bf16(C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), 100, 4, 64, 0, None) == 1
+    assert L.faser_k_gemm_bf16(C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), 128, 4, 60, 0, None) == 1
