@@ -266,6 +266,12 @@ faser_status faser_debug_drafted(faser_engine* e, int32_t* drafted, int32_t cap,
 faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* pages, int32_t cap,
                                   int32_t* n);
 
+/* Raw bf16 weight elements [offset, offset+n) of a LLAMA engine's model (0 draft, 1 target),
+ * tensor which: 0 lm_head [V][d], 1 embedding [V][d], 2 wqkv, 3 wo, 4 wgu (interleaved), 5 wd
+ * of `layer`. For checking the device generator against the oracle's. */
+faser_status faser_debug_weights(faser_engine* e, int32_t model, int32_t which, int32_t layer,
+                                 int64_t offset, int32_t n, uint16_t* out);
+
 /* ABI self-description: FASER_ABI_VERSION and sizeof() of every struct above, in
  * declaration order (toy_params, exit_policy, gate_plan, gate_entry, overlap_plan,
  * latency_params, latency_model, verify_outcome, model_desc, engine_cfg, step_plan,

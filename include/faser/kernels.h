@@ -22,6 +22,11 @@ extern "C" {
 faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,
                                int32_t t, int32_t k, int32_t splits, void* stream);
 
+/* Same with an explicit launch plan: bn in {32, 64, 128, 256} rows per tile (0 = auto) and
+ * splits in [1, 8] (0 = auto). For plan sweeps / microbenchmarks. */
+faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, int32_t n_out,
+                                    int32_t t, int32_t k, int32_t bn, int32_t splits, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

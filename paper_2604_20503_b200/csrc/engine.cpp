@@ -512,6 +512,12 @@ faser_status faser_debug_drafted(faser_engine* e, int32_t* drafted, int32_t cap,
   return faser::llama_debug_drafted(e->llama, drafted, cap, n);
 }
 
+faser_status faser_debug_weights(faser_engine* e, int32_t model, int32_t which, int32_t layer,
+                                 int64_t offset, int32_t n, uint16_t* out) {
+  if (!e || !e->llama) return FASER_EINVAL;
+  return faser::llama_debug_weights(e->llama, model, which, layer, offset, n, out);
+}
+
 faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n) {
   if (!e || !n || !e->llama) return FASER_EINVAL;
   return faser::llama_debug_kv_pages(e->llama, req_id, pages, cap, n);

@@ -10,16 +10,6 @@
 namespace faser {
 namespace {
 
-__global__ void sum_splits_kernel(const float* __restrict__ ws, float* __restrict__ out,
-                                  int splits, size_t n) {
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    float a = 0.f;
-    for (int z = 0; z < splits; ++z) a += ws[z * n + i];
-    out[i] = a;
-  }
-}
-
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -36,8 +26,10 @@ int num_sms() {
 
 using namespace faser;
 
-extern "C" faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,
-                                          int32_t t, int32_t k, int32_t splits, void* stream) {
+extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, int32_t n_out,
+                                               int32_t t, int32_t k, int32_t bn, int32_t splits,
+                                               void* stream) {
+  if (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256) return FASER_EINVAL;
   if (!w || !x || !out || n_out <= 0 || t < 0 || k <= 0) return FASER_EINVAL;
   if (n_out % 128 || k % 64) return FASER_EINVAL;
   int ndev = 0;
@@ -47,17 +39,22 @@ extern "C" faser_status faser_k_gemm_bf16(const void* w, const void* x, float* o
   GemmOperand W, X;
   if (make_weight_operand(&W, w, n_out, k) != cudaSuccess) return FASER_ECUDA;
   if (make_act_operand(&X, x, t, k) != cudaSuccess) return FASER_ECUDA;
-  if (splits <= 0) splits = gemm_splits_for(n_out, t, k, num_sms());
-  const int z = gemm_effective_splits(k, splits);
-  float* ws = out;
-  if (z > 1 && cudaMallocAsync(&ws, sizeof(float) * z * static_cast<size_t>(t) * n_out, s) != cudaSuccess)
-    return FASER_ENOMEM;
-  cudaError_t e = gemm_tn(W, X, ws, t, nullptr, t, splits, s);
-  if (e == cudaSuccess && z > 1) {
-    const size_t n = static_cast<size_t>(t) * n_out;
-    sum_splits_kernel<<<static_cast<int>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(ws, out, z, n);
-    e = cudaGetLastError();
+  GemmPlan plan = gemm_plan(n_out, t, k, num_sms());
+  if (bn > 0) plan.bn = bn;
+  if (splits > 0) {  // caller-forced split count (cluster size <= 8)
+    const int kb = k / 64, s1 = splits < 8 ? splits : 8;
+    const int kps = (kb + s1 - 1) / s1;
+    plan.splits = (kb + kps - 1) / kps;
   }
-  if (z > 1) cudaFreeAsync(ws, s);
+  EpiArgs ea;
+  ea.mode = kEpiStore;
+  ea.t_stride = t;
+  ea.out = out;
+  cudaError_t e = gemm_fused(W, X, t, plan, ea, s);
   return e == cudaSuccess ? FASER_OK : FASER_ECUDA;
+}
+
+extern "C" faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,
+                                          int32_t t, int32_t k, int32_t splits, void* stream) {
+  return faser_k_gemm_bf16_plan(w, x, out, n_out, t, k, 0, splits, stream);
 }

@@ -86,26 +86,16 @@ cudaError_t lm_init_gate_up(__nv_bfloat16* wgu, int ffn, int d, uint64_t seed, u
 cudaError_t lm_init_embedding(__nv_bfloat16* emb, const __nv_bfloat16* lm, const LlamaShape& m,
                               uint32_t ga, uint32_t gb, cudaStream_t s);
 
-// x[r] = emb[row_tok[r]] (fp32 residual) and xn[r] = bf16(rmsnorm(x[r])) (gamma = 1).
-cudaError_t lm_embed_norm(const LlamaShape& m, const __nv_bfloat16* emb, RowsDev rows, int rows_cap,
-                          float* x, __nv_bfloat16* xn, cudaStream_t s);
-// qkv = sum of split partials; RoPE(q,k) at row_pos; q -> qbuf bf16 [rows][n_q*hd];
-// k,v appended to the paged cache of `layer`.
-cudaError_t lm_qkv_rope_append(const LlamaShape& m, const float* ws, int splits, int t_stride,
-                               RowsDev rows, int rows_cap, const float2* rope, KvDev kv, int layer,
-                               __nv_bfloat16* qbuf, cudaStream_t s);
+// x[r] = emb[row_tok[r]] (fp32 residual), xb = bf16 copy (the GEMM operand; RMSNorm is folded
+// into the consuming GEMM's epilogue), ss[c][r] = sum of squares of 128-column chunk c.
+cudaError_t lm_embed(const LlamaShape& m, const __nv_bfloat16* emb, RowsDev rows, int rows_cap,
+                     float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s);
+// argmax_lowest over the per-128-vocab-tile (max, lowest id) partials of the logits epilogue.
+cudaError_t lm_argmax_reduce(int n_tiles, RowsDev rows, int rows_cap, const float2* amax, int* out,
+                             cudaStream_t s);
 // Causal attention of every row over its request's paged KV (GQA packed, mma.sync bf16).
 cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req,
                          int max_ctx, KvDev kv, int layer, const __nv_bfloat16* qbuf,
                          __nv_bfloat16* obuf, float* scratch, size_t scratch_bytes, cudaStream_t s);
-// x += sum of split partials (fp32 residual), xn = bf16(rmsnorm(x)).
-cudaError_t lm_residual_norm(const LlamaShape& m, const float* ws, int splits, int t_stride,
-                             RowsDev rows, int rows_cap, float* x, __nv_bfloat16* xn, cudaStream_t s);
-// h = bf16(silu(gate) * up) from the interleaved gate/up partials.
-cudaError_t lm_swiglu(const LlamaShape& m, const float* ws, int splits, int t_stride, RowsDev rows,
-                      int rows_cap, __nv_bfloat16* h, cudaStream_t s);
-// logits[r][v] = sum of split partials (in place into split 0), argmax (lowest id on ties).
-cudaError_t lm_logits_argmax(int vocab, float* ws, int splits, int t_stride, RowsDev rows,
-                             int rows_cap, int* argmax_out, cudaStream_t s);
 
 }  // namespace faser

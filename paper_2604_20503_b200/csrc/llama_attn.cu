@@ -308,7 +308,6 @@ __global__ void attn_combine_kernel(RowsDev rows, int n_q, int n_split, int rows
   if (row >= *rows.n_rows) return;
   float mm = kNegBig;
   for (int s = 0; s < n_split; ++s) {
-    // splits past the request's causal range never wrote: their slots hold (kNegBig, 0)
     mm = fmaxf(mm, part_ml[(static_cast<int64_t>(s) * rows_cap + row) * n_q + head].x);
   }
   float acc[HD / 32];
@@ -380,10 +379,8 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   float* part_o = scratch;
   float2* part_ml = reinterpret_cast<float2*>(scratch + static_cast<size_t>(n_split) * rows_cap * m.n_q * m.hd);
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(m.hd));
-  if (n_split > 1) {
-    const int64_t nml = static_cast<int64_t>(n_split) * rows_cap * m.n_q;
-    attn_clear_ml_kernel<<<static_cast<int>((nml + 255) / 256 < 4096 ? (nml + 255) / 256 : 4096), 256, 0, s>>>(part_ml, nml);
-  }
+  // every (row, split) slot is written by its CTA (empty key ranges write (-1e30, 0)), so the
+  // partial buffers need no clearing.
   cudaError_t e;
   if (m.hd == 64)
     e = rows_mode ? launch<64, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, rows_cap, scale_log2, s)

@@ -178,33 +178,37 @@ struct LmModel {
 
 // ------------------------------------------------------------------ activations of one model
 struct LmWork {
-  int rows_cap = 0;
-  Mem x, xs, xn, q, h, ws, attn, argmax, src_of;
-  size_t ws_floats = 0, attn_bytes = 0;
-  GemmOperand op_xn, op_attn, op_h;
-  // persistent row metadata (draft steps, prefill)
+  int rows_cap = 0, lm_rows_cap = 0;
+  // residual stream: fp32 x, its bf16 copy xb (GEMM operand), per-128-column sums of squares
+  Mem x, xb, ss, xs, xbs, sss;  // (+ scratch copies for early-exit compaction)
+  Mem ob, q, h, logits, amax, attn, argmax, src_of;
+  size_t attn_bytes = 0;
+  GemmOperand op_xb, op_ob, op_h;
+  // persistent row metadata (draft steps)
   Mem meta;
   RowsDev rows{};
 
-  void build(const LlamaShape& s, int cap, int lm_rows_cap) {
+  void build(const LlamaShape& s, int cap, int lm_cap) {
     rows_cap = cap;
+    lm_rows_cap = lm_cap;
     const int64_t d = s.d, qd = static_cast<int64_t>(s.n_q) * s.hd;
-    const int64_t xw = std::max(d, qd);
     x.alloc(static_cast<size_t>(cap) * d * 4);
     xs.alloc(static_cast<size_t>(cap) * d * 4);
-    xn.alloc(static_cast<size_t>(cap) * xw * 2);
+    xb.alloc(static_cast<size_t>(cap) * d * 2);
+    xbs.alloc(static_cast<size_t>(cap) * d * 2);
+    ss.alloc(static_cast<size_t>(cap) * (d / 128) * 4);
+    sss.alloc(static_cast<size_t>(cap) * (d / 128) * 4);
+    ob.alloc(static_cast<size_t>(cap) * qd * 2);
     q.alloc(static_cast<size_t>(cap) * qd * 2);
     h.alloc(static_cast<size_t>(cap) * s.ffn * 2);
-    const int64_t nmax = std::max<int64_t>({static_cast<int64_t>(s.qkv_out()), 2ll * s.ffn, d});
-    ws_floats = std::max<size_t>(static_cast<size_t>(cap) * nmax, static_cast<size_t>(lm_rows_cap) * s.vocab);
-    ws_floats = std::max<size_t>(ws_floats, static_cast<size_t>(8) << 20);  // split-K partials
-    ws.alloc(ws_floats * 4);
+    logits.alloc(static_cast<size_t>(lm_cap) * s.vocab * 4);
+    amax.alloc(static_cast<size_t>(lm_cap) * (s.vocab / 128) * 8);
     attn_bytes = static_cast<size_t>(64) << 20;
     attn.alloc(attn_bytes);
     argmax.alloc(static_cast<size_t>(cap) * 4);
     src_of.alloc(static_cast<size_t>(cap) * 4);
-    LCK(make_act_operand(&op_xn, xn.p, cap, s.d));
-    LCK(make_act_operand(&op_attn, xn.p, cap, static_cast<int>(qd)));
+    LCK(make_act_operand(&op_xb, xb.p, cap, s.d));
+    LCK(make_act_operand(&op_ob, ob.p, cap, static_cast<int>(qd)));
     LCK(make_act_operand(&op_h, h.p, cap, s.ffn));
     meta.alloc(static_cast<size_t>(cap) * 9 * 4 + 64);
     int* m = meta.as<int>();
@@ -341,6 +345,7 @@ class LlamaEngine {
     target.build(tsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream);
     wd.build(dsh, cap, B);
     wt.build(tsh, cap, verify_rows);
+    LCK(cudaDeviceSynchronize());
     s_tok.alloc(static_cast<size_t>(B) * max_seq * 4);
     s_len.alloc(B * 4);
     s_ncomm.alloc(B * 4);
@@ -403,22 +408,17 @@ class LlamaEngine {
     bool capture = false;
   };
 
-  int splits(int n_out, int T, int k) const { return gemm_splits_for(n_out, T, k, nsm); }
+  GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, nsm); }
 
-  void capture_stage(int stage, const LmModel& m, const LmWork& w, const Fwd& f, int spl) {
+  void capture_stage(int stage, const LmModel& m, const LmWork& w, const Fwd& f) {
     LCK(cudaStreamSynchronize(stream));
     int n = 0;
     LCK(cudaMemcpy(&n, f.rows.n_rows, 4, cudaMemcpyDeviceToHost));
     const int V = m.sh.vocab;
     Stage st;
     st.rows = n;
-    std::vector<float> part(static_cast<size_t>(n) * V);
-    st.logits.assign(static_cast<size_t>(n) * V, 0.f);
-    for (int z = 0; z < (stage == 0 ? 1 : spl); ++z) {  // stage 0 is already reduced into split 0
-      LCK(cudaMemcpy(part.data(), w.ws.as<float>() + static_cast<size_t>(z) * f.T * V,
-                     part.size() * 4, cudaMemcpyDeviceToHost));
-      for (size_t i = 0; i < part.size(); ++i) st.logits[i] += part[i];
-    }
+    st.logits.resize(static_cast<size_t>(n) * V);
+    LCK(cudaMemcpy(st.logits.data(), w.logits.p, st.logits.size() * 4, cudaMemcpyDeviceToHost));
     std::vector<int> req(n), jj(n);
     LCK(cudaMemcpy(req.data(), f.rows.row_req, 4 * n, cudaMemcpyDeviceToHost));
     LCK(cudaMemcpy(jj.data(), f.rows.row_j, 4 * n, cudaMemcpyDeviceToHost));
@@ -434,50 +434,74 @@ class LlamaEngine {
     const LlamaShape& s = m.sh;
     const int T = f.T;
     if (T <= 0) return;
+    if (T > w.rows_cap) throw LFail{FASER_ECAPACITY, "forward rows exceed capacity"};
+    const bool lm_head = f.logits || f.ee;
+    if (lm_head && T > w.lm_rows_cap) throw LFail{FASER_ECAPACITY, "LM-head rows exceed capacity"};
     const KvDev kv = m.kvdev(ptab.as<int>(), max_pages);
     const int qd = s.n_q * s.hd;
-    const int s_qkv = splits(s.qkv_out(), T, s.d), s_o = splits(s.d, T, qd);
-    const int s_gu = splits(2 * s.ffn, T, s.d), s_d = splits(s.d, T, s.ffn), s_lm = splits(s.vocab, T, s.d);
-    const int z_qkv = gemm_effective_splits(s.d, s_qkv), z_o = gemm_effective_splits(qd, s_o);
-    const int z_gu = gemm_effective_splits(s.d, s_gu), z_d = gemm_effective_splits(s.ffn, s_d);
-    const int z_lm = gemm_effective_splits(s.d, s_lm);
-    float* ws = w.ws.as<float>();
-    const size_t need = std::max<size_t>({static_cast<size_t>(z_qkv) * T * s.qkv_out(), static_cast<size_t>(z_o) * T * s.d,
-                                          static_cast<size_t>(z_gu) * T * 2 * s.ffn, static_cast<size_t>(z_d) * T * s.d,
-                                          f.logits || f.ee ? static_cast<size_t>(z_lm) * T * s.vocab : 0});
-    if (need > w.ws_floats) throw LFail{FASER_ECAPACITY, "GEMM workspace too small for this batch"};
+    const GemmPlan p_qkv = plan(s.qkv_out(), T, s.d), p_o = plan(s.d, T, qd);
+    const GemmPlan p_gu = plan(2 * s.ffn, T, s.d), p_d = plan(s.d, T, s.ffn), p_lm = plan(s.vocab, T, s.d);
     RowsDev rows = f.rows;
-    const int* nd = rows.n_rows;
-    LCK(lm_embed_norm(s, m.emb, rows, T, w.x.as<float>(), w.xn.as<__nv_bfloat16>(), stream));
+    EpiArgs base;
+    base.t_stride = T;
+    base.n_rows = rows.n_rows;
+    base.ss_chunks = s.d / 128;
+    base.d_norm = s.d;
+    base.eps = s.eps;
+    EpiArgs e_qkv = base;
+    e_qkv.mode = kEpiQkv;
+    e_qkv.ss_in = w.ss.as<float>();
+    e_qkv.rows = rows;
+    e_qkv.rope = m.rope.as<float2>();
+    e_qkv.kv = kv;
+    e_qkv.n_q = s.n_q;
+    e_qkv.n_kv = s.n_kv;
+    e_qkv.hd = s.hd;
+    e_qkv.q = w.q.as<__nv_bfloat16>();
+    EpiArgs e_res = base;
+    e_res.mode = kEpiResid;
+    e_res.x = w.x.as<float>();
+    e_res.xb = w.xb.as<__nv_bfloat16>();
+    e_res.ss_out = w.ss.as<float>();
+    EpiArgs e_glu = base;
+    e_glu.mode = kEpiSwiglu;
+    e_glu.ss_in = w.ss.as<float>();
+    e_glu.h = w.h.as<__nv_bfloat16>();
+    e_glu.ffn = s.ffn;
+    EpiArgs e_lm = base;
+    e_lm.mode = kEpiLogits;
+    e_lm.ss_in = w.ss.as<float>();
+    e_lm.logits = w.logits.as<float>();
+    e_lm.amax = w.amax.as<float2>();
+
+    LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), stream));
     ++launches;
     for (int l = 0; l < s.layers; ++l) {
-      LCK(gemm_tn(m.op_qkv[l], w.op_xn, ws, T, nd, T, s_qkv, stream));
-      LCK(lm_qkv_rope_append(s, ws, z_qkv, T, rows, T, m.rope.as<float2>(), kv, l, w.q.as<__nv_bfloat16>(), stream));
+      e_qkv.layer = l;
+      LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, stream));
       LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
-                       w.xn.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, stream));
-      LCK(gemm_tn(m.op_o[l], w.op_attn, ws, T, nd, T, s_o, stream));
-      LCK(lm_residual_norm(s, ws, z_o, T, rows, T, w.x.as<float>(), w.xn.as<__nv_bfloat16>(), stream));
-      LCK(gemm_tn(m.op_gu[l], w.op_xn, ws, T, nd, T, s_gu, stream));
-      LCK(lm_swiglu(s, ws, z_gu, T, rows, T, w.h.as<__nv_bfloat16>(), stream));
-      LCK(gemm_tn(m.op_d[l], w.op_h, ws, T, nd, T, s_d, stream));
-      LCK(lm_residual_norm(s, ws, z_d, T, rows, T, w.x.as<float>(), w.xn.as<__nv_bfloat16>(), stream));
-      launches += 9;
+                       w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, stream));
+      LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, stream));
+      LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, stream));
+      LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, stream));
+      launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
-        LCK(gemm_tn(m.op_lm, w.op_xn, ws, T, nd, T, s_lm, stream));
-        if (f.capture) capture_stage(layer, m, w, f, z_lm);
-        LCK(lm_exit_test(sl, cur_q, rows, ws, z_lm, static_cast<int64_t>(T) * s.vocab, s.vocab, f.k_table[layer], T, stream));
+        LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, stream));
+        if (f.capture) capture_stage(layer, m, w, f);
+        LCK(lm_exit_test(sl, cur_q, rows, w.logits.as<float>(), 1, 0, s.vocab, f.k_table[layer], T, stream));
         LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), stream));
-        LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, s.eps, w.x.as<float>(), w.xs.as<float>(),
-                           w.xn.as<__nv_bfloat16>(), T, stream));
+        LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(),
+                           w.ss.as<float>(), w.xs.as<float>(), w.xbs.as<__nv_bfloat16>(), w.sss.as<float>(),
+                           stream));
         launches += 5;
       }
     }
     if (f.logits) {
-      LCK(gemm_tn(m.op_lm, w.op_xn, ws, T, nd, T, s_lm, stream));
-      LCK(lm_logits_argmax(s.vocab, ws, z_lm, T, rows, T, f.argmax_out, stream));
+      LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, stream));
+      LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, stream));
       launches += 2;
-      if (f.capture) capture_stage(0, m, w, f, 1);
+      if (f.capture) capture_stage(0, m, w, f);
     }
   }
 
@@ -997,4 +1021,29 @@ faser_status llama_debug_kv_pages(LlamaEngine* e, int64_t req_id, int32_t* pages
   });
 }
 
+}  // namespace faser
+
+namespace faser {
+faser_status llama_debug_weights(LlamaEngine* e, int32_t model, int32_t which, int32_t layer, int64_t offset,
+                                 int32_t n, uint16_t* out) {
+  return lguard(e, [&] {
+    if (model < 0 || model > 1 || which < 0 || which > 5 || n < 0 || !out) throw LFail{FASER_EINVAL, "bad tensor"};
+    const LmModel& m = model == 0 ? e->draft : e->target;
+    const LlamaShape& s = m.sh;
+    if (which >= 2 && (layer < 0 || layer >= s.layers)) throw LFail{FASER_EINVAL, "layer out of range"};
+    const int64_t d = s.d, qd = static_cast<int64_t>(s.n_q) * s.hd;
+    const void* base = nullptr;
+    int64_t size = 0;
+    switch (which) {
+      case 0: base = m.lm; size = static_cast<int64_t>(s.vocab) * d; break;
+      case 1: base = m.emb; size = static_cast<int64_t>(s.vocab) * d; break;
+      case 2: base = m.lw[layer].wqkv; size = static_cast<int64_t>(s.qkv_out()) * d; break;
+      case 3: base = m.lw[layer].wo; size = d * qd; break;
+      case 4: base = m.lw[layer].wgu; size = 2ll * s.ffn * d; break;
+      default: base = m.lw[layer].wd; size = d * s.ffn; break;
+    }
+    if (offset < 0 || offset + n > size) throw LFail{FASER_EINVAL, "range outside tensor"};
+    LCK(cudaMemcpy(out, static_cast<const uint16_t*>(base) + offset, static_cast<size_t>(n) * 2, cudaMemcpyDeviceToHost));
+  });
+}
 }  // namespace faser

@@ -35,6 +35,8 @@ int64_t llama_launches(const LlamaEngine* e);
 faser_status llama_debug_verify_logits(LlamaEngine* e, int32_t stage, float* logits, int64_t* row_ids,
                                        int32_t cap_rows, int32_t* rows);
 faser_status llama_debug_drafted(LlamaEngine* e, int32_t* drafted, int32_t cap, int32_t* n);
+faser_status llama_debug_weights(LlamaEngine* e, int32_t model, int32_t which, int32_t layer, int64_t offset,
+                                 int32_t n, uint16_t* out);
 faser_status llama_debug_kv_pages(LlamaEngine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n);
 
 }  // namespace faser

@@ -1,8 +1,7 @@
-// llama_kernels.cu — element-wise / row kernels of the Llama-style draft & verify forwards:
-// deterministic weight init, embedding + RMSNorm, split-K reduction fused with RoPE + paged
-// KV append, residual + RMSNorm, SwiGLU, logits reduction + argmax (lowest id on ties,
-// argmax_lowest toylm.cpp:9-16). All are HBM/L2-bound row kernels; the projections
-// themselves are the tcgen05 GEMM (tc_gemm.cu) and attention is llama_attn.cu.
+// llama_kernels.cu — the small kernels of the Llama-style forwards that are not fused into
+// the tcgen05 GEMM epilogues (tc_gemm.cu): deterministic weight init, embedding gather (+ the
+// per-chunk sums of squares the next GEMM folds into its RMSNorm scale), and the final
+// argmax_lowest reduction (toylm.cpp:9-16: ties -> lowest id) over per-tile partials.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -67,151 +66,38 @@ int grid_for(int64_t n) {
   return static_cast<int>(g < 148 * 32 ? g : 148 * 32);
 }
 
-// ------------------------------------------------------------------ block reductions
-template <int NT>
-__device__ __forceinline__ float block_sum(float v, float* red) {
+// One CTA of 128 threads per (row, 128-column chunk).
+__global__ void __launch_bounds__(128) embed_kernel(const __nv_bfloat16* __restrict__ emb, RowsDev rows, int d,
+                                                    int t_stride, float* __restrict__ x,
+                                                    __nv_bfloat16* __restrict__ xb, float* __restrict__ ss) {
+  __shared__ float red[4];
+  const int r = blockIdx.x, c = blockIdx.y * 128 + threadIdx.x;
+  if (r >= *rows.n_rows) return;
+  const __nv_bfloat16 e = emb[static_cast<int64_t>(rows.row_tok[r]) * d + c];
+  const float v = __bfloat162float(e);
+  x[static_cast<int64_t>(r) * d + c] = v;
+  xb[static_cast<int64_t>(r) * d + c] = e;
+  float q = v * v;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
   __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NT / 32; ++i) s += red[i];
-  return s;
+  if (threadIdx.x == 0) ss[static_cast<int64_t>(blockIdx.y) * t_stride + r] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 
-constexpr int kRowThreads = 256;
-
-__global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(
-    const __nv_bfloat16* __restrict__ emb, RowsDev rows, int d, float eps, float* __restrict__ x,
-    __nv_bfloat16* __restrict__ xn) {
-  __shared__ float red[kRowThreads / 32];
-  const int r = blockIdx.x;
+// One warp per row.
+__global__ void argmax_reduce_kernel(int n_tiles, RowsDev rows, int t_stride, const float2* __restrict__ amax,
+                                     int* __restrict__ out) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= *rows.n_rows) return;
-  const int tok = rows.row_tok[r];
-  const __nv_bfloat16* e = emb + static_cast<int64_t>(tok) * d;
-  float* xr = x + static_cast<int64_t>(r) * d;
-  float ss = 0.f;
-  for (int c = threadIdx.x; c < d; c += kRowThreads) {
-    const float v = __bfloat162float(e[c]);
-    xr[c] = v;
-    ss += v * v;
-  }
-  ss = block_sum<kRowThreads>(ss, red);
-  const float inv = rsqrtf(ss / d + eps);
-  __nv_bfloat16* o = xn + static_cast<int64_t>(r) * d;
-  for (int c = threadIdx.x; c < d; c += kRowThreads) o[c] = __float2bfloat16_rn(xr[c] * inv);
-}
-
-__global__ void __launch_bounds__(kRowThreads) residual_norm_kernel(
-    const float* __restrict__ ws, int splits, int64_t split_stride, RowsDev rows, int d, float eps,
-    float* __restrict__ x, __nv_bfloat16* __restrict__ xn) {
-  __shared__ float red[kRowThreads / 32];
-  const int r = blockIdx.x;
-  if (r >= *rows.n_rows) return;
-  float* xr = x + static_cast<int64_t>(r) * d;
-  const float* p = ws + static_cast<int64_t>(r) * d;
-  float ss = 0.f;
-  for (int c = threadIdx.x; c < d; c += kRowThreads) {
-    float a = 0.f;
-    for (int z = 0; z < splits; ++z) a += p[z * split_stride + c];
-    const float v = xr[c] + a;
-    xr[c] = v;
-    ss += v * v;
-  }
-  ss = block_sum<kRowThreads>(ss, red);
-  const float inv = rsqrtf(ss / d + eps);
-  if (xn) {
-    __nv_bfloat16* o = xn + static_cast<int64_t>(r) * d;
-    for (int c = threadIdx.x; c < d; c += kRowThreads) o[c] = __float2bfloat16_rn(xr[c] * inv);
-  }
-}
-
-// One CTA per row. Threads walk (head, i) pairs with i < hd/2 (rotate-half RoPE).
-__global__ void __launch_bounds__(kRowThreads) qkv_rope_append_kernel(
-    const float* __restrict__ ws, int splits, int64_t split_stride, RowsDev rows, int n_q, int n_kv,
-    int hd, const float2* __restrict__ rope, KvDev kv, int layer, __nv_bfloat16* __restrict__ qbuf) {
-  const int r = blockIdx.x;
-  if (r >= *rows.n_rows) return;
-  const int half = hd / 2;
-  const int nout = (n_q + 2 * n_kv) * hd;
-  const int pos = rows.row_pos[r];
-  const int slot = rows.req_slot[rows.row_req[r]];
-  const int page = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + pos / kPage];
-  const int off = pos % kPage;
-  const float* p = ws + static_cast<int64_t>(r) * nout;
-  const float2* rp = rope + static_cast<int64_t>(pos) * half;
-  __nv_bfloat16* kvl = kv.pool + layer * kv.layer_stride;
-  const int heads = n_q + 2 * n_kv;
-  for (int e = threadIdx.x; e < heads * half; e += kRowThreads) {
-    const int h = e / half, i = e % half;
-    const int c0 = h * hd + i, c1 = c0 + half;
-    float a = 0.f, b = 0.f;
-    for (int z = 0; z < splits; ++z) {
-      a += p[z * split_stride + c0];
-      b += p[z * split_stride + c1];
-    }
-    if (h < n_q + n_kv) {  // rotate q and k
-      const float2 cs = rp[i];
-      const float ra = a * cs.x - b * cs.y;
-      const float rb = b * cs.x + a * cs.y;
-      a = ra;
-      b = rb;
-    }
-    if (h < n_q) {
-      __nv_bfloat16* q = qbuf + static_cast<int64_t>(r) * n_q * hd + h * hd;
-      q[i] = __float2bfloat16_rn(a);
-      q[i + half] = __float2bfloat16_rn(b);
-    } else {
-      const bool is_v = h >= n_q + n_kv;
-      const int kvh = is_v ? h - n_q - n_kv : h - n_q;
-      __nv_bfloat16* dst = kvl + ((static_cast<int64_t>(page) * n_kv + kvh) * 2 + (is_v ? 1 : 0)) * kPage * hd +
-                           off * hd;
-      dst[i] = __float2bfloat16_rn(a);
-      dst[i + half] = __float2bfloat16_rn(b);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __restrict__ ws, int splits,
-                                                             int64_t split_stride, RowsDev rows,
-                                                             int ffn, __nv_bfloat16* __restrict__ h) {
-  const int r = blockIdx.x;
-  if (r >= *rows.n_rows) return;
-  const float* p = ws + static_cast<int64_t>(r) * 2 * ffn;
-  for (int j = threadIdx.x; j < ffn; j += kRowThreads) {
-    const int grp = j / 64, w = j % 64;
-    const int cg = grp * 128 + w, cu = cg + 64;
-    float g = 0.f, u = 0.f;
-    for (int z = 0; z < splits; ++z) {
-      g += p[z * split_stride + cg];
-      u += p[z * split_stride + cu];
-    }
-    const float s = g / (1.f + __expf(-g));
-    h[static_cast<int64_t>(r) * ffn + j] = __float2bfloat16_rn(s * u);
-  }
-}
-
-// Sums the split partials into split 0 (the logits [rows][vocab]) and takes argmax_lowest.
-__global__ void __launch_bounds__(kRowThreads) logits_argmax_kernel(float* __restrict__ ws, int splits,
-                                                                    int64_t split_stride, RowsDev rows,
-                                                                    int vocab, int* __restrict__ out) {
-  __shared__ float sv[kRowThreads / 32];
-  __shared__ int si[kRowThreads / 32];
-  const int r = blockIdx.x;
-  if (r >= *rows.n_rows) return;
-  float* p = ws + static_cast<int64_t>(r) * vocab;
   float bv = -FLT_MAX;
   int bi = 0x7fffffff;
-  for (int v = threadIdx.x; v < vocab; v += kRowThreads) {
-    float a = p[v];
-    for (int z = 1; z < splits; ++z) a += p[z * split_stride + v];
-    if (splits > 1) p[v] = a;
-    if (a > bv) {  // increasing v per thread: strict '>' keeps the lowest id
-      bv = a;
-      bi = v;
+  for (int m = lane; m < n_tiles; m += 32) {
+    const float2 p = amax[static_cast<int64_t>(m) * t_stride + r];
+    const int pi = __float_as_int(p.y);
+    if (p.x > bv || (p.x == bv && pi < bi)) {
+      bv = p.x;
+      bi = pi;
     }
   }
 #pragma unroll
@@ -223,22 +109,7 @@ __global__ void __launch_bounds__(kRowThreads) logits_argmax_kernel(float* __res
       bi = oi;
     }
   }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    sv[w] = bv;
-    si[w] = bi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    bv = sv[0];
-    bi = si[0];
-    for (int i = 1; i < kRowThreads / 32; ++i)
-      if (sv[i] > bv || (sv[i] == bv && si[i] < bi)) {
-        bv = sv[i];
-        bi = si[i];
-      }
-    out[r] = bi;
-  }
+  if (lane == 0) out[r] = bi;
 }
 
 }  // namespace
@@ -265,44 +136,17 @@ cudaError_t lm_init_embedding(__nv_bfloat16* emb, const __nv_bfloat16* lm, const
   return cudaGetLastError();
 }
 
-cudaError_t lm_embed_norm(const LlamaShape& m, const __nv_bfloat16* emb, RowsDev rows, int rows_cap,
-                          float* x, __nv_bfloat16* xn, cudaStream_t s) {
+cudaError_t lm_embed(const LlamaShape& m, const __nv_bfloat16* emb, RowsDev rows, int rows_cap,
+                     float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s) {
   if (rows_cap <= 0) return cudaSuccess;
-  embed_norm_kernel<<<rows_cap, kRowThreads, 0, s>>>(emb, rows, m.d, m.eps, x, xn);
+  embed_kernel<<<dim3(rows_cap, m.d / 128), 128, 0, s>>>(emb, rows, m.d, rows_cap, x, xb, ss);
   return cudaGetLastError();
 }
 
-cudaError_t lm_qkv_rope_append(const LlamaShape& m, const float* ws, int splits, int t_stride,
-                               RowsDev rows, int rows_cap, const float2* rope, KvDev kv, int layer,
-                               __nv_bfloat16* qbuf, cudaStream_t s) {
+cudaError_t lm_argmax_reduce(int n_tiles, RowsDev rows, int rows_cap, const float2* amax, int* out,
+                             cudaStream_t s) {
   if (rows_cap <= 0) return cudaSuccess;
-  qkv_rope_append_kernel<<<rows_cap, kRowThreads, 0, s>>>(
-      ws, splits, static_cast<int64_t>(t_stride) * m.qkv_out(), rows, m.n_q, m.n_kv, m.hd, rope, kv,
-      layer, qbuf);
-  return cudaGetLastError();
-}
-
-cudaError_t lm_residual_norm(const LlamaShape& m, const float* ws, int splits, int t_stride,
-                             RowsDev rows, int rows_cap, float* x, __nv_bfloat16* xn, cudaStream_t s) {
-  if (rows_cap <= 0) return cudaSuccess;
-  residual_norm_kernel<<<rows_cap, kRowThreads, 0, s>>>(ws, splits, static_cast<int64_t>(t_stride) * m.d,
-                                                        rows, m.d, m.eps, x, xn);
-  return cudaGetLastError();
-}
-
-cudaError_t lm_swiglu(const LlamaShape& m, const float* ws, int splits, int t_stride, RowsDev rows,
-                      int rows_cap, __nv_bfloat16* h, cudaStream_t s) {
-  if (rows_cap <= 0) return cudaSuccess;
-  swiglu_kernel<<<rows_cap, kRowThreads, 0, s>>>(ws, splits, static_cast<int64_t>(t_stride) * 2 * m.ffn,
-                                                 rows, m.ffn, h);
-  return cudaGetLastError();
-}
-
-cudaError_t lm_logits_argmax(int vocab, float* ws, int splits, int t_stride, RowsDev rows,
-                             int rows_cap, int* argmax_out, cudaStream_t s) {
-  if (rows_cap <= 0) return cudaSuccess;
-  logits_argmax_kernel<<<rows_cap, kRowThreads, 0, s>>>(ws, splits, static_cast<int64_t>(t_stride) * vocab,
-                                                        rows, vocab, argmax_out);
+  argmax_reduce_kernel<<<(rows_cap * 32 + 255) / 256, 256, 0, s>>>(n_tiles, rows, rows_cap, amax, out);
   return cudaGetLastError();
 }
 

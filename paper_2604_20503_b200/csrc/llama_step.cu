@@ -161,37 +161,40 @@ __global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, i
   if (i == blockDim.x - 1) *rows.n_rows = scan[i];
 }
 
-__global__ void gather_kernel(RowsDev rows, const int* __restrict__ src_of, int d, const float* __restrict__ x,
-                              float* __restrict__ xs) {
+// Compaction, pass 1: copy the surviving rows' residual (fp32 + bf16 operand copy + per-chunk
+// sums of squares) to scratch in their new order.
+__global__ void gather_kernel(RowsDev rows, const int* __restrict__ src_of, int d, int t_stride,
+                              const float* __restrict__ x, const __nv_bfloat16* __restrict__ xb,
+                              const float* __restrict__ ss, float* __restrict__ xs,
+                              __nv_bfloat16* __restrict__ xbs, float* __restrict__ sss) {
   const int r = blockIdx.x;
   if (r >= *rows.n_rows) return;
-  const float4* s = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src_of[r]) * d);
-  float4* o = reinterpret_cast<float4*>(xs + static_cast<int64_t>(r) * d);
-  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) o[c] = s[c];
+  const int src = src_of[r];
+  const float4* s4 = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src) * d);
+  float4* o4 = reinterpret_cast<float4*>(xs + static_cast<int64_t>(r) * d);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) o4[c] = s4[c];
+  const uint4* b4 = reinterpret_cast<const uint4*>(xb + static_cast<int64_t>(src) * d);
+  uint4* ob4 = reinterpret_cast<uint4*>(xbs + static_cast<int64_t>(r) * d);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) ob4[c] = b4[c];
+  for (int c = threadIdx.x; c < d / 128; c += blockDim.x)
+    sss[static_cast<int64_t>(c) * t_stride + r] = ss[static_cast<int64_t>(c) * t_stride + src];
 }
 
-__global__ void scatter_back_norm_kernel(RowsDev rows, int d, float eps, const float* __restrict__ xs,
-                                         float* __restrict__ x, __nv_bfloat16* __restrict__ xn) {
-  __shared__ float red[8];
+// Compaction, pass 2: scratch -> live buffers.
+__global__ void scatter_back_kernel(RowsDev rows, int d, int t_stride, const float* __restrict__ xs,
+                                    const __nv_bfloat16* __restrict__ xbs, const float* __restrict__ sss,
+                                    float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                                    float* __restrict__ ss) {
   const int r = blockIdx.x;
   if (r >= *rows.n_rows) return;
-  const float* s = xs + static_cast<int64_t>(r) * d;
-  float* o = x + static_cast<int64_t>(r) * d;
-  float ss = 0.f;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    const float v = s[c];
-    o[c] = v;
-    ss += v * v;
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  float tot = 0.f;
-  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += red[i];
-  const float inv = rsqrtf(tot / d + eps);
-  for (int c = threadIdx.x; c < d; c += blockDim.x)
-    xn[static_cast<int64_t>(r) * d + c] = __float2bfloat16_rn(s[c] * inv);
+  const float4* s4 = reinterpret_cast<const float4*>(xs + static_cast<int64_t>(r) * d);
+  float4* o4 = reinterpret_cast<float4*>(x + static_cast<int64_t>(r) * d);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) o4[c] = s4[c];
+  const uint4* b4 = reinterpret_cast<const uint4*>(xbs + static_cast<int64_t>(r) * d);
+  uint4* ob4 = reinterpret_cast<uint4*>(xb + static_cast<int64_t>(r) * d);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) ob4[c] = b4[c];
+  for (int c = threadIdx.x; c < d / 128; c += blockDim.x)
+    ss[static_cast<int64_t>(c) * t_stride + r] = sss[static_cast<int64_t>(c) * t_stride + r];
 }
 
 __global__ void accept_commit_kernel(LmSlots sl, LmReqState rq, RowsDev rows, StepCtl ctl,
@@ -357,11 +360,12 @@ cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, 
   frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, layer, src_of);
   return cudaGetLastError();
 }
-cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, float eps, float* x, float* xs,
-                           __nv_bfloat16* xn, int rows_cap, cudaStream_t s) {
-  if (rows_cap <= 0) return cudaSuccess;
-  gather_kernel<<<rows_cap, 256, 0, s>>>(rows, src_of, d, x, xs);
-  scatter_back_norm_kernel<<<rows_cap, 256, 0, s>>>(rows, d, eps, xs, x, xn);
+cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, int t_stride, float* x,
+                           __nv_bfloat16* xb, float* ss, float* xs, __nv_bfloat16* xbs, float* sss,
+                           cudaStream_t s) {
+  if (t_stride <= 0) return cudaSuccess;
+  gather_kernel<<<t_stride, 256, 0, s>>>(rows, src_of, d, t_stride, x, xb, ss, xs, xbs, sss);
+  scatter_back_kernel<<<t_stride, 256, 0, s>>>(rows, d, t_stride, xs, xbs, sss, x, xb, ss);
   return cudaGetLastError();
 }
 cudaError_t lm_accept_commit(LmSlots sl, LmReqState rq, RowsDev rows, StepCtl ctl,

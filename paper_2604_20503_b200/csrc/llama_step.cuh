@@ -62,11 +62,13 @@ cudaError_t lm_verify_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n, int l
 cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,
                          int64_t split_stride, int vocab, int k_thr, int rows_cap, cudaStream_t s);
 // K4 frontier: per request earliest failing row prunes the suffix; compacts the row set.
-// src_of[new_row] = old row; x is gathered through xs (fp32 [rows][d]) and re-normalised.
+// src_of[new_row] = old row; the residual (x fp32, xb bf16, ss per-chunk sums of squares) is
+// gathered through scratch buffers of the same shapes.
 cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
                                 int* src_of, cudaStream_t s);
-cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, float eps, float* x, float* xs,
-                           __nv_bfloat16* xn, int rows_cap, cudaStream_t s);
+cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, int t_stride, float* x,
+                           __nv_bfloat16* xb, float* ss, float* xs, __nv_bfloat16* xbs, float* sss,
+                           cudaStream_t s);
 // K5: greedy acceptance (+ early-exit outcome bookkeeping) + commit + exempt rule.
 cudaError_t lm_accept_commit(LmSlots sl, LmReqState rq, RowsDev rows, StepCtl ctl,
                              faser_round_result* results, cudaStream_t s);

@@ -1,26 +1,31 @@
-// tc_gemm.cu — tcgen05/TMEM GEMM for the draft and verification forwards (K1/K2).
+// tc_gemm.cu — tcgen05/TMEM GEMM with fused split-K reduction and row epilogues, the
+// projection engine of the draft (K1) and verification (K2) forwards.
 //
-//   ws[z][t][n] = sum_{k in split z} W[n][k] * X[t][k]        (bf16 x bf16 -> fp32)
+//   D[n][t] = sum_k W[n][k] * X[t][k]           (bf16 x bf16 -> fp32 in TMEM)
 //
-// W is a weight matrix [N_out][K] (row-major = K-major), X the activations [T][K] of the
-// ragged verify rows (T = sum k_i) or draft rows. The kernel is "swap-AB": the weights fill
-// the 128-wide UMMA M dimension and the (few) tokens are the N dimension, so a verify batch
-// of T = 5..256 rows is one N tile and the weights are streamed from HBM exactly once per
-// split. Roles inside a 128-thread CTA:
+// "Swap-AB": the weights fill the 128-wide UMMA M dimension and the verify/draft rows are the
+// N dimension, so a batch of T = 1..256 rows is one N tile and the weights stream from HBM
+// exactly once. Roles in a 128-thread CTA:
 //   warp 0 / lane 0 : TMA producer (W tile 128x64, X tile BNx64 per stage, SWIZZLE_128B)
-//   warp 1 / lane 0 : tcgen05.mma issuer (UMMA 128xBNx16, accumulator in TMEM)
+//   warp 1 / lane 0 : tcgen05.mma issuer (UMMA 128xBNx16), commits free smem stages
 //   warp 2          : TMEM allocator
-//   warps 0-3       : epilogue (tcgen05.ld 32 lanes x 16 columns -> fp32 partial tile)
-// K is split across gridDim.z so that small-T launches still cover all 148 SMs; partial
-// sums are reduced in a fixed order by the consumer kernel (deterministic, and independent
-// of which rows survive early-exit pruning: the split count is fixed per forward).
-// T can be read from device memory (t_dev) so that a forward whose row set shrinks on the
-// device (early-exit compaction) launches once with its initial grid; tiles past the live
-// row count exit immediately.
+//   warps 0-3       : epilogue
+// K is split over gridDim.z so small-T launches cover all SMs. Every split CTA writes its fp32
+// partial tile; the LAST CTA to arrive on the tile's counter sums the partials in split order
+// (deterministic, independent of which rows survive early-exit pruning because the split count
+// is fixed per forward) and runs the fused epilogue from a shared-memory copy of the tile:
+//   store | residual add (+ per-tile sum of squares for the next RMSNorm) | RoPE + q write +
+//   paged KV append | SwiGLU | logits (+ per-tile argmax).
+// RMSNorm is folded: the GEMM consumes the un-normalised residual (bf16) and scales each token
+// column by rsqrt(mean(x^2)+eps) in the epilogue (W.(x*r) = r*(W.x)); gamma = 1 for these
+// random-init models.
+// Launch uses programmatic dependent launch: the prologue (barrier init, TMEM alloc, tensor-map
+// prefetch) overlaps the previous kernel; every dependent read is after griddepcontrol.wait.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cfloat>
 #include <cstdio>
 #include <mutex>
 
@@ -38,38 +43,56 @@ constexpr int kXBox = 32;                    // activation TMA box rows
 
 template <int BN>
 struct Cfg {
-  static constexpr int kStages = BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4;
+  static constexpr int kStages = 4;  // BN <= 64: ~100 KB smem -> 2 CTAs / SM
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+  static constexpr int kPipe = kStages * kStageBytes;
+  static constexpr int kTile = BN * kBM * 4;  // fp32 epilogue staging tile
+  static constexpr int kSmem = 1024 + (kPipe > kTile ? kPipe : kTile) + 12288;
 };
 
-template <int BN>
-__global__ void __launch_bounds__(128, 1)
-    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                   float* __restrict__ ws, int n_out, int t_stride, const int* __restrict__ t_dev,
-                   int t_host, int kb_total, int kb_per_split) {
-  using C = Cfg<BN>;
-  const int T = t_dev ? min(*t_dev, t_host) : t_host;
-  const int n0 = blockIdx.y * BN;
-  if (n0 >= T) return;
-  const int m0 = blockIdx.x * kBM;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int kb1 = min(kb_total, kb0 + kb_per_split);
-  if (kb0 >= kb1) return;
-  const int nkb = kb1 - kb0;
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_cta(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+template <int BN>
+__global__ void __launch_bounds__(128, 2)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ EpiArgs ea, int n_out, int kb_total, int kb_per_split, int splits) {
+  using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint8_t* aux = smem + (C::kPipe > C::kTile ? C::kPipe : C::kTile);
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + C::kStages;
   uint64_t* accum = empty + C::kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  float* s_rs = reinterpret_cast<float*>(aux + 256);  // [256] per-token RMSNorm scale
+  float* s_red = s_rs + 256;                          // [4][BN] per-warp partials
+  int* s_i0 = reinterpret_cast<int*>(s_red + 4 * 256);  // [4][BN] per-warp argmax ids
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kBM;
+  const int n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb1 = min(kb_total, kb0 + kb_per_split);
+  const int nkb = kb1 - kb0;
+
   if (threadIdx.x == 0) {
     sm100::tma_prefetch(&tmW);
     sm100::tma_prefetch(&tmX);
@@ -80,6 +103,10 @@ __global__ void __launch_bounds__(128, 1)
     sm100::mbar_init(accum, 1);
     sm100::fence_mbar_init();
   }
+  pdl_trigger();
+  pdl_wait();  // everything below may read the previous kernel's output
+  const int T = ea.n_rows ? min(*ea.n_rows, ea.t_stride) : ea.t_stride;
+  if (n0 >= T || nkb <= 0) return;  // uniform per CTA, before any TMEM / TMA use
   if (warp == 2) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
@@ -89,15 +116,16 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0 && lane == 0) {
     // ---------------------------------------------------------------- TMA producer
     const uint64_t pol_w = sm100::policy_evict_first();
+    const int xboxes = (min(BN, T - n0) + kXBox - 1) / kXBox;  // skip all-padding activation boxes
+    const uint32_t stage_bytes = kABytes + xboxes * kXBox * kBK * 2;
     for (int i = 0; i < nkb; ++i) {
       const int s = i % C::kStages;
       const uint32_t ph = (i / C::kStages) & 1;
       sm100::mbar_wait(&empty[s], ph ^ 1);
-      sm100::mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+      sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
       const int kc = (kb0 + i) * kBK;
       sm100::tma_load_2d_hint(sA + s * kABytes, &tmW, &full[s], kc, m0, pol_w);
-#pragma unroll
-      for (int j = 0; j < (BN + kXBox - 1) / kXBox; ++j)
+      for (int j = 0; j < xboxes; ++j)
         sm100::tma_load_2d(sB + s * C::kBBytes + j * kXBox * 128, &tmX, &full[s], kc, n0 + j * kXBox);
     }
   } else if (warp == 1 && lane == 0) {
@@ -111,10 +139,8 @@ __global__ void __launch_bounds__(128, 1)
       const uint64_t da = sm100::desc_sw128(sm100::smem_u32(sA + s * kABytes));
       const uint64_t db = sm100::desc_sw128(sm100::smem_u32(sB + s * C::kBBytes));
 #pragma unroll
-      for (int k = 0; k < kBK / kUmmaK; ++k) {
-        // advance along K inside the 128-byte swizzle atom: +32 bytes (>>4 = 2) per step
+      for (int k = 0; k < kBK / kUmmaK; ++k)  // +32 bytes along K inside the swizzle atom
         sm100::mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-      }
       sm100::mma_commit(&empty[s]);
     }
     sm100::mma_commit(accum);
@@ -124,24 +150,164 @@ __global__ void __launch_bounds__(128, 1)
   // ------------------------------------------------------------------ epilogue
   sm100::mbar_wait(accum, 0);
   sm100::tc_fence_after();
-  const int row = m0 + warp * 32 + lane;  // output feature of this thread
-  float* out = ws + static_cast<size_t>(blockIdx.z) * t_stride * n_out;
+  const int tn = min(BN, T - n0);          // live tokens of this tile
+  const int r = warp * 32 + lane;          // tile row owned in the TMEM read-out
+  float* S = reinterpret_cast<float*>(smem);  // [BN][128] fp32 staging (pipeline smem is free now)
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
-    if (n0 + c0 >= T) break;
+    if (c0 >= tn) break;
     float v[16];
     sm100::tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-    if (row < n_out) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int t = n0 + c0 + i;
-        if (t < T) out[static_cast<size_t>(t) * n_out + row] = v[i];
-      }
-    }
+    for (int i = 0; i < 16; ++i) S[(c0 + i) * kBM + r] = v[i];
   }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 2) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+  // Split-K: the `splits` CTAs of this tile are one thread-block cluster. Each owns a slice of the
+  // tile's tokens and sums that slice over every CTA's partial through DSMEM in rank order
+  // (deterministic), then runs the epilogue on its slice.
+  int ts = 0, te = tn;
+  if (splits > 1) {
+    cluster_sync();
+    const int per = (tn + splits - 1) / splits;
+    ts = min(tn, static_cast<int>(blockIdx.z) * per);
+    te = min(tn, ts + per);
+    const uint32_t base = sm100::smem_u32(S);
+    uint32_t rb[16];
+#pragma unroll
+    for (int z = 0; z < 16; ++z) rb[z] = z < splits ? map_cta(base, z) : 0u;
+    const int c4 = threadIdx.x & 31, tq = threadIdx.x >> 5;  // 4 rows (float4) x 4 tokens per pass
+    for (int t = ts + tq; t < te; t += 4) {
+      const uint32_t off = (t * kBM + c4 * 4) * 4;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int z = 0; z < 16; ++z) {
+        if (z < splits) {
+          const float4 v = ld_dsmem4(rb[z] + off);
+          a.x += v.x;
+          a.y += v.y;
+          a.z += v.z;
+          a.w += v.w;
+        }
+      }
+      // only this CTA reads its own slice rows, so the in-place write is race-free
+      *reinterpret_cast<float4*>(S + t * kBM + c4 * 4) = a;
+    }
+    __syncthreads();
+  }
+  // Per-token prologue (one thread per token of the slice): RMSNorm scale of the un-normalised
+  // residual input, and for the QKV epilogue the token's position and KV page.
+  int* s_pos = s_i0 + 4 * 256;  // [256]
+  int* s_page = s_pos + 256;    // [256]
+  for (int t = ts + threadIdx.x; t < te; t += 128) {
+    float rs = 1.f;
+    if (ea.ss_in) {
+      float ss = 0.f;
+#pragma unroll 4
+      for (int c = 0; c < ea.ss_chunks; ++c) ss += ea.ss_in[static_cast<size_t>(c) * ea.t_stride + n0 + t];
+      rs = rsqrtf(ss / ea.d_norm + ea.eps);
+    }
+    s_rs[t] = rs;
+    if (ea.mode == kEpiQkv) {
+      const int row = n0 + t;
+      const int pos = ea.rows.row_pos[row];
+      const int slot = ea.rows.req_slot[ea.rows.row_req[row]];
+      s_pos[t] = pos;
+      s_page[t] = ea.kv.ptab[static_cast<size_t>(slot) * ea.kv.max_pages + pos / kPage];
+    }
+  }
+  __syncthreads();
+
+  // Token-per-warp passes: lane owns 4 consecutive tile rows (float4), a warp covers the 128
+  // rows of one token, 4 tokens per pass.
+  const int mode = ea.mode;
+  const int c4 = lane * 4;
+  if (mode == kEpiStore || mode == kEpiResid || mode == kEpiLogits) {
+    for (int t = ts + warp; t < te; t += 4) {
+      const float rs = s_rs[t];
+      float4 a = *reinterpret_cast<const float4*>(S + t * kBM + c4);
+      const size_t idx = static_cast<size_t>(n0 + t) * n_out + m0 + c4;
+      if (mode == kEpiStore) {
+        *reinterpret_cast<float4*>(ea.out + idx) = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+      } else if (mode == kEpiResid) {
+        const float4 xv = *reinterpret_cast<const float4*>(ea.x + idx);
+        a = make_float4(xv.x + a.x, xv.y + a.y, xv.z + a.z, xv.w + a.w);
+        *reinterpret_cast<float4*>(ea.x + idx) = a;
+        __nv_bfloat162 b0 = __floats2bfloat162_rn(a.x, a.y), b1 = __floats2bfloat162_rn(a.z, a.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&b0);
+        pk.y = *reinterpret_cast<uint32_t*>(&b1);
+        *reinterpret_cast<uint2*>(ea.xb + idx) = pk;
+        float q = (a.x * a.x + a.y * a.y) + (a.z * a.z + a.w * a.w);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) ea.ss_out[static_cast<size_t>(blockIdx.x) * ea.t_stride + n0 + t] = q;
+      } else {  // kEpiLogits
+        a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+        *reinterpret_cast<float4*>(ea.logits + idx) = a;
+        float bv = a.x;
+        int bi = m0 + c4;
+        if (a.y > bv) { bv = a.y; bi = m0 + c4 + 1; }
+        if (a.z > bv) { bv = a.z; bi = m0 + c4 + 2; }
+        if (a.w > bv) { bv = a.w; bi = m0 + c4 + 3; }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        if (lane == 0) ea.amax[static_cast<size_t>(blockIdx.x) * ea.t_stride + n0 + t] = make_float2(bv, __int_as_float(bi));
+      }
+    }
+  } else if (mode == kEpiQkv) {
+    const int hd = ea.hd, half = hd >> 1;
+    constexpr int pairs = kBM / 2;  // 64 rotation pairs per 128-row tile
+    for (int e = threadIdx.x; e < (te - ts) * pairs; e += 128) {
+      const int t = ts + e / pairs, p = e % pairs;
+      const int hl = p / half, i = p % half;
+      const int ra = hl * hd + i, rb = ra + half;
+      const int head = (m0 + ra) / hd;
+      const float rs = s_rs[t];
+      float a = S[t * kBM + ra] * rs, b = S[t * kBM + rb] * rs;
+      const int row = n0 + t;
+      const int pos = s_pos[t];
+      if (head < ea.n_q + ea.n_kv) {
+        const float2 cs = ea.rope[static_cast<size_t>(pos) * half + i];
+        const float ra2 = a * cs.x - b * cs.y, rb2 = b * cs.x + a * cs.y;
+        a = ra2;
+        b = rb2;
+      }
+      if (head < ea.n_q) {
+        __nv_bfloat16* qd = ea.q + (static_cast<size_t>(row) * ea.n_q + head) * hd;
+        qd[i] = __float2bfloat16_rn(a);
+        qd[i + half] = __float2bfloat16_rn(b);
+      } else {
+        const bool is_v = head >= ea.n_q + ea.n_kv;
+        const int kvh = is_v ? head - ea.n_q - ea.n_kv : head - ea.n_q;
+        __nv_bfloat16* dst = ea.kv.pool + ea.layer * ea.kv.layer_stride +
+                             ((static_cast<size_t>(s_page[t]) * ea.n_kv + kvh) * 2 + (is_v ? 1 : 0)) * kPage * hd +
+                             (pos % kPage) * hd;
+        dst[i] = __float2bfloat16_rn(a);
+        dst[i + half] = __float2bfloat16_rn(b);
+      }
+    }
+  } else {  // kEpiSwiglu: 128-row group = 64 gate rows then 64 up rows
+    const int j0 = m0 >> 1;
+    for (int e = threadIdx.x; e < (te - ts) * 32; e += 128) {
+      const int t = ts + (e >> 5), w = (e & 31) * 2;
+      const float rs = s_rs[t];
+      const float2 g = *reinterpret_cast<const float2*>(S + t * kBM + w);
+      const float2 u = *reinterpret_cast<const float2*>(S + t * kBM + 64 + w);
+      const float g0 = g.x * rs, g1 = g.y * rs;
+      const float h0 = g0 / (1.f + __expf(-g0)) * (u.x * rs), h1 = g1 / (1.f + __expf(-g1)) * (u.y * rs);
+      *reinterpret_cast<__nv_bfloat162*>(ea.h + static_cast<size_t>(n0 + t) * ea.ffn + j0 + w) = __floats2bfloat162_rn(h0, h1);
+    }
+  }
+  if (splits > 1) cluster_sync();  // peers may still be reading this CTA's partial
 }
 
 // ------------------------------------------------------------------ host side
@@ -164,24 +330,31 @@ EncodeTiledFn encode_fn() {
 }
 
 template <int BN>
-void set_smem_attr() {
+cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int splits, const EpiArgs& ea,
+                      cudaStream_t s) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
+    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
+    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
-}
-
-template <int BN>
-cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, float* ws, int t_stride,
-                      const int* t_dev, int t, int splits, cudaStream_t s) {
-  set_smem_attr<BN>();
   const int kb_total = w.k / kBK;
   const int kps = (kb_total + splits - 1) / splits;
   const int z = (kb_total + kps - 1) / kps;
-  dim3 grid(w.rows / kBM, (t + BN - 1) / BN, z);
-  gemm_tn_kernel<BN><<<grid, 128, Cfg<BN>::kSmem, s>>>(w.map, x.map, ws, w.rows, t_stride, t_dev, t,
-                                                       kb_total, kps);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(w.rows / kBM, (t + BN - 1) / BN, z);
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = Cfg<BN>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = z;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN>, w.map, x.map, ea, w.rows, kb_total, kps, z);
 }
 
 }  // namespace
@@ -211,33 +384,43 @@ cudaError_t make_act_operand(GemmOperand* op, const void* x, int rows_cap, int k
   return make_operand(op, x, rows_cap, k, kXBox);
 }
 
-int gemm_bn_for(int t) { return t <= 32 ? 32 : t <= 64 ? 64 : t <= 128 ? 128 : 256; }
+// Tile width along the rows (tokens): the widest tile that still gives one full wave of CTAs;
+// below that, 32-row tiles plus split-K (cluster of <= kMaxSplit CTAs).
+constexpr int kMaxSplit = 8;
 
-int gemm_splits_for(int n_out, int t, int k, int num_sms) {
-  const int bn = gemm_bn_for(t);
-  const int tiles = (n_out / kBM) * ((t + bn - 1) / bn);
+GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
+  GemmPlan p;
+  const int mt = n_out / kBM;
+  p.bn = 32;
+  for (int bn : {256, 128, 64}) {
+    if (mt * ((t + bn - 1) / bn) >= num_sms) {
+      p.bn = bn;
+      break;
+    }
+  }
+  const int tiles = mt * ((t + p.bn - 1) / p.bn);
+  const int slots = num_sms * (p.bn <= 64 ? 2 : 1);  // resident CTAs per wave
   const int kb = k / kBK;
-  int s = (num_sms + tiles - 1) / tiles;   // one wave of CTAs (1 CTA / SM)
+  int s = tiles >= slots / 2 ? 1 : slots / tiles;   // never spill into a second wave
+  const int max_s = kb / 4 > 0 ? kb / 4 : 1;         // >= 4 k-blocks (256 of K) per split
+  s = s > max_s ? max_s : s;
+  s = s > kMaxSplit ? kMaxSplit : s;
   s = s < 1 ? 1 : s;
-  const int max_s = kb / 4 > 0 ? kb / 4 : 1;  // >= 4 k-blocks (256 of K) per split
-  return s > max_s ? max_s : s;
+  const int kps = (kb + s - 1) / s;
+  p.splits = (kb + kps - 1) / kps;
+  p.tiles = tiles;
+  return p;
 }
 
-int gemm_effective_splits(int k, int splits) {
-  const int kb = k / kBK;
-  const int kps = (kb + splits - 1) / splits;
-  return (kb + kps - 1) / kps;
-}
-
-cudaError_t gemm_tn(const GemmOperand& w, const GemmOperand& x, float* ws, int t_stride,
-                    const int* t_dev, int t, int splits, cudaStream_t s) {
+cudaError_t gemm_fused(const GemmOperand& w, const GemmOperand& x, int t, const GemmPlan& p, const EpiArgs& epi,
+                       cudaStream_t s) {
   if (t <= 0) return cudaSuccess;
   if (w.k != x.k) return cudaErrorInvalidValue;
-  switch (gemm_bn_for(t)) {
-    case 32: return launch_bn<32>(w, x, ws, t_stride, t_dev, t, splits, s);
-    case 64: return launch_bn<64>(w, x, ws, t_stride, t_dev, t, splits, s);
-    case 128: return launch_bn<128>(w, x, ws, t_stride, t_dev, t, splits, s);
-    default: return launch_bn<256>(w, x, ws, t_stride, t_dev, t, splits, s);
+  switch (p.bn) {
+    case 32: return launch_bn<32>(w, x, t, p.splits, epi, s);
+    case 64: return launch_bn<64>(w, x, t, p.splits, epi, s);
+    case 128: return launch_bn<128>(w, x, t, p.splits, epi, s);
+    default: return launch_bn<256>(w, x, t, p.splits, epi, s);
   }
 }
 

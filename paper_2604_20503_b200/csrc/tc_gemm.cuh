@@ -1,7 +1,10 @@
-// tc_gemm.cuh — host interface of the tcgen05 swap-AB GEMM (see tc_gemm.cu).
+// tc_gemm.cuh — host interface of the tcgen05 swap-AB GEMM with fused epilogues (tc_gemm.cu).
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include "llama.cuh"
 
 namespace faser {
 
@@ -16,14 +19,52 @@ struct GemmOperand {
 cudaError_t make_weight_operand(GemmOperand* op, const void* w, int n_out, int k);  // box 128 rows
 cudaError_t make_act_operand(GemmOperand* op, const void* x, int rows_cap, int k);  // box 32 rows
 
-// Tile width along tokens and the K split a launch over T rows will use.
-int gemm_bn_for(int t);
-int gemm_splits_for(int n_out, int t, int k, int num_sms);
-int gemm_effective_splits(int k, int splits);
+enum EpiMode : int {
+  kEpiStore = 0,   // out[t][n] = acc * rs[t]                        (fp32)
+  kEpiResid = 1,   // x[t][n] += acc; xb = bf16(x); ss_out[mtile][t] = sum_n x^2 over the tile
+  kEpiQkv = 2,     // RoPE(q,k) at row_pos; q -> bf16 [t][n_q*hd]; k,v -> paged KV cache
+  kEpiSwiglu = 3,  // h[t][j] = bf16(silu(gate*rs) * up*rs), gate/up interleaved in 64-row groups
+  kEpiLogits = 4,  // logits[t][v] = acc*rs (fp32) + per-tile (max, lowest idx) per token
+};
 
-// ws[z][t][n] (z < effective splits, t < T, row stride n_out, split stride t_stride*n_out)
-// = partial of sum_k W[n][k] X[t][k]. T = min(*t_dev, t) when t_dev != nullptr.
-cudaError_t gemm_tn(const GemmOperand& w, const GemmOperand& x, float* ws, int t_stride,
-                    const int* t_dev, int t, int splits, cudaStream_t s);
+// Everything the fused epilogue may need (unused fields ignored per mode).
+struct EpiArgs {
+  int mode = kEpiStore;
+  int t_stride = 0;          // row capacity of this launch (host T)
+  const int* n_rows = nullptr;  // live rows (device), nullptr -> t_stride
+  // RMSNorm folded into the epilogue: acc *= rsqrt(sum_c ss_in[c][t] / d_norm + eps)
+  const float* ss_in = nullptr;
+  int ss_chunks = 0, d_norm = 0;
+  float eps = 0.f;
+  float* out = nullptr;                  // kEpiStore
+  float* x = nullptr;                    // kEpiResid
+  __nv_bfloat16* xb = nullptr;           // kEpiResid
+  float* ss_out = nullptr;               // kEpiResid [n_out/128][t_stride]
+  RowsDev rows{};                        // kEpiQkv
+  const float2* rope = nullptr;          // kEpiQkv [pos][hd/2] (cos, sin)
+  KvDev kv{};                            // kEpiQkv
+  int layer = 0, n_q = 0, n_kv = 0, hd = 0;
+  __nv_bfloat16* q = nullptr;            // kEpiQkv [t][n_q*hd]
+  __nv_bfloat16* h = nullptr;            // kEpiSwiglu [t][ffn]
+  int ffn = 0;
+  float* logits = nullptr;               // kEpiLogits [t][n_out]
+  float2* amax = nullptr;                // kEpiLogits [n_out/128][t_stride] (value, idx bits)
+};
+
+// Launch plan: token-tile width and K split (the splits of a tile form one thread-block cluster
+// and reduce through DSMEM). Fixed per forward so surviving rows' numerics do not depend on
+// early-exit pruning.
+struct GemmPlan {
+  int bn = 32;
+  int splits = 1;
+  int tiles = 0;
+};
+GemmPlan gemm_plan(int n_out, int t, int k, int num_sms);
+
+// D[n][t] = sum_k W[n][k] X[t][k] over T = min(*n_rows, t) rows, epilogue per `epi`.
+// Launched with programmatic stream serialization: the prologue overlaps the previous kernel;
+// all dependent reads happen after griddepcontrol.wait.
+cudaError_t gemm_fused(const GemmOperand& w, const GemmOperand& x, int t, const GemmPlan& p,
+                       const EpiArgs& epi, cudaStream_t s);
 
 }  // namespace faser

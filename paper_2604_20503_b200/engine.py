@@ -283,6 +283,12 @@ class ServingEngine:
         _check(lib().faser_debug_drafted(self.h, _ptr(buf), self.cfg.max_batch, C.byref(n)), self.h)
         return buf[:n.value]
 
+    def debug_weights(self, model, which, layer, offset, n):
+        out = np.zeros(max(n, 1), np.uint16)
+        _check(lib().faser_debug_weights(self.h, model, which, layer, C.c_int64(offset), n, _ptr(out)),
+               self.h)
+        return out[:n]
+
     def debug_kv_pages(self, req_id):
         buf = np.zeros(4096, np.int32)
         n = C.c_int32()

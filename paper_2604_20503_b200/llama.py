@@ -25,7 +25,7 @@ def _pair(draft, target, b=12345):
 
 
 # Target bigram strength sets the acceptance rate (tuned on B200).
-TARGET_BIGRAM = {"tiny": 4.0, "cfg3": 22.0, "cfg4": 22.0}
+TARGET_BIGRAM = {"tiny": 2.0, "cfg3": 22.0, "cfg4": 22.0}
 DRAFT_BIGRAM = 24.0
 
 

@@ -26,7 +26,7 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("n_out,T,K", SHAPES)
-@pytest.mark.parametrize("splits", [0, 1])
+@pytest.mark.parametrize("splits", [0, 1, 3])
 def test_gemm_matches_fp32(L, n_out, T, K, splits):
     import torch
     g = torch.Generator(device="cuda").manual_seed(n_out * 7 + T * 3 + K)

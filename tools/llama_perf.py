@@ -29,5 +29,11 @@ for s in range(10):
     tok += sum(r.committed for r in res)
     ts.append(eng.last_step_timing())
 ts = np.array(ts)
+if os.environ.get("PROFILE_ONE_STEP"):
+    import torch
+    torch.cuda.profiler.start()
+    eng.step()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 print(f"{preset} B={B} k={k}: draft {ts[:,0].mean():.3f} ms verify {ts[:,1].mean():.3f} ms step {ts[:,2].mean():.3f} ms; "
       f"{tok / (ts[:,2].sum() / 1e3):.0f} tok/s device; launches {eng.kernel_launches()}")
