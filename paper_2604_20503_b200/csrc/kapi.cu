@@ -29,6 +29,9 @@ using namespace faser;
 extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, int32_t n_out,
                                                int32_t t, int32_t k, int32_t bn, int32_t splits,
                                                void* stream) {
+  // bn may carry a pipeline-depth request in its upper bits: 1000 + bn = shallow, 2000 + bn = deep
+  int depth = bn / 1000;
+  bn %= 1000;
   if (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256) return FASER_EINVAL;
   if (!w || !x || !out || n_out <= 0 || t < 0 || k <= 0) return FASER_EINVAL;
   if (n_out % 128 || k % 64) return FASER_EINVAL;
@@ -41,6 +44,8 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
   if (make_act_operand(&X, x, t, k) != cudaSuccess) return FASER_ECUDA;
   GemmPlan plan = gemm_plan(n_out, t, k, num_sms());
   if (bn > 0) plan.bn = bn;
+  if (depth == 1) plan.deep = false;
+  if (depth == 2) plan.deep = true;
   if (splits > 0) {  // caller-forced split count (cluster size <= 8)
     const int kb = k / 64, s1 = splits < 8 ? splits : 8;
     const int kps = (kb + s1 - 1) / s1;

@@ -6,13 +6,16 @@
 // (m = row*G + g), so a verify of k_i+... rows x 8 heads is one or a few 16-row tiles and the
 // KV page is read once per (request, kv head) tile. QK^T and PV run on mma.sync bf16
 // (m16n8k16, fp32 accumulate); K/V pages (64 tokens x head_dim, contiguous) are staged into
-// XOR-swizzled shared memory with cp.async, double-buffered.
+// XOR-swizzled shared memory with a 3-stage cp.async pipeline.
 // Two work splits:
-//   KEYS mode (few query rows, decode/verify): the 4 warps share one 16-row M tile and split
-//            each 64-key page 4 ways; partial softmax states are merged through smem.
-//   ROWS mode (>= 64 packed rows, long verify / prefill): each warp owns a 16-row M tile and
-//            walks all keys of the page.
-// Long contexts with few CTAs are split over KV (flash-decoding); a combine kernel merges.
+//   GROUP mode (<= 64 packed rows, decode/verify): ONE CTA per (request, kv head) holds all
+//            of its 1/2/4 M tiles, so each KV page is read once; warps split the page's four
+//            16-key chunks among the warps sharing an M tile and merge through smem.
+//   ROWS mode (> 64 packed rows, long verify / prefill): each warp owns a 16-row M tile and
+//            walks all keys of the page; CTAs cover 64 packed rows each.
+// Few CTAs + long contexts split over KV (flash-decoding); the LAST split CTA to finish a
+// (request, kv head, block) merges the partial softmax states in split order (deterministic),
+// so there is no separate combine launch.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -67,15 +70,17 @@ template <int HD, bool ROWS>
 __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int layer, int n_q, int n_kv,
                                                    const __nv_bfloat16* __restrict__ qbuf,
                                                    __nv_bfloat16* __restrict__ obuf, float* __restrict__ part_o,
-                                                   float2* __restrict__ part_ml, int n_split, int rows_cap,
-                                                   float scale_log2) {
+                                                   float2* __restrict__ part_ml, int* __restrict__ counters,
+                                                   int n_split, int rows_cap, int n_blocks, float scale_log2) {
+  constexpr int kStages = 3;
   constexpr int kChunks = HD / 8;          // 16-byte chunks per K/V row
   constexpr int kTileBytes = 64 * HD * 2;  // one K (or V) page
   constexpr int kKS = HD / 16;             // k-steps over head_dim
   constexpr int kDT = HD / 8;              // 8-wide dim tiles of O
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sK[2] = {smem, smem + 2 * kTileBytes};
-  uint8_t* sV[2] = {smem + kTileBytes, smem + 3 * kTileBytes};
+  __shared__ int s_last;
+  // let the next (PDL-launched) GEMM start streaming its weights while attention runs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int req = blockIdx.x, kvh = blockIdx.y;
   const int nr = rows.req_n[req];
@@ -83,9 +88,13 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   const int M = nr * G;
   const int blk = blockIdx.z / n_split, sp = blockIdx.z % n_split;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta_m0 = ROWS ? blk * 64 : blk * 16;
+  const int cta_m0 = ROWS ? blk * 64 : 0;
   if (cta_m0 >= M) return;
-  const int cta_m1 = min(M, cta_m0 + (ROWS ? 64 : 16));
+  const int cta_m1 = ROWS ? min(M, cta_m0 + 64) : M;
+  // GROUP mode: nmt M tiles, warps (mt = warp % nmt) share tile mt and take every nkg-th chunk
+  const int nmt = ROWS ? 4 : (M <= 16 ? 1 : M <= 32 ? 2 : 4);
+  const int nkg = 4 / nmt;
+  const int mt = warp % nmt, kg = warp / nmt;
   const int first = rows.req_first[req], pos0 = rows.req_pos0[req];
   const int slot = rows.req_slot[req];
   const int key_end = pos0 + (cta_m1 - 1) / G + 1;
@@ -94,12 +103,12 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   const int t0 = sp * tps, t1 = min(tiles, t0 + tps);
 
   // ---- Q fragments of this warp's 16-row tile
-  const int mt0 = ROWS ? cta_m0 + warp * 16 : cta_m0;
+  const int mt0 = cta_m0 + mt * 16;
   const int mlo = mt0 + (lane >> 2), mhi = mlo + 8;
   uint32_t qa[kKS][4];
   {
     const int rlo = mlo / G, glo = mlo % G, rhi = mhi / G, ghi = mhi % G;
-    const bool vlo = mlo < M, vhi = mhi < M;
+    const bool vlo = mlo < cta_m1, vhi = mhi < cta_m1;
     const __nv_bfloat16* qlo = qbuf + (static_cast<int64_t>(first + (vlo ? rlo : 0)) * n_q + kvh * G + glo) * HD;
     const __nv_bfloat16* qhi = qbuf + (static_cast<int64_t>(first + (vhi ? rhi : 0)) * n_q + kvh * G + ghi) * HD;
 #pragma unroll
@@ -112,6 +121,8 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
     }
   }
   const int lim_lo = pos0 + mlo / G, lim_hi = pos0 + mhi / G;  // last visible key per row
+  // warp-uniform: last key any row of this warp's tile can see (-1: tile past the live rows)
+  const int warp_lim = mt0 < cta_m1 ? pos0 + (min(mt0 + 15, cta_m1 - 1)) / G : -1;
 
   float o[kDT][4];
 #pragma unroll
@@ -123,31 +134,34 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
     const int page = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t];
     const uint8_t* gk = reinterpret_cast<const uint8_t*>(kvl + (static_cast<int64_t>(page) * n_kv + kvh) * 2 * 64 * HD);
     const uint8_t* gv = gk + kTileBytes;
+    uint8_t* sk = smem + buf * 2 * kTileBytes;
+    uint8_t* sv = sk + kTileBytes;
 #pragma unroll
     for (int i = threadIdx.x; i < 64 * kChunks; i += 128) {
       const int r = i / kChunks, c = i % kChunks;
-      cp_async16(sK[buf] + swz<HD>(r, c), gk + i * 16);
-      cp_async16(sV[buf] + swz<HD>(r, c), gv + i * 16);
+      cp_async16(sk + swz<HD>(r, c), gk + i * 16);
+      cp_async16(sv + swz<HD>(r, c), gv + i * 16);
     }
-    cp_async_commit();
   };
 
-  if (t0 < t1) load_tile(t0, 0);
-  for (int t = t0; t < t1; ++t) {
-    const int buf = (t - t0) & 1;
-    if (t + 1 < t1) {
-      load_tile(t + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const uint8_t* k_s = sK[buf];
-    const uint8_t* v_s = sV[buf];
 #pragma unroll
-    for (int cc = 0; cc < (ROWS ? 4 : 1); ++cc) {
-      const int c = ROWS ? cc : warp;  // 16-key chunk of the page
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (t0 + st < t1) load_tile(t0 + st, st);
+    cp_async_commit();
+  }
+  for (int t = t0; t < t1; ++t) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // tile t landed for everyone; tile t-1's buffer is free
+    {
+      const int nt = t + kStages - 1;
+      if (nt < t1) load_tile(nt, (nt - t0) % kStages);
+      cp_async_commit();
+    }
+    const uint8_t* k_s = smem + ((t - t0) % kStages) * 2 * kTileBytes;
+    const uint8_t* v_s = k_s + kTileBytes;
+    for (int c = ROWS ? 0 : kg; c < 4; c += (ROWS ? 1 : nkg)) {  // 16-key chunks of the page
       const int kbase = t * 64 + c * 16;
+      if (kbase > warp_lim) continue;  // chunk fully past the causal limit of every row of the tile
       // S = Q K^T over 16 keys (two n-tiles of 8)
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
@@ -159,17 +173,16 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
         mma16816(s[0], qa[kk], b[0], b[1]);
         mma16816(s[1], qa[kk], b[2], b[3]);
       }
-      // scale, causal mask, online softmax
       float mx_lo = kNegBig, mx_hi = kNegBig;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int nt2 = 0; nt2 < 2; ++nt2) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int key = kbase + nt * 8 + (lane & 3) * 2 + e;
-          s[nt][e] = key <= lim_lo ? s[nt][e] * scale_log2 : -INFINITY;
-          s[nt][2 + e] = key <= lim_hi ? s[nt][2 + e] * scale_log2 : -INFINITY;
-          mx_lo = fmaxf(mx_lo, s[nt][e]);
-          mx_hi = fmaxf(mx_hi, s[nt][2 + e]);
+          const int key = kbase + nt2 * 8 + (lane & 3) * 2 + e;
+          s[nt2][e] = key <= lim_lo ? s[nt2][e] * scale_log2 : -INFINITY;
+          s[nt2][2 + e] = key <= lim_hi ? s[nt2][2 + e] * scale_log2 : -INFINITY;
+          mx_lo = fmaxf(mx_lo, s[nt2][e]);
+          mx_hi = fmaxf(mx_hi, s[nt2][2 + e]);
         }
       }
 #pragma unroll
@@ -184,13 +197,13 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
       float p[2][4];
       float sl = 0.f, sh = 0.f;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        p[nt][0] = exp2f(s[nt][0] - nm_lo);
-        p[nt][1] = exp2f(s[nt][1] - nm_lo);
-        p[nt][2] = exp2f(s[nt][2] - nm_hi);
-        p[nt][3] = exp2f(s[nt][3] - nm_hi);
-        sl += p[nt][0] + p[nt][1];
-        sh += p[nt][2] + p[nt][3];
+      for (int nt2 = 0; nt2 < 2; ++nt2) {
+        p[nt2][0] = exp2f(s[nt2][0] - nm_lo);
+        p[nt2][1] = exp2f(s[nt2][1] - nm_lo);
+        p[nt2][2] = exp2f(s[nt2][2] - nm_hi);
+        p[nt2][3] = exp2f(s[nt2][3] - nm_hi);
+        sl += p[nt2][0] + p[nt2][1];
+        sh += p[nt2][2] + p[nt2][3];
       }
       l_lo = l_lo * al_lo + sl;
       l_hi = l_hi * al_hi + sh;
@@ -206,7 +219,6 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
       pa[1] = pack_bf16(p[0][2], p[0][3]);
       pa[2] = pack_bf16(p[1][0], p[1][1]);
       pa[3] = pack_bf16(p[1][2], p[1][3]);
-      // O += P V over the 16 keys
 #pragma unroll
       for (int dt = 0; dt < kDT; dt += 2) {
         uint32_t b[4];
@@ -217,20 +229,20 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
         mma16816(o[dt + 1], pa, b[2], b[3]);
       }
     }
-    __syncthreads();
   }
-  // quad-reduce the row sums
+  cp_async_wait<0>();
+  __syncthreads();
 #pragma unroll
   for (int off = 1; off <= 2; off <<= 1) {
     l_lo += __shfl_xor_sync(0xffffffffu, l_lo, off);
     l_hi += __shfl_xor_sync(0xffffffffu, l_hi, off);
   }
 
-  if (!ROWS) {
-    // merge the 4 warps' partial states (same 16 rows, disjoint keys) through smem
-    float* so = reinterpret_cast<float*>(smem);             // [4][16][HD]
-    float* sm = so + 4 * 16 * HD;                           // [4][16] m
-    float* sl = sm + 64;                                    // [4][16] l
+  // ---- merge the warps that share an M tile (GROUP mode) through smem: per-row (m, l, O)
+  float* so = reinterpret_cast<float*>(smem);  // [4 warps][16][HD]
+  float* sm = so + 4 * 16 * HD;                // [4][16]
+  float* sl_ = sm + 64;                        // [4][16]
+  {
     const int rl = lane >> 2, rh = rl + 8;
 #pragma unroll
     for (int dt = 0; dt < kDT; ++dt) {
@@ -243,106 +255,103 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
     if ((lane & 3) == 0) {
       sm[warp * 16 + rl] = m_lo;
       sm[warp * 16 + rh] = m_hi;
-      sl[warp * 16 + rl] = l_lo;
-      sl[warp * 16 + rh] = l_hi;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < 16 * HD; e += 128) {
-      const int r = e / HD, col = e % HD;
-      const int m = cta_m0 + r;
-      if (m >= M) continue;
-      float mm = kNegBig;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) mm = fmaxf(mm, sm[w * 16 + r]);
-      float l = 0.f, acc = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float f = exp2f(sm[w * 16 + r] - mm);
-        l += sl[w * 16 + r] * f;
-        acc += so[(w * 16 + r) * HD + col] * f;
-      }
-      const int row = first + m / G, head = kvh * G + m % G;
-      if (n_split == 1) {
-        obuf[(static_cast<int64_t>(row) * n_q + head) * HD + col] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
-      } else {
-        part_o[((static_cast<int64_t>(sp) * rows_cap + row) * n_q + head) * HD + col] = acc;
-        if (col == 0) part_ml[(static_cast<int64_t>(sp) * rows_cap + row) * n_q + head] = make_float2(mm, l);
-      }
-    }
-  } else {
-    const int rr[2] = {mlo, mhi};
-    const float ll[2] = {l_lo, l_hi}, mmv[2] = {m_lo, m_hi};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = rr[h];
-      if (m >= M) continue;
-      const int row = first + m / G, head = kvh * G + m % G;
-#pragma unroll
-      for (int dt = 0; dt < kDT; ++dt) {
-        const int col = dt * 8 + (lane & 3) * 2;
-        const float a = o[dt][2 * h], b = o[dt][2 * h + 1];
-        if (n_split == 1) {
-          const float inv = ll[h] > 0.f ? 1.f / ll[h] : 0.f;
-          *reinterpret_cast<__nv_bfloat162*>(obuf + (static_cast<int64_t>(row) * n_q + head) * HD + col) =
-              __floats2bfloat162_rn(a * inv, b * inv);
-        } else {
-          float* po = part_o + ((static_cast<int64_t>(sp) * rows_cap + row) * n_q + head) * HD + col;
-          po[0] = a;
-          po[1] = b;
-          if (dt == 0 && (lane & 3) == 0)
-            part_ml[(static_cast<int64_t>(sp) * rows_cap + row) * n_q + head] = make_float2(mmv[h], ll[h]);
-        }
-      }
+      sl_[warp * 16 + rl] = l_lo;
+      sl_[warp * 16 + rh] = l_hi;
     }
   }
-}
-
-// One warp per (row, head): merge the KV-split partials.
-template <int HD>
-__global__ void attn_combine_kernel(RowsDev rows, int n_q, int n_split, int rows_cap,
-                                    const float* __restrict__ part_o, const float2* __restrict__ part_ml,
-                                    __nv_bfloat16* __restrict__ obuf) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int row = gw / n_q, head = gw % n_q;
-  if (row >= *rows.n_rows) return;
-  float mm = kNegBig;
-  for (int s = 0; s < n_split; ++s) {
-    mm = fmaxf(mm, part_ml[(static_cast<int64_t>(s) * rows_cap + row) * n_q + head].x);
+  __syncthreads();
+  // each (packed row, dim) of this CTA: combine its warps -> final (n_split == 1) or partial
+  const int ntiles = ROWS ? 4 : nmt;
+  const int wpt = ROWS ? 1 : nkg;  // warps per tile
+  for (int e = threadIdx.x; e < ntiles * 16 * HD; e += 128) {
+    const int tl = e / (16 * HD), r = (e / HD) % 16, col = e % HD;
+    const int m = cta_m0 + tl * 16 + r;
+    if (m >= cta_m1) continue;
+    float mm = kNegBig;
+    for (int g = 0; g < wpt; ++g) mm = fmaxf(mm, sm[(tl + g * nmt) * 16 + r]);
+    float l = 0.f, acc = 0.f;
+    for (int g = 0; g < wpt; ++g) {
+      const int w = tl + g * nmt;
+      const float f = exp2f(sm[w * 16 + r] - mm);
+      l += sl_[w * 16 + r] * f;
+      acc += so[(w * 16 + r) * HD + col] * f;
+    }
+    const int row = first + m / G, head = kvh * G + m % G;
+    if (n_split == 1) {
+      obuf[(static_cast<int64_t>(row) * n_q + head) * HD + col] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
+    } else {
+      part_o[((static_cast<int64_t>(sp) * rows_cap + row) * n_q + head) * HD + col] = acc;
+      if (col == 0) part_ml[(static_cast<int64_t>(sp) * rows_cap + row) * n_q + head] = make_float2(mm, l);
+    }
   }
-  float acc[HD / 32];
-#pragma unroll
-  for (int i = 0; i < HD / 32; ++i) acc[i] = 0.f;
-  float l = 0.f;
-  for (int s = 0; s < n_split; ++s) {
-    const float2 ml = part_ml[(static_cast<int64_t>(s) * rows_cap + row) * n_q + head];
-    const float f = exp2f(ml.x - mm);
-    l += ml.y * f;
-    const float* po = part_o + ((static_cast<int64_t>(s) * rows_cap + row) * n_q + head) * HD;
-#pragma unroll
-    for (int i = 0; i < HD / 32; ++i) acc[i] += po[lane + 32 * i] * f;
+  if (n_split == 1) return;
+  // ---- split-KV: the last CTA of this (request, kv head, block) merges the splits in order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* cnt = counters + (static_cast<int64_t>(req) * n_kv + kvh) * n_blocks + blk;
+    const int prev = atomicAdd(cnt, 1);
+    s_last = prev == n_split - 1;
+    if (s_last) *cnt = 0;  // self-reset for the next layer / launch
   }
-  const float inv = l > 0.f ? 1.f / l : 0.f;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // per packed row: merged max, and each split's weight exp2(m_s - m) / l  (fixed split order)
+  float* sfac = reinterpret_cast<float*>(smem);  // [64 rows][16 splits]
+  const int nrow = cta_m1 - cta_m0;
+  for (int mr = threadIdx.x; mr < nrow; mr += 128) {
+    const int m = cta_m0 + mr;
+    const int row = first + m / G, head = kvh * G + m % G;
+    float2 ml[16];
+    float mm = kNegBig;
 #pragma unroll
-  for (int i = 0; i < HD / 32; ++i)
-    obuf[(static_cast<int64_t>(row) * n_q + head) * HD + lane + 32 * i] = __float2bfloat16_rn(acc[i] * inv);
-}
-
-// Marks every split's (m, l) slot empty before the attention kernel runs, so splits that fall
-// outside a request's causal range contribute nothing.
-__global__ void attn_clear_ml_kernel(float2* ml, int64_t n) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    ml[i] = make_float2(kNegBig, 0.f);
+    for (int sp2 = 0; sp2 < 16; ++sp2) {
+      if (sp2 < n_split) {
+        ml[sp2] = __ldcg(&part_ml[(static_cast<int64_t>(sp2) * rows_cap + row) * n_q + head]);
+        mm = fmaxf(mm, ml[sp2].x);
+      }
+    }
+    float l = 0.f;
+#pragma unroll
+    for (int sp2 = 0; sp2 < 16; ++sp2)
+      if (sp2 < n_split) l += ml[sp2].y * exp2f(ml[sp2].x - mm);
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+    for (int sp2 = 0; sp2 < 16; ++sp2)
+      if (sp2 < n_split) sfac[mr * 16 + sp2] = exp2f(ml[sp2].x - mm) * inv;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrow * (HD / 4); e += 128) {
+    const int mr = e / (HD / 4), c4 = (e % (HD / 4)) * 4;
+    const int m = cta_m0 + mr;
+    const int row = first + m / G, head = kvh * G + m % G;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int sp2 = 0; sp2 < 16; ++sp2) {
+      if (sp2 < n_split) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(
+            &part_o[((static_cast<int64_t>(sp2) * rows_cap + row) * n_q + head) * HD + c4]));
+        const float f = sfac[mr * 16 + sp2];
+        acc.x += v.x * f;
+        acc.y += v.y * f;
+        acc.z += v.z * f;
+        acc.w += v.w * f;
+      }
+    }
+    __nv_bfloat16* od = obuf + (static_cast<int64_t>(row) * n_q + head) * HD + c4;
+    *reinterpret_cast<__nv_bfloat162*>(od) = __floats2bfloat162_rn(acc.x, acc.y);
+    *reinterpret_cast<__nv_bfloat162*>(od + 2) = __floats2bfloat162_rn(acc.z, acc.w);
+  }
 }
 
 template <int HD, bool ROWS>
 cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int n_split, KvDev kv,
                    int layer, const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, float* part_o,
-                   float2* part_ml, int rows_cap, float scale_log2, cudaStream_t s) {
+                   float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s) {
   constexpr int kTile = 64 * HD * 2;
   constexpr int kMerge = (4 * 16 * HD + 128) * 4;
-  constexpr int kSmem = 4 * kTile > kMerge ? 4 * kTile : kMerge;
+  constexpr int kSmem = 6 * kTile > kMerge ? 6 * kTile : kMerge;  // 3 stages x (K + V)
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_kernel<HD, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
@@ -350,7 +359,7 @@ cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int
   }
   dim3 grid(n_req, m.n_kv, blocks * n_split);
   attn_kernel<HD, ROWS><<<grid, 128, kSmem, s>>>(rows, kv, layer, m.n_q, m.n_kv, qbuf, obuf, part_o,
-                                                 part_ml, n_split, rows_cap, scale_log2);
+                                                 part_ml, counters, n_split, rows_cap, blocks, scale_log2);
   return cudaGetLastError();
 }
 
@@ -363,39 +372,33 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   if (m.hd != 64 && m.hd != 128) return cudaErrorInvalidValue;
   const int G = m.n_q / m.n_kv;
   const int Mmax = max_rows_per_req * G;
-  const bool rows_mode = Mmax >= 64;
-  const int blocks = rows_mode ? (Mmax + 63) / 64 : (Mmax + 15) / 16;
+  const bool rows_mode = Mmax > 64;
+  const int blocks = rows_mode ? (Mmax + 63) / 64 : 1;
   const int rows_cap = n_req * max_rows_per_req;  // row indices are < sum of req_n <= this
+  // scratch = [counters (1 MiB, zeroed at allocation, self-resetting)][part_o][part_ml]
+  constexpr size_t kCounterBytes = size_t(1) << 20;
+  int* counters = reinterpret_cast<int*>(scratch);
+  if (static_cast<size_t>(n_req) * m.n_kv * blocks * 4 > kCounterBytes) return cudaErrorInvalidValue;
+  float* body = scratch + kCounterBytes / 4;
+  const size_t body_bytes = scratch_bytes - kCounterBytes;
   const int base = n_req * m.n_kv * blocks;
   const int tiles = (max_ctx + 63) / 64;
   int n_split = 1;
-  if (base < 2 * 148 && tiles >= 4) {
+  if (base < 148 && tiles >= 4) {
     n_split = (2 * 148 + base - 1) / base;
-    const int max_split = (tiles + 1) / 2;  // >= 2 pages per split
+    const int max_split = (tiles + 1) / 2 < 16 ? (tiles + 1) / 2 : 16;  // >= 2 pages per split
     if (n_split > max_split) n_split = max_split;
   }
   const size_t per_split = static_cast<size_t>(rows_cap) * m.n_q * (m.hd * 4 + 8);
-  while (n_split > 1 && per_split * n_split > scratch_bytes) --n_split;
-  float* part_o = scratch;
-  float2* part_ml = reinterpret_cast<float2*>(scratch + static_cast<size_t>(n_split) * rows_cap * m.n_q * m.hd);
+  while (n_split > 1 && per_split * n_split > body_bytes) --n_split;
+  float* part_o = body;
+  float2* part_ml = reinterpret_cast<float2*>(body + static_cast<size_t>(n_split) * rows_cap * m.n_q * m.hd);
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(m.hd));
-  // every (row, split) slot is written by its CTA (empty key ranges write (-1e30, 0)), so the
-  // partial buffers need no clearing.
-  cudaError_t e;
   if (m.hd == 64)
-    e = rows_mode ? launch<64, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, rows_cap, scale_log2, s)
-                  : launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, rows_cap, scale_log2, s);
-  else
-    e = rows_mode ? launch<128, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, rows_cap, scale_log2, s)
-                  : launch<128, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, rows_cap, scale_log2, s);
-  if (e != cudaSuccess || n_split == 1) return e;
-  const int64_t warps = static_cast<int64_t>(rows_cap) * m.n_q;
-  const int grid = static_cast<int>((warps * 32 + 255) / 256);
-  if (m.hd == 64)
-    attn_combine_kernel<64><<<grid, 256, 0, s>>>(rows, m.n_q, n_split, rows_cap, part_o, part_ml, obuf);
-  else
-    attn_combine_kernel<128><<<grid, 256, 0, s>>>(rows, m.n_q, n_split, rows_cap, part_o, part_ml, obuf);
-  return cudaGetLastError();
+    return rows_mode ? launch<64, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s)
+                     : launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+  return rows_mode ? launch<128, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s)
+                   : launch<128, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
 }
 
 }  // namespace faser

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -205,6 +206,7 @@ struct LmWork {
     amax.alloc(static_cast<size_t>(lm_cap) * (s.vocab / 128) * 8);
     attn_bytes = static_cast<size_t>(64) << 20;
     attn.alloc(attn_bytes);
+    LCK(cudaMemset(attn.p, 0, size_t(1) << 20));  // split-KV counters (self-resetting)
     argmax.alloc(static_cast<size_t>(cap) * 4);
     src_of.alloc(static_cast<size_t>(cap) * 4);
     LCK(make_act_operand(&op_xb, xb.p, cap, s.d));
@@ -252,6 +254,7 @@ class LlamaEngine {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
   int nsm = 148;
+  bool graph_mode = false;  // FASER_CUDA_GRAPH=1: each step is captured and replayed as one graph
   int max_spec = 16;
   int max_seq = 0;    // slot row capacity (tokens)
   int max_pages = 0;  // pages per slot
@@ -329,6 +332,7 @@ class LlamaEngine {
     if (cfg.device < 0 || cfg.device >= ndev) throw LFail{FASER_EINVAL, "device index out of range"};
     LCK(cudaSetDevice(cfg.device));
     nsm = num_sms_dev();
+    graph_mode = getenv("FASER_CUDA_GRAPH") && getenv("FASER_CUDA_GRAPH")[0] == '1';
     dsh = shape_of(m->draft);
     tsh = shape_of(m->target);
     eos = tsh.vocab - 1;
@@ -409,6 +413,10 @@ class LlamaEngine {
   };
 
   GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, nsm); }
+  bool capturing = false;
+  cudaError_t record_event(cudaEvent_t e) {
+    return capturing ? cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal) : cudaEventRecord(e, stream);
+  }
 
   void capture_stage(int stage, const LmModel& m, const LmWork& w, const Fwd& f) {
     LCK(cudaStreamSynchronize(stream));
@@ -747,7 +755,12 @@ class LlamaEngine {
     vrows.req_slot = dev_of(v_rslot);
     vrows.req_pos0 = dev_of(v_pos0);
 
-    LCK(cudaEventRecord(ev[0], stream));
+    const bool use_graph = graph_mode && cfg.debug_capture == 0;
+    if (use_graph) {
+      LCK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+    }
+    LCK(record_event(ev[0]));
     LCK(lm_ptab_scatter(ptab.as<int>(), max_pages, dev_of(b_tr), n_tr, stream));
     LCK(lm_admit(sl, dev_of(b_adm), static_cast<int>(newly.size()), stream));
     launches += (n_tr > 0) + (!newly.empty());
@@ -791,7 +804,7 @@ class LlamaEngine {
       LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, stream));
       launches += 2;
     }
-    LCK(cudaEventRecord(ev[1], stream));
+    LCK(record_event(ev[1]));
     // ---- verify (+ early exit) + accept/commit
     const bool ee = cfg.mode >= FASER_MODE_VSD_AD_EE;
     int k_table[FASER_MAX_LAYERS + 1];
@@ -831,7 +844,18 @@ class LlamaEngine {
     StepCtl ctl{n, L, eos, ee ? 1 : 0, cfg.exempt_rule};
     LCK(lm_accept_commit(sl, q, vrows, ctl, d_res.as<faser_round_result>(), stream));
     launches += 2;
-    LCK(cudaEventRecord(ev[2], stream));
+    LCK(record_event(ev[2]));
+    if (use_graph) {
+      capturing = false;
+      cudaGraph_t g = nullptr;
+      LCK(cudaStreamEndCapture(stream, &g));
+      cudaGraphExec_t ge = nullptr;
+      LCK(cudaGraphInstantiate(&ge, g, 0));
+      LCK(cudaGraphLaunch(ge, stream));
+      LCK(cudaStreamSynchronize(stream));
+      cudaGraphExecDestroy(ge);
+      cudaGraphDestroy(g);
+    }
     LCK(cudaMemcpyAsync(h_res, d_res.p, sizeof(faser_round_result) * n, cudaMemcpyDeviceToHost, stream));
     if (capture) {
       std::vector<int32_t> dr(static_cast<size_t>(n) * FASER_MAX_SPEC);

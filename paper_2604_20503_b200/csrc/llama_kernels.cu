@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(128) embed_kernel(const __nv_bfloat16* __restr
                                                     int t_stride, float* __restrict__ x,
                                                     __nv_bfloat16* __restrict__ xb, float* __restrict__ ss) {
   __shared__ float red[4];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int r = blockIdx.x, c = blockIdx.y * 128 + threadIdx.x;
   if (r >= *rows.n_rows) return;
   const __nv_bfloat16 e = emb[static_cast<int64_t>(rows.row_tok[r]) * d + c];

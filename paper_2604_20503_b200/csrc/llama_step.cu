@@ -185,6 +185,7 @@ __global__ void scatter_back_kernel(RowsDev rows, int d, int t_stride, const flo
                                     const __nv_bfloat16* __restrict__ xbs, const float* __restrict__ sss,
                                     float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
                                     float* __restrict__ ss) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int r = blockIdx.x;
   if (r >= *rows.n_rows) return;
   const float4* s4 = reinterpret_cast<const float4*>(xs + static_cast<int64_t>(r) * d);

@@ -41,9 +41,11 @@ constexpr int kUmmaK = 16;
 constexpr int kABytes = kBM * kBK * 2;       // 16 KiB
 constexpr int kXBox = 32;                    // activation TMA box rows
 
-template <int BN>
+// ST = pipeline depth: "shallow" 4-stage configs (~100 KB smem for BN <= 64, 2 CTAs / SM, room
+// for the next GEMM's weight prefetch) or "deep" configs filling ~200 KB (1 CTA / SM).
+template <int BN, int ST>
 struct Cfg {
-  static constexpr int kStages = 4;  // BN <= 64: ~100 KB smem -> 2 CTAs / SM
+  static constexpr int kStages = ST;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
@@ -68,11 +70,11 @@ __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-template <int BN>
-__global__ void __launch_bounds__(128, 2)
+template <int BN, int ST>
+__global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ EpiArgs ea, int n_out, int kb_total, int kb_per_split, int splits) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, ST>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -103,10 +105,27 @@ __global__ void __launch_bounds__(128, 2)
     sm100::mbar_init(accum, 1);
     sm100::fence_mbar_init();
   }
+  __syncthreads();  // barrier inits visible before the producer touches them
   pdl_trigger();
+  // Weights do not depend on the previous kernel: stream the first stages of this CTA's weight
+  // slice now, overlapping the previous kernel's tail (programmatic dependent launch).
+  const int npre = nkb < C::kStages ? nkb : C::kStages;
+  const uint64_t pol_w = sm100::policy_evict_first();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < npre; ++i) {
+      sm100::mbar_expect_tx(&full[i], kABytes);
+      sm100::tma_load_2d_hint(sA + i * kABytes, &tmW, &full[i], (kb0 + i) * kBK, m0, pol_w);
+    }
+  }
   pdl_wait();  // everything below may read the previous kernel's output
   const int T = ea.n_rows ? min(*ea.n_rows, ea.t_stride) : ea.t_stride;
-  if (n0 >= T || nkb <= 0) return;  // uniform per CTA, before any TMEM / TMA use
+  if (n0 >= T) {  // uniform per CTA: tile entirely past the live rows (early-exit compaction)
+    if (warp == 0 && lane == 0) {  // drain the prefetched weight tiles before exiting
+      for (int i = 0; i < npre; ++i) sm100::mbar_arrive(&full[i]);
+      for (int i = 0; i < npre; ++i) sm100::mbar_wait(&full[i], 0);
+    }
+    return;
+  }
   if (warp == 2) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
@@ -115,16 +134,19 @@ __global__ void __launch_bounds__(128, 2)
 
   if (warp == 0 && lane == 0) {
     // ---------------------------------------------------------------- TMA producer
-    const uint64_t pol_w = sm100::policy_evict_first();
     const int xboxes = (min(BN, T - n0) + kXBox - 1) / kXBox;  // skip all-padding activation boxes
-    const uint32_t stage_bytes = kABytes + xboxes * kXBox * kBK * 2;
+    const uint32_t xbytes = xboxes * kXBox * kBK * 2;
     for (int i = 0; i < nkb; ++i) {
       const int s = i % C::kStages;
       const uint32_t ph = (i / C::kStages) & 1;
-      sm100::mbar_wait(&empty[s], ph ^ 1);
-      sm100::mbar_arrive_expect_tx(&full[s], stage_bytes);
       const int kc = (kb0 + i) * kBK;
-      sm100::tma_load_2d_hint(sA + s * kABytes, &tmW, &full[s], kc, m0, pol_w);
+      if (i < npre) {  // weight tile already in flight: add the activation tile and arrive
+        sm100::mbar_arrive_expect_tx(&full[s], xbytes);
+      } else {
+        sm100::mbar_wait(&empty[s], ph ^ 1);
+        sm100::mbar_arrive_expect_tx(&full[s], kABytes + xbytes);
+        sm100::tma_load_2d_hint(sA + s * kABytes, &tmW, &full[s], kc, m0, pol_w);
+      }
       for (int j = 0; j < xboxes; ++j)
         sm100::tma_load_2d(sB + s * C::kBBytes + j * kXBox * 128, &tmX, &full[s], kc, n0 + j * kXBox);
     }
@@ -329,13 +351,14 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int BN>
+template <int BN, int ST>
 cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int splits, const EpiArgs& ea,
                       cudaStream_t s) {
+  using C = Cfg<BN, ST>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
-    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_kernel<BN, ST>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   const int kb_total = w.k / kBK;
   const int kps = (kb_total + splits - 1) / splits;
@@ -343,7 +366,7 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(w.rows / kBM, (t + BN - 1) / BN, z);
   cfg.blockDim = dim3(128, 1, 1);
-  cfg.dynamicSmemBytes = Cfg<BN>::kSmem;
+  cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -353,8 +376,8 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = z;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN>, w.map, x.map, ea, w.rows, kb_total, kps, z);
+  cfg.numAttrs = z > 1 ? 2 : 1;  // cluster launch only when the K split needs DSMEM
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST>, w.map, x.map, ea, w.rows, kb_total, kps, z);
 }
 
 }  // namespace
@@ -384,31 +407,47 @@ cudaError_t make_act_operand(GemmOperand* op, const void* x, int rows_cap, int k
   return make_operand(op, x, rows_cap, k, kXBox);
 }
 
-// Tile width along the rows (tokens): the widest tile that still gives one full wave of CTAs;
-// below that, 32-row tiles plus split-K (cluster of <= kMaxSplit CTAs).
-constexpr int kMaxSplit = 8;
+// Launch plan, from a (BN, splits, depth) sweep of graph-timed back-to-back launches on B200
+// (tools/gemm_stream.py, profiles/README.md):
+//  * enough tiles (>= 120) with one token tile covering all rows: no split, deep pipeline;
+//  * otherwise 32-row tiles with a K split of <= 4 (8-CTA clusters schedule badly at 1 CTA/SM),
+//    deep pipeline while the grid fits one CTA per SM, 4-stage (2 CTAs/SM) beyond.
+constexpr int kMaxSplit = 4;
 
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
   GemmPlan p;
   const int mt = n_out / kBM;
-  p.bn = 32;
-  for (int bn : {256, 128, 64}) {
-    if (mt * ((t + bn - 1) / bn) >= num_sms) {
+  const int kb = k / kBK;
+  int cover = 32;
+  while (cover < t && cover < 256) cover <<= 1;
+  for (int bn = cover; bn >= 64; bn >>= 1) {  // widest token tile that still gives >= 80 tiles
+    const int tl = mt * ((t + bn - 1) / bn);
+    if (tl >= (bn == cover ? 80 : 120)) {  // a narrower tile re-streams weights per token tile
       p.bn = bn;
-      break;
+      p.splits = 1;
+      p.deep = true;
+      p.tiles = tl;
+      return p;
     }
   }
-  const int tiles = mt * ((t + p.bn - 1) / p.bn);
-  const int slots = num_sms * (p.bn <= 64 ? 2 : 1);  // resident CTAs per wave
-  const int kb = k / kBK;
-  int s = tiles >= slots / 2 ? 1 : slots / tiles;   // never spill into a second wave
-  const int max_s = kb / 4 > 0 ? kb / 4 : 1;         // >= 4 k-blocks (256 of K) per split
+  if (mt * ((t + 31) / 32) >= 120) {
+    p.bn = 32;
+    p.splits = 1;
+    p.deep = true;
+    p.tiles = mt * ((t + 31) / 32);
+    return p;
+  }
+  p.bn = 32;
+  const int tiles = mt * ((t + 31) / 32);
+  int s = (2 * num_sms) / tiles;
+  const int max_s = kb / 4 > 0 ? kb / 4 : 1;  // >= 4 k-blocks (256 of K) per split
   s = s > max_s ? max_s : s;
   s = s > kMaxSplit ? kMaxSplit : s;
   s = s < 1 ? 1 : s;
   const int kps = (kb + s - 1) / s;
   p.splits = (kb + kps - 1) / kps;
   p.tiles = tiles;
+  p.deep = tiles * p.splits <= num_sms;
   return p;
 }
 
@@ -416,11 +455,12 @@ cudaError_t gemm_fused(const GemmOperand& w, const GemmOperand& x, int t, const 
                        cudaStream_t s) {
   if (t <= 0) return cudaSuccess;
   if (w.k != x.k) return cudaErrorInvalidValue;
+  const bool deep = p.deep;
   switch (p.bn) {
-    case 32: return launch_bn<32>(w, x, t, p.splits, epi, s);
-    case 64: return launch_bn<64>(w, x, t, p.splits, epi, s);
-    case 128: return launch_bn<128>(w, x, t, p.splits, epi, s);
-    default: return launch_bn<256>(w, x, t, p.splits, epi, s);
+    case 32: return deep ? launch_bn<32, 8>(w, x, t, p.splits, epi, s) : launch_bn<32, 4>(w, x, t, p.splits, epi, s);
+    case 64: return deep ? launch_bn<64, 7>(w, x, t, p.splits, epi, s) : launch_bn<64, 4>(w, x, t, p.splits, epi, s);
+    case 128: return deep ? launch_bn<128, 6>(w, x, t, p.splits, epi, s) : launch_bn<128, 3>(w, x, t, p.splits, epi, s);
+    default: return deep ? launch_bn<256, 4>(w, x, t, p.splits, epi, s) : launch_bn<256, 2>(w, x, t, p.splits, epi, s);
   }
 }
 

@@ -58,6 +58,7 @@ struct GemmPlan {
   int bn = 32;
   int splits = 1;
   int tiles = 0;
+  bool deep = true;  // deep pipeline (~200 KB smem, 1 CTA / SM) vs 4-stage (2 CTAs / SM)
 };
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms);
 

@@ -22,12 +22,19 @@ def run(n, t, k, bn=0, splits=0, iters=60):
     for i in range(copies):
         assert L.faser_k_gemm_bf16_plan(C.c_void_p(ws[i].data_ptr()), C.c_void_p(x.data_ptr()),
                                         C.c_void_p(out.data_ptr()), n, t, k, bn, splits, C.c_void_p(s)) == 0
+    # capture the launch sequence in a CUDA graph so host launch overhead is excluded
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        cs = torch.cuda.current_stream().cuda_stream
+        for i in range(iters):
+            L.faser_k_gemm_bf16_plan(C.c_void_p(ws[i % copies].data_ptr()), C.c_void_p(x.data_ptr()),
+                                     C.c_void_p(out.data_ptr()), n, t, k, bn, splits, C.c_void_p(cs))
+    g.replay()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
-    for i in range(iters):
-        L.faser_k_gemm_bf16_plan(C.c_void_p(ws[i % copies].data_ptr()), C.c_void_p(x.data_ptr()),
-                                 C.c_void_p(out.data_ptr()), n, t, k, bn, splits, C.c_void_p(s))
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / iters
