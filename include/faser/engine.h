@@ -297,6 +297,49 @@ faser_status faser_make_gate_plan(const faser_exit_policy* policy, const faser_g
 faser_status faser_plan_overlap(int32_t s, int32_t b, const faser_latency_model* models,
                                 const double* r_grid, int32_t n_r, faser_overlap_plan* out);
 
+/* --------------------------------------- per-request speculative-length controller (host)
+ * AdaptiveDrafter / GpPosterior / AcceptanceBook / AcceptanceWindow (drafter.hpp:15-129,
+ * drafter.cpp:14-230, sdcore.hpp:17-35) restated natively (the reference needs Eigen, which is
+ * absent: parity of k_i assignment is unpinned). The GP posterior is computed from
+ * per-candidate sufficient statistics (mathematically identical to the reference's LLT over
+ * the raw window). */
+typedef struct faser_drafter_cfg {
+  int32_t n_candidates;
+  int32_t candidates[16];      /* S = {1,2,3,4,5,6,8,10} (drafter.hpp:16) */
+  int32_t window_ctx;          /* 64 */
+  int32_t window_request;      /* 16 */
+  int32_t reserved0;
+  double epsilon;              /* 1e-6 */
+  double kernel_len, kernel_var, noise_var; /* 1, 1, 0.1 */
+  double cold_start_accept;    /* 0.7 */
+} faser_drafter_cfg;
+
+typedef struct faser_drafter faser_drafter;
+
+void faser_drafter_default_cfg(faser_drafter_cfg* out);
+faser_status faser_drafter_create(const faser_drafter_cfg* cfg, const faser_latency_model* models,
+                                  faser_drafter** out);
+void faser_drafter_destroy(faser_drafter* d);
+/* AdaptiveDrafter::assign_lengths (drafter.cpp:175-207) for the batch (req_ids[n]), batch size
+ * b and draft SM share r -> k_out[n]. */
+faser_status faser_drafter_assign(faser_drafter* d, const int64_t* req_ids, int32_t n, int32_t b,
+                                  double r, int32_t* k_out);
+/* Feedback of one executed round: per request (spec, submitted, accepted) -> the request's
+ * AcceptanceWindow (push, W = window_request) and the context AcceptanceBook; then
+ * AdaptiveDrafter::observe_round(b, r, t_obs_ms, mean ratio per distinct spec length). */
+faser_status faser_drafter_observe(faser_drafter* d, int32_t b, double r, double t_obs_ms,
+                                   const int64_t* req_ids, const int32_t* spec,
+                                   const int32_t* submitted, const int32_t* accepted, int32_t n);
+/* Drops a finished request's acceptance window. */
+faser_status faser_drafter_release(faser_drafter* d, int64_t req_id);
+/* GpPosterior mu/sigma per candidate of context (b, r) and its round count (for tests). */
+faser_status faser_drafter_posterior(faser_drafter* d, int32_t b, double r, double* mu,
+                                     double* sigma, int32_t* rounds);
+/* DrafterConfig::beta (drafter.cpp:14-17) and objective (drafter.cpp:19-23). */
+double faser_drafter_beta(const faser_drafter_cfg* cfg, int32_t round);
+faser_status faser_drafter_objective(double t_hat_ms, int32_t s, double a_hat, double epsilon,
+                                     double* out);
+
 /* Deterministic workload inputs (workload.cpp:116-122): synth_prompt. */
 faser_status faser_synth_prompt(uint64_t seed, int32_t index, int32_t len, int32_t vocab,
                                 int32_t* out);

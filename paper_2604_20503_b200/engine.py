@@ -43,6 +43,9 @@ def lib():
         L.faser_engine_stream.argtypes = [C.c_void_p]
         L.faser_engine_destroy.argtypes = [C.c_void_p]
         L.faser_engine_destroy.restype = None
+        L.faser_drafter_destroy.argtypes = [C.c_void_p]
+        L.faser_drafter_destroy.restype = None
+        L.faser_drafter_beta.restype = C.c_double
         _LIB = L
     return _LIB
 

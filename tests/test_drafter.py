@@ -1,0 +1,105 @@
+"""CPU tier: the native AdaptiveDrafter restatement (drafter.cpp) against a numpy restatement of
+the reference's raw-window GP (drafter.cpp:46-80, Eigen LLT), its cold-start sweep
+(drafter.cpp:182-186) and its LCB argmin (drafter.cpp:188-205). The reference TU needs Eigen
+(absent), so this pins the controller to the reference's published algorithm, not its binary."""
+import math
+
+import numpy as np
+
+from paper_2604_20503_b200 import abi, controller, engine
+
+S = [1, 2, 3, 4, 5, 6, 8, 10]
+
+
+def gp_reference(window, cfg):
+    """drafter.cpp:46-80 with a dense solve over the raw window (what Eigen's LLT computes)."""
+    m = len(S)
+    if not window:
+        return np.zeros(m), np.full(m, math.sqrt(cfg.kernel_var))
+    idx = np.array([w[0] for w in window], float)
+    y = np.array([w[1] for w in window])
+    mean = y.mean()
+    ls2 = 2 * cfg.kernel_len ** 2
+    K = cfg.kernel_var * np.exp(-(idx[:, None] - idx[None, :]) ** 2 / ls2) + cfg.noise_var * np.eye(len(idx))
+    alpha = np.linalg.solve(K, y - mean)
+    mu, sd = np.zeros(m), np.zeros(m)
+    for c in range(m):
+        k = cfg.kernel_var * np.exp(-(c - idx) ** 2 / ls2)
+        mu[c] = mean + k @ alpha
+        sd[c] = math.sqrt(max(cfg.kernel_var - k @ np.linalg.solve(K, k), 1e-12))
+    return mu, sd
+
+
+def test_beta_and_objective():
+    cfg = controller.DrafterCfg.default()
+    L = engine.lib()
+    for n in (0, 1, 2, 10, 1000):
+        exp = 2 * math.log(8 * max(n, 1) ** 2 * math.pi ** 2 / 6)
+        assert abs(L.faser_drafter_beta(cfg and __import__("ctypes").byref(cfg), n) - exp) < 1e-12
+    import ctypes as C
+    out = C.c_double()
+    assert L.faser_drafter_objective(C.c_double(3.0), 4, C.c_double(0.5), C.c_double(1e-6), C.byref(out)) == 0
+    assert abs(out.value - 3.0 / (2.0 + 1e-6)) < 1e-15
+    assert L.faser_drafter_objective(C.c_double(0.0), 4, C.c_double(0.5), C.c_double(1e-6), C.byref(out)) == abi.EINVAL
+    assert L.faser_drafter_objective(C.c_double(1.0), 0, C.c_double(0.5), C.c_double(1e-6), C.byref(out)) == abi.EINVAL
+
+
+def test_cold_start_sweep_then_lcb():
+    d = controller.AdaptiveDrafter()
+    rng = np.random.default_rng(0)
+    ids = list(range(6))
+    seen = []
+    for rnd in range(len(S)):
+        k = d.assign_lengths(ids, 6, 0.5)
+        assert len(set(k)) == 1
+        seen.append(k[0])
+        acc = [int(rng.integers(0, k[0] + 1)) for _ in ids]
+        d.observe_round(6, 0.5, 1.0 + 0.1 * k[0], ids, k, k, acc)
+    assert seen == S  # every arm swept once
+    k = d.assign_lengths(ids, 6, 0.5)
+    assert all(x in S for x in k)
+
+
+def test_posterior_matches_raw_window_llt():
+    cfg = controller.DrafterCfg.default()
+    d = controller.AdaptiveDrafter(cfg)
+    rng = np.random.default_rng(1)
+    window = []  # (index, cost, round)
+    b, r = 16, 0.5
+    for rnd in range(1, 90):
+        ks = [S[int(i)] for i in rng.integers(0, 8, size=5)]
+        sub = ks
+        acc = [int(rng.integers(0, k + 1)) for k in ks]
+        t = float(rng.uniform(1, 5))
+        d.observe_round(b, r, t, list(range(5)), ks, sub, acc)
+        by_s = {}
+        for k, a in zip(ks, acc):
+            by_s.setdefault(k, []).append(a / k)
+        for k in sorted(by_s):
+            ratio = sum(by_s[k]) / len(by_s[k])
+            window.append((S.index(k), t / (k * ratio + cfg.epsilon), rnd))
+        window = [w for w in window if w[2] > rnd - cfg.window_ctx]
+        if rnd % 11 == 0:
+            mu, sd, n = d.posterior(b, r)
+            emu, esd = gp_reference(window, cfg)
+            assert n == rnd
+            assert np.allclose(mu, emu, rtol=1e-9, atol=1e-9), (mu, emu)
+            assert np.allclose(sd, esd, rtol=1e-9, atol=1e-9), (sd, esd)
+
+
+def test_contexts_are_bucketed():
+    d = controller.AdaptiveDrafter()
+    d.observe_round(16, 0.5, 1.0, [0], [4], [4], [2])
+    assert d.posterior(17, 0.46)[2] == 1     # round(log2 17) = 4, decile 5: same context
+    assert d.posterior(64, 0.5)[2] == 0
+    assert d.posterior(16, 0.9)[2] == 0
+
+
+def test_rejects_unknown_length():
+    d = controller.AdaptiveDrafter()
+    try:
+        d.observe_round(4, 0.5, 1.0, [0], [7], [7], [3])
+    except engine.FaserError as e:
+        assert e.status == abi.EINVAL
+    else:
+        raise AssertionError("7 is not in the candidate set")
