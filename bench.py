@@ -142,7 +142,8 @@ def llama_desc(name):
 
 def make_engine(desc, args, local_rank):
     from paper_2604_20503_b200 import engine
-    mode = abi.MODE_VSD_AD_EE if args.mode == "ee" else abi.MODE_VSD
+    mode = {"vsd": abi.MODE_VSD, "ad": abi.MODE_VSD_AD, "ee": abi.MODE_VSD_AD_EE,
+            "ov": abi.MODE_FULL, "full": abi.MODE_FULL}[args.mode]
     return engine.ServingEngine(desc=desc, max_batch=args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
                                 mode=mode, default_spec_length=args.k, max_spec_length=16,
                                 prefill_rows=8192, device=local_rank)
@@ -156,17 +157,30 @@ def gate_plan(desc, args):
     return abi.GatePlan(lo, lo + 1, 1.0)
 
 
-def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None):
-    """n_steps serving iterations; per-request first/last commit times on `clock`."""
+def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=None, chunk=0):
+    """n_steps serving iterations; per-request first/last commit times on `clock`. With a
+    drafter (AdaptiveDrafter) the per-request k_i come from assign_lengths before each step and
+    the round is fed back with observe_round after it (the reference loop)."""
     tokens = 0
     for _ in range(n_steps):
         if feeder is not None:
             feeder()
-        if not eng.live_requests():
+        live = eng.live_requests()
+        if not live:
             break
+        if drafter is not None:
+            eng.set_spec_lengths(live, drafter.assign_lengths(live, len(live), 1.0))
         if gate is not None:
             eng.set_gate(gate)
+        if chunk:
+            eng.set_overlap(True, chunk)
         res = eng.step()
+        for r in res:
+            state["acc"] = state.get("acc", 0) + r.outcome.accepted_count
+            state["sub"] = state.get("sub", 0) + r.outcome.submitted
+            state["flr"] = state.get("flr", 0.0) + r.outcome.full_layers_run
+        if drafter is not None:
+            drafter.observe_results(res, len(live), 1.0, max(eng.last_step_timing()[2], 1e-3))
         now = clock()
         for r in res:
             if r.committed:
@@ -191,6 +205,13 @@ def llama_ours(args, rank, world, local_rank):
     base = rank * n_req  # request-sharded replicas: each rank owns its own requests
     prompts, outl = prompts_for(base, n_req, V, IN_RANGE, OUT_RANGE)
     gate = gate_plan(desc, args)
+    chunk = args.chunk if args.mode in ("ov", "full") else 0
+
+    def new_drafter():
+        if args.mode in ("vsd", "ov"):
+            return None
+        from paper_2604_20503_b200 import controller
+        return controller.AdaptiveDrafter()
 
     def sync_all():
         torch.cuda.synchronize()
@@ -208,7 +229,8 @@ def llama_ours(args, rank, world, local_rank):
         dev_clock[0] += eng.last_step_timing()[2] / 1e3
         return dev_clock[0]
 
-    run_llama_steps(eng, args.warmup, clock, st, gate=gate)
+    drafter = new_drafter()
+    run_llama_steps(eng, args.warmup, clock, st, gate=gate, drafter=drafter, chunk=chunk)
     stream = torch.cuda.ExternalStream(eng.stream_ptr())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st = {"first": {}, "last": {}}
@@ -229,7 +251,7 @@ def llama_ours(args, rank, world, local_rank):
     with Clocks(local_rank) as clk:
         ev0.record(stream)
         t0 = time.perf_counter()
-        tokens = run_llama_steps(eng, args.steps, clock_acc, st, gate=gate)
+        tokens = run_llama_steps(eng, args.steps, clock_acc, st, gate=gate, drafter=drafter, chunk=chunk)
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -253,7 +275,8 @@ def llama_ours(args, rank, world, local_rank):
             nxt[0] += 1
 
     st2 = {"first": {}, "last": {}}
-    run_llama_steps(eng, args.warmup, time.perf_counter, st2, feeder, gate=gate)
+    drafter2 = new_drafter()
+    run_llama_steps(eng, args.warmup, time.perf_counter, st2, feeder, gate=gate, drafter=drafter2, chunk=chunk)
 
     def feeder_counting():
         a, b = eng.last_step_bytes()
@@ -265,7 +288,8 @@ def llama_ours(args, rank, world, local_rank):
     sync_all()
     st2 = {"first": {}, "last": {}}
     t0 = time.perf_counter()
-    tokens2 = run_llama_steps(eng, args.steps, time.perf_counter, st2, feeder_counting, gate=gate)
+    tokens2 = run_llama_steps(eng, args.steps, time.perf_counter, st2, feeder_counting, gate=gate,
+                              drafter=drafter2, chunk=chunk)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     e2e_tpot = p50_tpot_ms(st2["first"], st2["last"])
@@ -302,6 +326,8 @@ def llama_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "device_ms_per_step": {"draft": draft_ms / k, "verify_accept": verify_ms / k},
+        "acceptance": st.get("acc", 0) / max(st.get("sub", 1), 1),
+        "layer_work_per_drafted_token": st.get("flr", 0.0) / max(st.get("sub", 1), 1),
         "wall_s_timed": wall,
     }
     line["roofline"] = llama_roofline(desc, B, args.k, verify_ms / k, draft_ms / k)
@@ -465,7 +491,8 @@ def main():
     ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "tiny", "toy"])
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--k", type=int, default=4)
-    ap.add_argument("--mode", default="vsd", choices=["vsd", "ee"])
+    ap.add_argument("--mode", default="vsd", choices=["vsd", "ad", "ee", "ov", "full"])
+    ap.add_argument("--chunk", type=int, default=2)
     ap.add_argument("--gate-layer", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -170,6 +170,10 @@ typedef struct faser_llama_shape {
   int32_t d_model, layers, n_heads, n_kv_heads, head_dim, ffn, vocab, reserved0;
   double rope_theta, rms_eps;
   double bigram_scale, embed_noise, init_std;
+  /* fraction of "hard" tokens t whose successor in THIS model is g(t) + V/2 (mod V) instead of
+   * g(t): set on the target only, it makes the pair disagree exactly on those contexts and the
+   * disagreement is visible from the first layers (early exit has signal). 0 = plain bigram. */
+  double hard_fraction;
   uint64_t seed;
 } faser_llama_shape;
 

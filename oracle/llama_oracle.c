@@ -51,7 +51,7 @@ static float bf2f(uint16_t h) {
   return f;
 }
 
-enum { TAG_LM = 1, TAG_EMB_NOISE = 2, TAG_QKV = 3, TAG_O = 4, TAG_GATE = 5, TAG_UP = 6, TAG_DOWN = 7 };
+enum { TAG_LM = 1, TAG_EMB_NOISE = 2, TAG_QKV = 3, TAG_O = 4, TAG_GATE = 5, TAG_UP = 6, TAG_DOWN = 7, TAG_HARD = 8 };
 
 typedef struct {
   uint16_t *wqkv, *wo, *wgu, *wd;
@@ -100,12 +100,16 @@ lmo_model* lmo_create(const faser_llama_shape* s, uint32_t ga, uint32_t gb) {
   gen_matrix(m->lm, V * d, m->seed, TAG_LM * 4096u, m->std);
   {
     const uint64_t base = tensor_base(m->seed, TAG_EMB_NOISE * 4096u);
+    const uint64_t base_hard = tensor_base(m->seed, TAG_HARD * 4096u);
+    const double hard = s->hard_fraction;
     const float c = scale_for(m->noise);
     const float beta = m->beta;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < V * d; ++i) {
       const int64_t t = i / d, col = i % d;
-      const int64_t g = (int64_t)(((uint64_t)ga * (uint64_t)t + gb) % (uint64_t)V);
+      int64_t g = (int64_t)(((uint64_t)ga * (uint64_t)t + gb) % (uint64_t)V);
+      const double u = (double)(mix64(base_hard + (uint64_t)t) >> 11) * 0x1.0p-53;
+      if (u < hard) g = (g + V / 2) % V;
       volatile float prod = beta * bf2f(m->lm[g * d + col]);  // two separately rounded ops
       m->emb[i] = f2bf(prod + gen_value(base, i, c));
     }

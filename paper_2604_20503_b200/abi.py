@@ -89,7 +89,7 @@ class LlamaShape(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("d_model", "layers", "n_heads", "n_kv_heads", "head_dim",
                                          "ffn", "vocab", "reserved0")] + [
         (n, C.c_double) for n in ("rope_theta", "rms_eps", "bigram_scale", "embed_noise",
-                                  "init_std")] + [("seed", C.c_uint64)]
+                                  "init_std", "hard_fraction")] + [("seed", C.c_uint64)]
 
 
 class ModelDesc(C.Structure):

@@ -33,6 +33,7 @@ struct LlamaShape {
   int d, layers, n_q, n_kv, hd, ffn, vocab;
   float rope_theta, eps;
   float bigram_scale, embed_noise, init_std;
+  double hard_fraction;
   uint64_t seed;
   int qkv_out() const { return (n_q + 2 * n_kv) * hd; }
 };
@@ -47,7 +48,7 @@ __host__ __device__ inline uint64_t lm_mix64(uint64_t x) {
 }
 
 // Tensor tags (per model, per layer): tag = kind * 4096 + layer.
-enum : uint32_t { kTagLm = 1, kTagEmbNoise = 2, kTagQkv = 3, kTagO = 4, kTagGate = 5, kTagUp = 6, kTagDown = 7 };
+enum : uint32_t { kTagLm = 1, kTagEmbNoise = 2, kTagQkv = 3, kTagO = 4, kTagGate = 5, kTagUp = 6, kTagDown = 7, kTagHard = 8 };
 
 struct LayerW {
   const __nv_bfloat16* wqkv;  // [qkv_out][d]

@@ -78,6 +78,7 @@ LlamaShape shape_of(const faser_llama_shape& s) {
   m.bigram_scale = static_cast<float>(s.bigram_scale);
   m.embed_noise = static_cast<float>(s.embed_noise);
   m.init_std = static_cast<float>(s.init_std);
+  m.hard_fraction = s.hard_fraction;
   m.seed = s.seed;
   return m;
 }
@@ -93,6 +94,7 @@ void validate_shape(const faser_llama_shape& s, const char* which) {
   if (s.ffn <= 0 || s.ffn % 64) bad("ffn must be a positive multiple of 64");
   if (s.vocab < 2 || s.vocab % 128) bad("vocab must be a multiple of 128");
   if (!(s.rms_eps > 0) || !(s.rope_theta > 0) || !(s.init_std > 0)) bad("eps/theta/std must be > 0");
+  if (!(s.hard_fraction >= 0.0 && s.hard_fraction <= 1.0)) bad("hard_fraction must lie in [0, 1]");
 }
 
 // ------------------------------------------------------------------ one model on device
@@ -251,8 +253,11 @@ class LlamaEngine {
   LlamaShape dsh{}, tsh{};
   LmModel draft, target;
   LmWork wd, wt;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // draft lane (and everything in serial mode)
+  cudaStream_t vstream = nullptr;  // verify lane of the overlapped (FULL) mode
+  cudaStream_t fs = nullptr;       // stream the current forward() launches on
   cudaEvent_t ev[4] = {};
+  cudaEvent_t ev_chunk[FASER_MAX_SPEC + 1] = {};
   int nsm = 148;
   bool graph_mode = false;  // FASER_CUDA_GRAPH=1: each step is captured and replayed as one graph
   int max_spec = 16;
@@ -268,7 +273,7 @@ class LlamaEngine {
   Mem s_tok, s_len, s_ncomm, s_maxout, s_done, s_exempt, ptab;
   LmSlots sl{};
   // per-request step state (sorted order), persistent
-  Mem r_drafted, r_count, r_active, r_gl, r_npl, r_pl, r_prl, r_pr, r_fail, r_truth;
+  Mem r_drafted, r_count, r_active, r_gl, r_npl, r_pl, r_prl, r_pr, r_fail, r_truth, r_truth_rj;
   LmReqState rq{};
   LmReqState cur_q{};  // rq + this step's per-request arrays (slot, k, ...) in the blob
   // step blob
@@ -308,6 +313,9 @@ class LlamaEngine {
     if (h_res) cudaFreeHost(h_res);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto e : ev_chunk)
+      if (e) cudaEventDestroy(e);
+    if (vstream) cudaStreamDestroy(vstream);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -337,7 +345,10 @@ class LlamaEngine {
     tsh = shape_of(m->target);
     eos = tsh.vocab - 1;
     LCK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    LCK(cudaStreamCreateWithFlags(&vstream, cudaStreamNonBlocking));
+    fs = stream;
     for (auto& e : ev) LCK(cudaEventCreate(&e));
+    for (auto& e : ev_chunk) LCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     max_seq = cfg.max_seq_len + max_spec + 2;
     max_pages = (max_seq + kPage - 1) / kPage;
     n_pages = cfg.max_batch * max_pages;
@@ -375,6 +386,7 @@ class LlamaEngine {
     r_pr.alloc(B * 8);
     r_fail.alloc(B * 4);
     r_truth.alloc(static_cast<size_t>(cap) * 4);
+    r_truth_rj.alloc(static_cast<size_t>(B) * FASER_MAX_SPEC * 4);
     rq.drafted = r_drafted.as<int32_t>();
     rq.count = r_count.as<int32_t>();
     rq.active = r_active.as<int32_t>();
@@ -385,6 +397,7 @@ class LlamaEngine {
     rq.pr = r_pr.as<int32_t>();
     rq.failmask = r_fail.as<uint32_t>();
     rq.truth = r_truth.as<int32_t>();
+    rq.truth_rj = r_truth_rj.as<int32_t>();
     // blob: request arrays (5n) + verify rows (4T + 4n + 16) + ptab triples + admits + prefill rows
     blob_cap = static_cast<size_t>(B) * 64 + static_cast<size_t>(verify_rows) * 16 +
                static_cast<size_t>(B) * max_pages * 12 + static_cast<size_t>(B) * sizeof(LmAdmit) +
@@ -401,6 +414,11 @@ class LlamaEngine {
   }
 
   // ---------------------------------------------------------------- forward
+  struct VChunk {
+    RowsDev rows;
+    int T = 0, max_rows = 0;
+  };
+  bool use_graph_mode() const { return graph_mode && cfg.debug_capture == 0; }
   struct Fwd {
     RowsDev rows;
     int T = 0, n_req = 0, max_rows = 0, max_ctx = 0;
@@ -419,7 +437,7 @@ class LlamaEngine {
   }
 
   void capture_stage(int stage, const LmModel& m, const LmWork& w, const Fwd& f) {
-    LCK(cudaStreamSynchronize(stream));
+    LCK(cudaStreamSynchronize(fs));
     int n = 0;
     LCK(cudaMemcpy(&n, f.rows.n_rows, 4, cudaMemcpyDeviceToHost));
     const int V = m.sh.vocab;
@@ -482,32 +500,32 @@ class LlamaEngine {
     e_lm.logits = w.logits.as<float>();
     e_lm.amax = w.amax.as<float2>();
 
-    LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), stream));
+    LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), fs));
     ++launches;
     for (int l = 0; l < s.layers; ++l) {
       e_qkv.layer = l;
-      LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, stream));
+      LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, fs));
       LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
-                       w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, stream));
-      LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, stream));
-      LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, stream));
-      LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, stream));
+                       w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, fs));
+      LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs));
+      LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs));
+      LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs));
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
-        LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, stream));
+        LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs));
         if (f.capture) capture_stage(layer, m, w, f);
-        LCK(lm_exit_test(sl, cur_q, rows, w.logits.as<float>(), 1, 0, s.vocab, f.k_table[layer], T, stream));
-        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), stream));
+        LCK(lm_exit_test(sl, cur_q, rows, w.logits.as<float>(), 1, 0, s.vocab, f.k_table[layer], T, fs));
+        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), fs));
         LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(),
                            w.ss.as<float>(), w.xs.as<float>(), w.xbs.as<__nv_bfloat16>(), w.sss.as<float>(),
-                           stream));
+                           fs));
         launches += 5;
       }
     }
     if (f.logits) {
-      LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, stream));
-      LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, stream));
+      LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs));
+      LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, fs));
       launches += 2;
       if (f.capture) capture_stage(0, m, w, f);
     }
@@ -648,6 +666,50 @@ class LlamaEngine {
       }
       v_nrows[0] = total;
     }
+    // overlapped mode: verify row sets per frontier chunk [q*c, (q+1)*c) of drafted positions
+    struct VChunkH {
+      int32_t *nrows, *row_req, *row_pos, *row_tok, *row_j, *first, *nn, *rslot, *pos0;
+      int T, max_rows;
+    };
+    std::vector<VChunkH> chunks_h;
+    const bool overlap = cfg.mode == FASER_MODE_FULL && plan && plan->overlap.enabled &&
+                         plan->overlap.chunk >= 1 && plan->overlap.chunk < kmax && !use_graph_mode();
+    if (overlap) {
+      const int c = plan->overlap.chunk;
+      for (int q0 = 0; q0 < kmax; q0 += c) {
+        int T = 0;
+        for (int i = 0; i < n; ++i) T += std::max(0, std::min(ents[i].k, q0 + c) - q0);
+        VChunkH h;
+        h.T = T;
+        h.max_rows = std::min(c, kmax - q0);
+        h.nrows = carve<int32_t>(off, 4);
+        h.row_req = carve<int32_t>(off, T);
+        h.row_pos = carve<int32_t>(off, T);
+        h.row_tok = carve<int32_t>(off, T);
+        h.row_j = carve<int32_t>(off, T);
+        h.first = carve<int32_t>(off, n);
+        h.nn = carve<int32_t>(off, n);
+        h.rslot = carve<int32_t>(off, n);
+        h.pos0 = carve<int32_t>(off, n);
+        int row = 0;
+        for (int i = 0; i < n; ++i) {
+          Req& r = reqs.at(live[ents[i].live_idx]);
+          const int j1 = std::min(ents[i].k, q0 + c);
+          h.first[i] = row;
+          h.nn[i] = std::max(0, j1 - q0);
+          h.rslot[i] = r.slot;
+          h.pos0[i] = r.len - 1 + q0;
+          for (int j = q0; j < j1; ++j, ++row) {
+            h.row_req[row] = i;
+            h.row_pos[row] = r.len - 1 + j;
+            h.row_tok[row] = 0;
+            h.row_j[row] = j;
+          }
+        }
+        h.nrows[0] = T;
+        chunks_h.push_back(h);
+      }
+    }
     // admissions: slot row copy + page reservation for the prompt prefix
     for (int64_t id : newly) {
       Req& r = reqs.at(id);
@@ -737,6 +799,22 @@ class LlamaEngine {
     h2d = static_cast<int64_t>(blob_bytes);
     d2h = static_cast<int64_t>(sizeof(faser_round_result)) * n;
 
+    std::vector<VChunk> chunks_v;
+    for (const VChunkH& h : chunks_h) {
+      VChunk v;
+      v.T = h.T;
+      v.max_rows = h.max_rows;
+      v.rows.n_rows = dev_of(h.nrows);
+      v.rows.row_req = dev_of(h.row_req);
+      v.rows.row_pos = dev_of(h.row_pos);
+      v.rows.row_tok = dev_of(h.row_tok);
+      v.rows.row_j = dev_of(h.row_j);
+      v.rows.req_first = dev_of(h.first);
+      v.rows.req_n = dev_of(h.nn);
+      v.rows.req_slot = dev_of(h.rslot);
+      v.rows.req_pos0 = dev_of(h.pos0);
+      chunks_v.push_back(v);
+    }
     LmReqState q = rq;
     q.slot = dev_of(b_slot);
     q.k = dev_of(b_k);
@@ -786,26 +864,8 @@ class LlamaEngine {
       forward(draft, wd, f);
       forward(target, wt, f);
     }
-    // ---- draft loop
+    // ---- early-exit configuration
     const bool capture = cfg.debug_capture != 0;
-    for (int t = 0; t < kmax; ++t) {
-      int nt = 0;
-      while (nt < n && ents[nt].k > t) ++nt;
-      LCK(lm_draft_prep(sl, q, wd.rows, nt, t, stream));
-      Fwd f;
-      f.rows = wd.rows;
-      f.T = nt;
-      f.n_req = nt;
-      f.max_rows = 1;
-      f.max_ctx = maxctx;
-      f.logits = true;
-      f.argmax_out = wd.argmax.as<int>();
-      forward(draft, wd, f);
-      LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, stream));
-      launches += 2;
-    }
-    LCK(record_event(ev[1]));
-    // ---- verify (+ early exit) + accept/commit
     const bool ee = cfg.mode >= FASER_MODE_VSD_AD_EE;
     int k_table[FASER_MAX_LAYERS + 1];
     int glo = 0, ghi = 0;
@@ -824,8 +884,58 @@ class LlamaEngine {
         throw LFail{FASER_EINVAL, "invalid exit policy"};
       }
     }
-    LCK(lm_verify_prep(sl, q, vrows, n, L, eos, total, stream));
-    {
+    auto draft_step = [&](int t) {
+      int nt = 0;
+      while (nt < n && ents[nt].k > t) ++nt;
+      LCK(lm_draft_prep(sl, q, wd.rows, nt, t, stream));
+      Fwd f;
+      f.rows = wd.rows;
+      f.T = nt;
+      f.n_req = nt;
+      f.max_rows = 1;
+      f.max_ctx = maxctx;
+      f.logits = true;
+      f.argmax_out = wd.argmax.as<int>();
+      fs = stream;
+      forward(draft, wd, f);
+      LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, stream));
+      launches += 2;
+    };
+    cudaStream_t vs = stream;  // stream of the verify lane
+    if (!chunks_v.empty()) {
+      // ---- overlapped (FULL) mode: frontier chunk q is verified on the verify lane while the
+      // draft lane drafts chunk q+1 (overlap.cpp:44-91 made real); truth is scattered per
+      // (request, position) so the accept sees exactly what one full verify would produce.
+      vs = vstream;
+      const int c = plan->overlap.chunk;
+      for (size_t qi = 0; qi < chunks_v.size(); ++qi) {
+        for (int t = static_cast<int>(qi) * c; t < std::min(kmax, static_cast<int>(qi + 1) * c); ++t) draft_step(t);
+        if (qi + 1 == chunks_v.size()) LCK(record_event(ev[1]));
+        LCK(cudaEventRecord(ev_chunk[qi], stream));
+        LCK(cudaStreamWaitEvent(vstream, ev_chunk[qi], 0));
+        const VChunk& vc = chunks_v[qi];
+        LCK(lm_verify_tokens(sl, q, vc.rows, vc.T, vstream));
+        Fwd f;
+        f.rows = vc.rows;
+        f.T = vc.T;
+        f.n_req = n;
+        f.max_rows = vc.max_rows;
+        f.max_ctx = maxctx;
+        f.logits = true;
+        f.argmax_out = rq.truth;
+        fs = vstream;
+        forward(target, wt, f);
+        LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vstream));
+        launches += 2;
+      }
+      LCK(lm_verify_init(q, n, L, eos, vstream));
+      ++launches;
+    } else {
+      for (int t = 0; t < kmax; ++t) draft_step(t);
+      LCK(record_event(ev[1]));
+      // ---- verify (+ early exit)
+      LCK(lm_verify_init(q, n, L, eos, stream));
+      LCK(lm_verify_tokens(sl, q, vrows, total, stream));
       Fwd f;
       f.rows = vrows;
       f.T = total;
@@ -839,12 +949,20 @@ class LlamaEngine {
       f.gate_hi = ghi;
       f.k_table = k_table;
       f.capture = capture;
+      fs = stream;
       forward(target, wt, f);
+      LCK(lm_truth_scatter(vrows, rq.truth, rq.truth_rj, total, stream));
+      launches += 3;
     }
-    StepCtl ctl{n, L, eos, ee ? 1 : 0, cfg.exempt_rule};
-    LCK(lm_accept_commit(sl, q, vrows, ctl, d_res.as<faser_round_result>(), stream));
-    launches += 2;
-    LCK(record_event(ev[2]));
+    StepCtl ctl{n, L, eos, (ee && chunks_v.empty()) ? 1 : 0, cfg.exempt_rule};
+    LCK(lm_accept_commit(sl, q, vrows, ctl, d_res.as<faser_round_result>(), vs));
+    ++launches;
+    {
+      const cudaStream_t keep = stream;
+      stream = vs;  // record_event targets the lane that finishes the step
+      LCK(record_event(ev[2]));
+      stream = keep;
+    }
     if (use_graph) {
       capturing = false;
       cudaGraph_t g = nullptr;
@@ -856,7 +974,8 @@ class LlamaEngine {
       cudaGraphExecDestroy(ge);
       cudaGraphDestroy(g);
     }
-    LCK(cudaMemcpyAsync(h_res, d_res.p, sizeof(faser_round_result) * n, cudaMemcpyDeviceToHost, stream));
+    LCK(cudaMemcpyAsync(h_res, d_res.p, sizeof(faser_round_result) * n, cudaMemcpyDeviceToHost, vs));
+    if (vs != stream) LCK(cudaStreamSynchronize(vs));
     if (capture) {
       std::vector<int32_t> dr(static_cast<size_t>(n) * FASER_MAX_SPEC);
       LCK(cudaMemcpyAsync(dr.data(), rq.drafted, dr.size() * 4, cudaMemcpyDeviceToHost, stream));

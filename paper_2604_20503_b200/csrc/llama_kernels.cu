@@ -50,12 +50,15 @@ __global__ void init_gate_up_kernel(__nv_bfloat16* w, int ffn, int d, uint64_t b
 
 __global__ void init_embedding_kernel(__nv_bfloat16* emb, const __nv_bfloat16* lm, int vocab, int d,
                                       uint32_t ga, uint32_t gb, float beta, uint64_t base_noise,
-                                      float c) {
+                                      float c, uint64_t base_hard, double hard_fraction) {
   const int64_t n = static_cast<int64_t>(vocab) * d;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t t = i / d, col = i % d;
-    const int64_t g = (static_cast<uint64_t>(ga) * static_cast<uint64_t>(t) + gb) % static_cast<uint64_t>(vocab);
+    int64_t g = (static_cast<uint64_t>(ga) * static_cast<uint64_t>(t) + gb) % static_cast<uint64_t>(vocab);
+    // "hard" tokens: successor shifted by V/2 (exact: 53-bit integer -> double, power-of-two scale)
+    const double u = static_cast<double>(lm_mix64(base_hard + static_cast<uint64_t>(t)) >> 11) * 0x1.0p-53;
+    if (u < hard_fraction) g = (g + vocab / 2) % vocab;
     const float lv = __bfloat162float(lm[g * d + col]);
     emb[i] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(beta, lv), gen_value(base_noise, i, c)));
   }
@@ -133,7 +136,7 @@ cudaError_t lm_init_embedding(__nv_bfloat16* emb, const __nv_bfloat16* lm, const
                               uint32_t ga, uint32_t gb, cudaStream_t s) {
   init_embedding_kernel<<<grid_for(static_cast<int64_t>(m.vocab) * m.d), 256, 0, s>>>(
       emb, lm, m.vocab, m.d, ga, gb, m.bigram_scale, tensor_base(m.seed, kTagEmbNoise * 4096u),
-      scale_for(m.embed_noise));
+      scale_for(m.embed_noise), tensor_base(m.seed, kTagHard * 4096u), m.hard_fraction);
   return cudaGetLastError();
 }
 

@@ -48,17 +48,23 @@ __global__ void draft_post_kernel(LmReqState rq, const int* argmax, int n_t, int
   if (r < n_t) rq.drafted[r * kMS + t] = argmax[r];
 }
 
-__global__ void verify_prep_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layers,
-                                   int eos) {
+// Row tokens of a verify forward (whole verify or one overlap chunk): row (r, j) reads
+// ctx.back() for j == 0, else drafted[r][j-1].
+__global__ void verify_tokens_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows_cap || i >= *rows.n_rows) return;
+  const int r = rows.row_req[i], j = rows.row_j[i];
+  const int slot = rq.slot[r];
+  rows.row_tok[i] = j == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + sl.len[slot] - 1]
+                           : rq.drafted[r * kMS + j - 1];
+}
+
+// Per-request verify state once every token is drafted: drafted length (EOS stop) and the
+// early-exit frontier.
+__global__ void verify_init_kernel(LmReqState rq, int n, int layers, int eos) {
   const int r = blockIdx.x;
   if (r >= n) return;
-  const int slot = rq.slot[r];
   const int k = rq.k[r];
-  const int first = rows.req_first[r];
-  const int base = sl.len[slot] - 1;
-  for (int j = threadIdx.x; j < k; j += blockDim.x)
-    rows.row_tok[first + j] = j == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + base]
-                                     : rq.drafted[r * kMS + j - 1];
   for (int j = threadIdx.x; j < kMS; j += blockDim.x) rq.prune_layer[r * kMS + j] = layers;
   if (threadIdx.x == 0) {
     int count = k;
@@ -75,6 +81,14 @@ __global__ void verify_prep_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int 
     rq.pr[2 * r + 1] = -1;
     rq.failmask[r] = 0u;
   }
+}
+
+// Final argmax of every live verify row -> truth_rj[request][j] (chunk-order independent).
+__global__ void truth_scatter_kernel(RowsDev rows, const int* __restrict__ argmax, int* __restrict__ truth_rj,
+                                     int rows_cap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows_cap || i >= *rows.n_rows) return;
+  truth_rj[rows.row_req[i] * kMS + rows.row_j[i]] = argmax[i];
 }
 
 constexpr int kExitThreads = 256;
@@ -208,8 +222,7 @@ __global__ void accept_commit_kernel(LmSlots sl, LmReqState rq, RowsDev rows, St
   const bool ee = ctl.early_exit != 0;
   const int32_t* d = rq.drafted + r * kMS;
   const int32_t* plr = rq.prune_layer + r * kMS;
-  const int first = rows.req_first[r];
-  const int32_t* truth = rq.truth + first;
+  const int32_t* truth = rq.truth_rj + r * kMS;
   int active = ee ? rq.active[r] : count;
   int pr_j = rq.pr[2 * r], pr_l = rq.pr[2 * r + 1];
   bool pruned = pr_j >= 0;
@@ -340,11 +353,19 @@ cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cuda
   draft_post_kernel<<<cdiv(n_t, 256), 256, 0, s>>>(rq, argmax, n_t, t);
   return cudaGetLastError();
 }
-cudaError_t lm_verify_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layers, int eos,
-                           int rows_cap, cudaStream_t s) {
-  (void)rows_cap;
+cudaError_t lm_verify_tokens(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  verify_tokens_kernel<<<cdiv(rows_cap, 128), 128, 0, s>>>(sl, rq, rows, rows_cap);
+  return cudaGetLastError();
+}
+cudaError_t lm_verify_init(LmReqState rq, int n, int layers, int eos, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  verify_prep_kernel<<<n, 32, 0, s>>>(sl, rq, rows, n, layers, eos);
+  verify_init_kernel<<<n, 32, 0, s>>>(rq, n, layers, eos);
+  return cudaGetLastError();
+}
+cudaError_t lm_truth_scatter(RowsDev rows, const int* argmax, int* truth_rj, int rows_cap, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  truth_scatter_kernel<<<cdiv(rows_cap, 128), 128, 0, s>>>(rows, argmax, truth_rj, rows_cap);
   return cudaGetLastError();
 }
 cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,

@@ -39,6 +39,7 @@ struct LmReqState {
   int32_t* pr;          // [n][2] last pruned_at (j, layer), -1 if none
   uint32_t* failmask;   // [n] exit-test failures at the current gated layer
   int32_t* truth;       // [rows] final argmax per verify row (compacted order)
+  int32_t* truth_rj;    // [n][FASER_MAX_SPEC] final argmax by (request, drafted position)
 };
 
 struct StepCtl {
@@ -54,10 +55,12 @@ struct StepCtl {
 cudaError_t lm_draft_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int t, cudaStream_t s);
 // after draft step t: drafted[r][t] = argmax[r].
 cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s);
-// verify rows: request r has k'_r rows (host-built metadata); fills row tokens from drafted,
-// draft lengths (EOS stop) and resets the early-exit state.
-cudaError_t lm_verify_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layers, int eos,
-                           int rows_cap, cudaStream_t s);
+// verify rows (whole verify or one overlap chunk): row tokens from ctx.back() / drafted.
+cudaError_t lm_verify_tokens(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, cudaStream_t s);
+// once all tokens are drafted: drafted lengths (EOS stop) and the early-exit state.
+cudaError_t lm_verify_init(LmReqState rq, int n, int layers, int eos, cudaStream_t s);
+// final argmax rows -> truth_rj[request][j].
+cudaError_t lm_truth_scatter(RowsDev rows, const int* argmax, int* truth_rj, int rows_cap, cudaStream_t s);
 // K4: rank-count exit test of every live row against its drafted token at gated `layer`.
 cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,
                          int64_t split_stride, int vocab, int k_thr, int rows_cap, cudaStream_t s);

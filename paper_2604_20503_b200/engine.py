@@ -234,6 +234,11 @@ class ServingEngine:
     def set_gate(self, gate):
         self.plan.gate = gate
 
+    def set_overlap(self, enabled, chunk=2, r=0.5):
+        """OverlapPlan (overlap.hpp:11-17): in MODE_FULL, frontier chunk q of the drafted tokens
+        is verified on a second lane while chunk q+1 is drafted."""
+        self.plan.overlap = abi.OverlapPlan(1 if enabled else 0, chunk, r, 0.0, 0.0)
+
     def step(self):
         n = C.c_int32()
         _check(lib().faser_step(self.h, C.byref(self.plan), self._res, self.cfg.max_batch,

@@ -11,11 +11,11 @@ BIGRAM_A = 7919  # prime, coprime to every preset vocab
 
 
 def shape(d, layers, heads, kv_heads, head_dim, ffn, vocab, seed, theta=10000.0, eps=1e-5,
-          bigram=8.0, noise=0.02, std=0.02):
+          bigram=8.0, noise=0.02, std=0.02, hard=0.0):
     return abi.LlamaShape(d_model=d, layers=layers, n_heads=heads, n_kv_heads=kv_heads,
                           head_dim=head_dim, ffn=ffn, vocab=vocab, reserved0=0, rope_theta=theta,
                           rms_eps=eps, bigram_scale=bigram, embed_noise=noise, init_std=std,
-                          seed=seed)
+                          hard_fraction=hard, seed=seed)
 
 
 def _pair(draft, target, b=12345):
@@ -24,33 +24,39 @@ def _pair(draft, target, b=12345):
                          bigram_b=b % target.vocab)
 
 
-# Target bigram strength sets the acceptance rate (tuned on B200).
-TARGET_BIGRAM = {"tiny": 2.0, "cfg3": 22.0, "cfg4": 22.0}
+# Target bigram strength + hard-token fraction set the acceptance rate (tuned on B200,
+# DESIGN.md section 3): a strong bigram makes the target follow its successor map; the draft
+# disagrees exactly on the target's "hard" tokens (successor shifted by V/2).
+TARGET_BIGRAM = {"tiny": 2.0, "cfg3": 32.0, "cfg4": 128.0}
+TARGET_HARD = {"tiny": 0.0, "cfg3": 0.2, "cfg4": 0.2}
 DRAFT_BIGRAM = 24.0
 
 
-def config3(target_bigram=None, draft_bigram=None):
+def config3(target_bigram=None, draft_bigram=None, hard=None):
     """llama-68m-shaped draft / TinyLlama-1.1B-shaped target, V=32000 (config 3)."""
     tb = TARGET_BIGRAM["cfg3"] if target_bigram is None else target_bigram
     db = DRAFT_BIGRAM if draft_bigram is None else draft_bigram
+    hf = TARGET_HARD["cfg3"] if hard is None else hard
     return _pair(shape(768, 2, 12, 12, 64, 3072, 32000, seed=11, bigram=db),
-                 shape(2048, 22, 32, 4, 64, 5632, 32000, seed=12, bigram=tb))
+                 shape(2048, 22, 32, 4, 64, 5632, 32000, seed=12, bigram=tb, hard=hf))
 
 
-def config4(target_bigram=None, draft_bigram=None):
+def config4(target_bigram=None, draft_bigram=None, hard=None):
     """Llama-3.2-1B-shaped draft / Llama-3.1-8B-shaped target, V=128256 (config 4)."""
     tb = TARGET_BIGRAM["cfg4"] if target_bigram is None else target_bigram
     db = DRAFT_BIGRAM if draft_bigram is None else draft_bigram
+    hf = TARGET_HARD["cfg4"] if hard is None else hard
     return _pair(shape(2048, 16, 32, 8, 64, 8192, 128256, seed=21, theta=500000.0, bigram=db),
-                 shape(4096, 32, 32, 8, 128, 14336, 128256, seed=22, theta=500000.0, bigram=tb))
+                 shape(4096, 32, 32, 8, 128, 14336, 128256, seed=22, theta=500000.0, bigram=tb, hard=hf))
 
 
-def tiny(target_bigram=None, draft_bigram=None, vocab=512):
+def tiny(target_bigram=None, draft_bigram=None, vocab=512, hard=None):
     """Small pair with the same structure (GQA target, MHA draft) for fast parity tests."""
     tb = TARGET_BIGRAM["tiny"] if target_bigram is None else target_bigram
     db = DRAFT_BIGRAM if draft_bigram is None else draft_bigram
+    hf = TARGET_HARD["tiny"] if hard is None else hard
     return _pair(shape(128, 2, 2, 2, 64, 256, vocab, seed=31, bigram=db),
-                 shape(256, 4, 4, 2, 64, 512, vocab, seed=32, bigram=tb))
+                 shape(256, 4, 4, 2, 64, 512, vocab, seed=32, bigram=tb, hard=hf))
 
 
 PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4}

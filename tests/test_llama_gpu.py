@@ -316,3 +316,31 @@ def test_engine_rejects_bad_requests():
     eng.submit(3, [1, 2, 3], 0)  # max_out 0: done immediately, never scheduled
     assert eng.live_requests() == []
     eng.close()
+
+
+@pytest.mark.parametrize("chunk,k", [(1, 4), (2, 5), (3, 7)])
+def test_overlapped_full_mode_matches_serial(chunk, k):
+    """MODE_FULL with an overlap plan (frontier chunks verified on a second lane while the next
+    chunk is drafted) must take the same decisions as the serial verify and stay lossless."""
+    desc = llama.tiny()
+    V = desc.target.vocab
+    rng = np.random.default_rng(17)
+    prompts = rand_prompts(V, 6, rng, 2, 50)
+    max_out = [int(rng.integers(3, 30)) for _ in range(6)]
+    outs = {}
+    for mode in (abi.MODE_VSD, abi.MODE_FULL):
+        eng = engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=160, mode=mode, default_spec_length=k,
+                                   max_spec_length=16, prefill_rows=1024)
+        for i, (p, m) in enumerate(zip(prompts, max_out)):
+            eng.submit(i, p, m)
+        log = []
+        while eng.live_requests():
+            eng.set_overlap(mode == abi.MODE_FULL, chunk)
+            log += [(r.req_id, r.drafted, r.outcome.accepted_count, tuple(r.tokens[:r.committed])) for r in eng.step()]
+        outs[mode] = (log, [eng.committed(i) for i in range(6)])
+        eng.close()
+    assert outs[abi.MODE_FULL][1] == outs[abi.MODE_VSD][1]
+    assert outs[abi.MODE_FULL][0] == outs[abi.MODE_VSD][0]
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
+    for i, (p, m) in enumerate(zip(prompts, max_out)):
+        assert outs[abi.MODE_FULL][1][i] == tgt.greedy(p, m, V - 1)

@@ -9,8 +9,9 @@ from paper_2604_20503_b200 import abi, engine, llama  # noqa: E402
 
 preset = sys.argv[1]
 betas = [float(b) for b in sys.argv[2].split(",")]
+hard = float(sys.argv[3]) if len(sys.argv) > 3 else None
 for beta in betas:
-    desc = llama.PRESETS[preset](target_bigram=beta)
+    desc = llama.PRESETS[preset](target_bigram=beta, hard=hard)
     V = desc.target.vocab
     rng = np.random.default_rng(1)
     eng = engine.ServingEngine(desc=desc, max_batch=16, max_seq_len=512, mode=abi.MODE_VSD,
