@@ -126,6 +126,24 @@ def prompts_for(base, n, vocab, in_range, out_range, seed=1):
     return out, outl[base:base + n]
 
 
+def shard_base(rank, n_req):
+    """Request-sharded replicas: rank r owns requests [r*n_req, (r+1)*n_req) of the workload
+    (synth_prompt is indexed, so the shards are disjoint and their union is the 1-GPU run)."""
+    return rank * n_req
+
+
+def aggregate(stats, dist):
+    """Whole-job numbers: device time and e2e wall time are the MAX over ranks, tokens the SUM.
+    stats = [dev_ms, tokens, e2e_s, e2e_tokens] (float64 tensor on this rank's device)."""
+    if dist is None:
+        return [float(x) for x in stats.tolist()]
+    mx = stats.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = stats.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return [mx[0].item(), sm[1].item(), mx[2].item(), sm[3].item()]
+
+
 def p50_tpot_ms(first, last):
     tp = [(last[r][0] - first[r]) / (last[r][1] - 1) for r in last if last[r][1] >= 2]
     return 1e3 * statistics.median(tp) if tp else None
@@ -202,7 +220,7 @@ def llama_ours(args, rank, world, local_rank):
     B = args.batch
     V = desc.target.vocab
     n_req = B * (args.steps + args.warmup) // 40 + 2 * B
-    base = rank * n_req  # request-sharded replicas: each rank owns its own requests
+    base = shard_base(rank, n_req)  # request-sharded replicas: each rank owns its own requests
     prompts, outl = prompts_for(base, n_req, V, IN_RANGE, OUT_RANGE)
     gate = gate_plan(desc, args)
     chunk = args.chunk if args.mode in ("ov", "full") else 0
@@ -296,13 +314,7 @@ def llama_ours(args, rank, world, local_rank):
     eng.close()
 
     stats = torch.tensor([dev_ms, float(tokens), e2e_s, float(tokens2)], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        mx = stats.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = stats.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        dev_ms, e2e_s = mx[0].item(), mx[2].item()
-        tokens, tokens2 = sm[1].item(), sm[3].item()
+    dev_ms, tokens, e2e_s, tokens2 = aggregate(stats, dist)
     if rank != 0:
         if dist is not None:
             dist.barrier()

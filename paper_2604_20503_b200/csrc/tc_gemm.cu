@@ -27,6 +27,7 @@
 
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "sm100.cuh"
@@ -375,6 +376,8 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
   attr[1].val.clusterDim.x = 1;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = z;
+  static const bool no_pdl = getenv("FASER_NO_PDL") != nullptr;
+  attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = z > 1 ? 2 : 1;  // cluster launch only when the K split needs DSMEM
   return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST>, w.map, x.map, ea, w.rows, kb_total, kps, z);

@@ -344,3 +344,28 @@ def test_overlapped_full_mode_matches_serial(chunk, k):
     tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
     for i, (p, m) in enumerate(zip(prompts, max_out)):
         assert outs[abi.MODE_FULL][1][i] == tgt.greedy(p, m, V - 1)
+
+
+def test_request_sharded_replicas_equal_single_engine():
+    """Configs 1-4 shard by request: two independent engines (replicas; here on one
+    device) serving disjoint halves produce per-request outputs identical to one engine serving
+    the whole backlog."""
+    desc = llama.tiny()
+    V = desc.target.vocab
+    rng = np.random.default_rng(23)
+    prompts = rand_prompts(V, 10, rng, 2, 40)
+    max_out = [int(rng.integers(3, 25)) for _ in range(10)]
+
+    def serve(ids):
+        eng = make(desc, batch=4, k=4)
+        for i in ids:
+            eng.submit(i, prompts[i], max_out[i])
+        while eng.live_requests():
+            eng.step()
+        out = {i: eng.committed(i) for i in ids}
+        eng.close()
+        return out
+
+    single = serve(range(10))
+    sharded = {**serve(range(0, 10, 2)), **serve(range(1, 10, 2))}
+    assert sharded == single
