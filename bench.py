@@ -276,6 +276,14 @@ def llama_ours(args, rank, world, local_rank):
     launches = eng.kernel_launches() - launches0
     dev_ms = ev0.elapsed_time(ev1)
     tpot = p50_tpot_ms(st["first"], st["last"])
+    # per-kernel-class CUDA-event timing over steps that immediately follow the timed region
+    # (same engine and workload state; kept out of the timed region so event records cannot
+    # perturb the programmatic-dependent-launch overlap being measured)
+    eng.set_kernel_timing(True)
+    run_llama_steps(eng, max(args.steps // 2, 3), clock, {"first": {}, "last": {}}, gate=gate,
+                    drafter=drafter, chunk=chunk)
+    kstats = eng.kernel_stats()
+    eng.set_kernel_timing(False)
     eng.close()
 
     # ---------------------------------------------------------------- e2e (host buffers)
@@ -342,13 +350,36 @@ def llama_ours(args, rank, world, local_rank):
         "layer_work_per_drafted_token": st.get("flr", 0.0) / max(st.get("sub", 1), 1),
         "wall_s_timed": wall,
     }
-    line["roofline"] = llama_roofline(desc, B, args.k, verify_ms / k, draft_ms / k)
+    line["roofline"], line["kernels"] = kernel_roofline(kstats)
+    line["verify_forward_roofline"] = llama_roofline(desc, B, args.k, verify_ms / k, draft_ms / k)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = llama_cpu_baseline(desc, args, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def kernel_roofline(kstats):
+    """roofline object for the dominant kernel class (largest device time), achieved =
+    algorithmic bytes per launch / average launch duration (CUDA events around each launch)."""
+    pk, src = peaks()
+    table = {}
+    for name, v in kstats.items():
+        if v["launches"]:
+            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            table[name] = {"avg_us": 1e3 * v["ms"] / v["launches"], "launches": v["launches"],
+                           "bytes_per_launch": v["bytes"] / v["launches"], "achieved_GBs": gbs,
+                           "frac_hbm": gbs / pk["hbm_gbs"], "total_ms": v["ms"]}
+    if not table:
+        return None, table
+    top = max(table, key=lambda n: table[n]["total_ms"])
+    t = table[top]
+    roof = {"bound": "hbm", "achieved": t["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": t["achieved_GBs"] / pk["hbm_gbs"], "traffic": None, "peak_source": src,
+            "kernel": top, "avg_launch_us": t["avg_us"], "bytes_per_launch": t["bytes_per_launch"],
+            "share_of_timed_kernels": t["total_ms"] / sum(x["total_ms"] for x in table.values())}
+    return roof, table
 
 
 def llama_roofline(desc, B, k, verify_ms, draft_ms):

@@ -276,6 +276,15 @@ faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* page
 faser_status faser_debug_weights(faser_engine* e, int32_t model, int32_t which, int32_t layer,
                                  int64_t offset, int32_t n, uint16_t* out);
 
+/* Per-kernel-class device timing (CUDA events recorded around every launch of the class on its
+ * stream; enabled by faser_set_kernel_timing, off by default). Classes: 0 target verify
+ * projection GEMMs (tcgen05), 1 target verify attention, 2 draft-model GEMMs, 3 draft
+ * attention, 4 target LM-head GEMM (final + gated). Accumulated since the last reset:
+ * total ms, launches, algorithmic bytes (weights + activations read + outputs written). */
+faser_status faser_set_kernel_timing(faser_engine* e, int32_t enabled);
+faser_status faser_kernel_stats(faser_engine* e, int32_t cls, double* ms, int64_t* launches,
+                                double* bytes);
+
 /* ABI self-description: FASER_ABI_VERSION and sizeof() of every struct above, in
  * declaration order (toy_params, exit_policy, gate_plan, gate_entry, overlap_plan,
  * latency_params, latency_model, verify_outcome, model_desc, engine_cfg, step_plan,

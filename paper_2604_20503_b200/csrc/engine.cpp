@@ -518,6 +518,16 @@ faser_status faser_debug_weights(faser_engine* e, int32_t model, int32_t which, 
   return faser::llama_debug_weights(e->llama, model, which, layer, offset, n, out);
 }
 
+faser_status faser_set_kernel_timing(faser_engine* e, int32_t enabled) {
+  if (!e || !e->llama) return FASER_EINVAL;
+  return faser::llama_set_kernel_timing(e->llama, enabled);
+}
+
+faser_status faser_kernel_stats(faser_engine* e, int32_t cls, double* ms, int64_t* launches, double* bytes) {
+  if (!e || !e->llama) return FASER_EINVAL;
+  return faser::llama_kernel_stats(e->llama, cls, ms, launches, bytes);
+}
+
 faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n) {
   if (!e || !n || !e->llama) return FASER_EINVAL;
   return faser::llama_debug_kv_pages(e->llama, req_id, pages, cap, n);

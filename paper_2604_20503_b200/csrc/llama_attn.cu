@@ -8,9 +8,9 @@
 // (m16n8k16, fp32 accumulate); K/V pages (64 tokens x head_dim, contiguous) are staged into
 // XOR-swizzled shared memory with a 3-stage cp.async pipeline.
 // Two work splits:
-//   GROUP mode (<= 64 packed rows, decode/verify): ONE CTA per (request, kv head) holds all
-//            of its 1/2/4 M tiles, so each KV page is read once; warps split the page's four
-//            16-key chunks among the warps sharing an M tile and merge through smem.
+//   GROUP mode (<= 64 packed rows, decode/verify): one CTA per (request, kv head, 16-row M
+//            tile); the 4 warps split each page's four 16-key chunks and merge through smem
+//            (short per-warp dependency chains; the extra page reads hit L2).
 //   ROWS mode (> 64 packed rows, long verify / prefill): each warp owns a 16-row M tile and
 //            walks all keys of the page; CTAs cover 64 packed rows each.
 // Few CTAs + long contexts split over KV (flash-decoding); the LAST split CTA to finish a
@@ -21,6 +21,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "llama.cuh"
 
@@ -84,20 +85,23 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
 
   const int req = blockIdx.x, kvh = blockIdx.y;
   const int nr = rows.req_n[req];
-  const int G = n_q / n_kv;
-  const int M = nr * G;
+  const int gs = 31 - __clz(n_q / n_kv);  // G = n_q / n_kv is a power of two (checked on the host)
+  const int gm = (1 << gs) - 1;
+  const int G = 1 << gs;
+  const int M = nr << gs;
   const int blk = blockIdx.z / n_split, sp = blockIdx.z % n_split;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta_m0 = ROWS ? blk * 64 : 0;
+  const int cta_m0 = ROWS ? blk * 64 : blk * 16;
   if (cta_m0 >= M) return;
-  const int cta_m1 = ROWS ? min(M, cta_m0 + 64) : M;
-  // GROUP mode: nmt M tiles, warps (mt = warp % nmt) share tile mt and take every nkg-th chunk
-  const int nmt = ROWS ? 4 : (M <= 16 ? 1 : M <= 32 ? 2 : 4);
+  const int cta_m1 = min(M, cta_m0 + (ROWS ? 64 : 16));
+  // GROUP mode: one 16-row M tile per CTA, the 4 warps split each page's four 16-key chunks
+  // (latency-bound decode: short per-warp dependency chains beat reading each page once)
+  const int nmt = ROWS ? 4 : 1;
   const int nkg = 4 / nmt;
   const int mt = warp % nmt, kg = warp / nmt;
   const int first = rows.req_first[req], pos0 = rows.req_pos0[req];
   const int slot = rows.req_slot[req];
-  const int key_end = pos0 + (cta_m1 - 1) / G + 1;
+  const int key_end = pos0 + ((cta_m1 - 1) >> gs) + 1;
   const int tiles = (key_end + 63) / 64;
   const int tps = (tiles + n_split - 1) / n_split;
   const int t0 = sp * tps, t1 = min(tiles, t0 + tps);
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   const int mlo = mt0 + (lane >> 2), mhi = mlo + 8;
   uint32_t qa[kKS][4];
   {
-    const int rlo = mlo / G, glo = mlo % G, rhi = mhi / G, ghi = mhi % G;
+    const int rlo = mlo >> gs, glo = mlo & gm, rhi = mhi >> gs, ghi = mhi & gm;
     const bool vlo = mlo < cta_m1, vhi = mhi < cta_m1;
     const __nv_bfloat16* qlo = qbuf + (static_cast<int64_t>(first + (vlo ? rlo : 0)) * n_q + kvh * G + glo) * HD;
     const __nv_bfloat16* qhi = qbuf + (static_cast<int64_t>(first + (vhi ? rhi : 0)) * n_q + kvh * G + ghi) * HD;
@@ -120,9 +124,9 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
       qa[kk][3] = vhi ? *reinterpret_cast<const uint32_t*>(qhi + c + 8) : 0u;
     }
   }
-  const int lim_lo = pos0 + mlo / G, lim_hi = pos0 + mhi / G;  // last visible key per row
+  const int lim_lo = pos0 + (mlo >> gs), lim_hi = pos0 + (mhi >> gs);  // last visible key per row
   // warp-uniform: last key any row of this warp's tile can see (-1: tile past the live rows)
-  const int warp_lim = mt0 < cta_m1 ? pos0 + (min(mt0 + 15, cta_m1 - 1)) / G : -1;
+  const int warp_lim = mt0 < cta_m1 ? pos0 + ((min(mt0 + 15, cta_m1 - 1)) >> gs) : -1;
 
   float o[kDT][4];
 #pragma unroll
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
       l += sl_[w * 16 + r] * f;
       acc += so[(w * 16 + r) * HD + col] * f;
     }
-    const int row = first + m / G, head = kvh * G + m % G;
+    const int row = first + (m >> gs), head = kvh * G + (m & gm);
     if (n_split == 1) {
       obuf[(static_cast<int64_t>(row) * n_q + head) * HD + col] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
     } else {
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   const int nrow = cta_m1 - cta_m0;
   for (int mr = threadIdx.x; mr < nrow; mr += 128) {
     const int m = cta_m0 + mr;
-    const int row = first + m / G, head = kvh * G + m % G;
+    const int row = first + (m >> gs), head = kvh * G + (m & gm);
     float2 ml[16];
     float mm = kNegBig;
 #pragma unroll
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   for (int e = threadIdx.x; e < nrow * (HD / 4); e += 128) {
     const int mr = e / (HD / 4), c4 = (e % (HD / 4)) * 4;
     const int m = cta_m0 + mr;
-    const int row = first + m / G, head = kvh * G + m % G;
+    const int row = first + (m >> gs), head = kvh * G + (m & gm);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int sp2 = 0; sp2 < 16; ++sp2) {
@@ -371,9 +375,10 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   if (n_req <= 0 || max_rows_per_req <= 0) return cudaSuccess;
   if (m.hd != 64 && m.hd != 128) return cudaErrorInvalidValue;
   const int G = m.n_q / m.n_kv;
+  if (G & (G - 1)) return cudaErrorInvalidValue;  // GQA group must be a power of two
   const int Mmax = max_rows_per_req * G;
   const bool rows_mode = Mmax > 64;
-  const int blocks = rows_mode ? (Mmax + 63) / 64 : 1;
+  const int blocks = rows_mode ? (Mmax + 63) / 64 : (Mmax + 15) / 16;
   const int rows_cap = n_req * max_rows_per_req;  // row indices are < sum of req_n <= this
   // scratch = [counters (1 MiB, zeroed at allocation, self-resetting)][part_o][part_ml]
   constexpr size_t kCounterBytes = size_t(1) << 20;
@@ -384,8 +389,9 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   const int base = n_req * m.n_kv * blocks;
   const int tiles = (max_ctx + 63) / 64;
   int n_split = 1;
-  if (base < 148 && tiles >= 4) {
-    n_split = (2 * 148 + base - 1) / base;
+  static const int target = getenv("FASER_ATTN_CTAS") ? atoi(getenv("FASER_ATTN_CTAS")) : 148;
+  if (base < target / 2 && tiles >= 4) {
+    n_split = (target + base - 1) / base;
     const int max_split = (tiles + 1) / 2 < 16 ? (tiles + 1) / 2 : 16;  // >= 2 pages per split
     if (n_split > max_split) n_split = max_split;
   }

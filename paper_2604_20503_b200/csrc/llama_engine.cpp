@@ -89,6 +89,7 @@ void validate_shape(const faser_llama_shape& s, const char* which) {
   if (s.layers < 1 || s.layers > FASER_MAX_LAYERS) bad("layers out of range");
   if (s.head_dim != 64 && s.head_dim != 128) bad("head_dim must be 64 or 128");
   if (s.n_heads < 1 || s.n_kv_heads < 1 || s.n_heads % s.n_kv_heads) bad("n_heads must be a multiple of n_kv_heads");
+  if ((s.n_heads / s.n_kv_heads) & (s.n_heads / s.n_kv_heads - 1)) bad("n_heads / n_kv_heads must be a power of two");
   if ((s.n_heads + 2 * s.n_kv_heads) * s.head_dim % 128) bad("qkv width must be a multiple of 128");
   if ((s.n_heads * s.head_dim) % 128) bad("n_heads*head_dim must be a multiple of 128");
   if (s.ffn <= 0 || s.ffn % 64) bad("ffn must be a positive multiple of 64");
@@ -428,9 +429,57 @@ class LlamaEngine {
     int gate_lo = 0, gate_hi = 0;
     const int* k_table = nullptr;
     bool capture = false;
+    int64_t kv_tokens = 0;  // sum over requests of the context each attention call reads
   };
 
   GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, nsm); }
+  // ---- per-kernel-class timing (opt-in): event pairs around launches, resolved after the step
+  static constexpr int kClasses = 5;
+  bool ktiming = false;
+  struct KPend {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<KPend> kpend;
+  std::vector<cudaEvent_t> kpool;
+  double k_ms[kClasses] = {}, k_bytes[kClasses] = {};
+  int64_t k_n[kClasses] = {};
+  cudaEvent_t kev() {
+    if (kpool.empty()) {
+      cudaEvent_t e;
+      LCK(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = kpool.back();
+    kpool.pop_back();
+    return e;
+  }
+  template <class F>
+  void timed(int cls, double bytes, F&& launch) {
+    if (!ktiming || capturing || cls < 0) {
+      launch();
+      return;
+    }
+    KPend p{cls, kev(), kev(), bytes};
+    LCK(cudaEventRecord(p.a, fs));
+    launch();
+    LCK(cudaEventRecord(p.b, fs));
+    kpend.push_back(p);
+  }
+  void resolve_kernel_timing() {
+    for (KPend& p : kpend) {
+      float ms = 0.f;
+      LCK(cudaEventSynchronize(p.b));
+      LCK(cudaEventElapsedTime(&ms, p.a, p.b));
+      k_ms[p.cls] += ms;
+      k_bytes[p.cls] += p.bytes;
+      k_n[p.cls] += 1;
+      kpool.push_back(p.a);
+      kpool.push_back(p.b);
+    }
+    kpend.clear();
+  }
   bool capturing = false;
   cudaError_t record_event(cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal) : cudaEventRecord(e, stream);
@@ -502,14 +551,27 @@ class LlamaEngine {
 
     LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), fs));
     ++launches;
+    // kernel classes for timing: target verify (logits) vs draft model; prefill untimed
+    const bool is_target = &m == &target;
+    const int gcls = f.logits ? (is_target ? 0 : 2) : -1;
+    const int acls = f.logits ? (is_target ? 1 : 3) : -1;
+    // algorithmic bytes of one projection launch: weights + activation rows in (bf16) + out
+    auto gbytes = [&](int64_t n_out, int64_t k, int64_t out_cols) {
+      return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * out_cols;
+    };
+    // attention: the K/V bytes every request reads (its context incl. the new rows) + q/o
+    const double abytes = static_cast<double>(f.kv_tokens) * 2 * s.n_kv * s.hd * 2 + 4.0 * T * s.n_q * s.hd;
     for (int l = 0; l < s.layers; ++l) {
       e_qkv.layer = l;
-      LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, fs));
-      LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
-                       w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, fs));
-      LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs));
-      LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs));
-      LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs));
+      timed(gcls, gbytes(s.qkv_out(), s.d, s.qkv_out()),
+            [&] { LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, fs)); });
+      timed(acls, abytes, [&] {
+        LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
+                         w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, fs));
+      });
+      timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); });
+      timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); });
+      timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); });
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
@@ -524,7 +586,8 @@ class LlamaEngine {
       }
     }
     if (f.logits) {
-      LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs));
+      timed(is_target ? 4 : 2, gbytes(s.vocab, s.d, 2 * s.vocab),
+            [&] { LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs)); });
       LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, fs));
       launches += 2;
       if (f.capture) capture_stage(0, m, w, f);
@@ -607,6 +670,7 @@ class LlamaEngine {
     };
     std::vector<Ent> ents(n);
     int kmax = 0, total = 0, maxctx = 0;
+    int64_t ctx_sum = 0;
     for (int i = 0; i < n; ++i) {
       Req& r = reqs.at(live[i]);
       const int remaining = r.max_out - static_cast<int>(r.committed.size());
@@ -623,6 +687,7 @@ class LlamaEngine {
       // draft & verify write positions len-1 .. len+k-2
       ensure_pages(r, r.len + ents[i].k - 2);
       maxctx = std::max(maxctx, r.len - 1 + ents[i].k);
+      ctx_sum += r.len - 1;
     }
     if (total > wt.rows_cap) throw LFail{FASER_ECAPACITY, "verify rows exceed capacity"};
 
@@ -896,6 +961,7 @@ class LlamaEngine {
       f.max_ctx = maxctx;
       f.logits = true;
       f.argmax_out = wd.argmax.as<int>();
+      f.kv_tokens = ctx_sum + static_cast<int64_t>(nt) * (t + 1);
       fs = stream;
       forward(draft, wd, f);
       LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, stream));
@@ -923,6 +989,7 @@ class LlamaEngine {
         f.max_ctx = maxctx;
         f.logits = true;
         f.argmax_out = rq.truth;
+        f.kv_tokens = ctx_sum + vc.T;
         fs = vstream;
         forward(target, wt, f);
         LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vstream));
@@ -944,6 +1011,7 @@ class LlamaEngine {
       f.max_ctx = maxctx;
       f.logits = true;
       f.argmax_out = rq.truth;
+      f.kv_tokens = ctx_sum + total;
       f.ee = ee;
       f.gate_lo = glo;
       f.gate_hi = ghi;
@@ -986,6 +1054,7 @@ class LlamaEngine {
                     &dr[static_cast<size_t>(i) * FASER_MAX_SPEC], FASER_MAX_SPEC * 4);
     }
     LCK(cudaStreamSynchronize(stream));
+    if (ktiming) resolve_kernel_timing();
     cudaEventElapsedTime(&t_draft, ev[0], ev[1]);
     cudaEventElapsedTime(&t_verify, ev[1], ev[2]);
     cudaEventElapsedTime(&t_step, ev[0], ev[2]);
@@ -1187,6 +1256,26 @@ faser_status llama_debug_weights(LlamaEngine* e, int32_t model, int32_t which, i
     }
     if (offset < 0 || offset + n > size) throw LFail{FASER_EINVAL, "range outside tensor"};
     LCK(cudaMemcpy(out, static_cast<const uint16_t*>(base) + offset, static_cast<size_t>(n) * 2, cudaMemcpyDeviceToHost));
+  });
+}
+}  // namespace faser
+
+namespace faser {
+faser_status llama_set_kernel_timing(LlamaEngine* e, int32_t on) {
+  return lguard(e, [&] {
+    e->ktiming = on != 0;
+    for (int c = 0; c < LlamaEngine::kClasses; ++c) {
+      e->k_ms[c] = e->k_bytes[c] = 0.0;
+      e->k_n[c] = 0;
+    }
+  });
+}
+faser_status llama_kernel_stats(LlamaEngine* e, int32_t cls, double* ms, int64_t* launches, double* bytes) {
+  return lguard(e, [&] {
+    if (cls < 0 || cls >= LlamaEngine::kClasses) throw LFail{FASER_EINVAL, "unknown kernel class"};
+    if (ms) *ms = e->k_ms[cls];
+    if (launches) *launches = e->k_n[cls];
+    if (bytes) *bytes = e->k_bytes[cls];
   });
 }
 }  // namespace faser

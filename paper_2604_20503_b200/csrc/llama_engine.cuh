@@ -37,6 +37,8 @@ faser_status llama_debug_verify_logits(LlamaEngine* e, int32_t stage, float* log
 faser_status llama_debug_drafted(LlamaEngine* e, int32_t* drafted, int32_t cap, int32_t* n);
 faser_status llama_debug_weights(LlamaEngine* e, int32_t model, int32_t which, int32_t layer, int64_t offset,
                                  int32_t n, uint16_t* out);
+faser_status llama_set_kernel_timing(LlamaEngine* e, int32_t on);
+faser_status llama_kernel_stats(LlamaEngine* e, int32_t cls, double* ms, int64_t* launches, double* bytes);
 faser_status llama_debug_kv_pages(LlamaEngine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n);
 
 }  // namespace faser

@@ -271,6 +271,20 @@ class ServingEngine:
     def kernel_launches(self):
         return lib().faser_kernel_launches(self.h)
 
+    # ---- per-kernel-class device timing (CUDA events around launches)
+    KERNEL_CLASSES = ("verify_gemm", "verify_attention", "draft_gemm", "draft_attention", "verify_lm_head")
+
+    def set_kernel_timing(self, enabled):
+        _check(lib().faser_set_kernel_timing(self.h, 1 if enabled else 0), self.h)
+
+    def kernel_stats(self):
+        out = {}
+        for i, name in enumerate(self.KERNEL_CLASSES):
+            ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+            _check(lib().faser_kernel_stats(self.h, i, C.byref(ms), C.byref(n), C.byref(b)), self.h)
+            out[name] = {"ms": ms.value, "launches": n.value, "bytes": b.value}
+        return out
+
     # ---- Llama validation hooks (cfg.debug_capture = 1)
     def debug_verify_logits(self, stage=0):
         """(logits [rows][V] float32, ids [rows][2] = (req_id, j)) of the last step's verify
