@@ -27,6 +27,18 @@ faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t
 faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, int32_t n_out,
                                     int32_t t, int32_t k, int32_t bn, int32_t splits, void* stream);
 
+/* K3: causal attention of n_req ragged query blocks over the paged KV cache (one layer).
+ * q bf16 [rows][n_q][hd]; kv bf16 pool [pages][n_kv][2 (K,V)][64][hd]; ptab int32
+ * [n_req][max_pages] (request i uses ptab row i); request i has req_n[i] query rows starting at
+ * row req_first[i], at positions req_pos0[i] .. req_pos0[i]+req_n[i]-1, attending to keys
+ * [0, pos]. out bf16 [rows][n_q][hd]. scratch: device workspace (>= 2 MiB, first MiB zeroed
+ * before the first call). n_q / n_kv must be a power of two, hd in {64, 128}. */
+faser_status faser_k_attention(const void* q, const void* kv, const int32_t* ptab, int32_t max_pages,
+                               int32_t n_req, const int32_t* req_first, const int32_t* req_n,
+                               const int32_t* req_pos0, int32_t max_rows, int32_t max_ctx,
+                               int32_t n_q, int32_t n_kv, int32_t hd, void* out, void* scratch,
+                               int64_t scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,10 +5,17 @@
 #include <string>
 
 #include "faser/kernels.h"
+#include "llama.cuh"
 #include "tc_gemm.cuh"
 
 namespace faser {
 namespace {
+
+__global__ void iota_kernel(int* a, int n, int* n_rows, int total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+  if (i == 0) *n_rows = total;
+}
 
 int num_sms() {
   static int n = 0;
@@ -62,4 +69,46 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
 extern "C" faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,
                                           int32_t t, int32_t k, int32_t splits, void* stream) {
   return faser_k_gemm_bf16_plan(w, x, out, n_out, t, k, 0, splits, stream);
+}
+
+extern "C" faser_status faser_k_attention(const void* q, const void* kv, const int32_t* ptab, int32_t max_pages,
+                                          int32_t n_req, const int32_t* req_first, const int32_t* req_n,
+                                          const int32_t* req_pos0, int32_t max_rows, int32_t max_ctx,
+                                          int32_t n_q, int32_t n_kv, int32_t hd, void* out, void* scratch,
+                                          int64_t scratch_bytes, void* stream) {
+  if (!q || !kv || !ptab || !req_first || !req_n || !req_pos0 || !out || !scratch) return FASER_EINVAL;
+  if (n_req <= 0 || max_rows <= 0 || n_q <= 0 || n_kv <= 0 || n_q % n_kv || (hd != 64 && hd != 128) ||
+      scratch_bytes < (int64_t(2) << 20))
+    return FASER_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FASER_ECUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // request i's slot (page-table row) is i; n_rows is unused by the kernel but kept valid
+  static int* d_slot = nullptr;
+  static int cap = 0;
+  if (n_req + 1 > cap) {
+    if (d_slot) cudaFree(d_slot);
+    cap = n_req + 1 > 4096 ? n_req + 1 : 4096;
+    if (cudaMalloc(&d_slot, sizeof(int) * cap) != cudaSuccess) return FASER_ENOMEM;
+  }
+  iota_kernel<<<(n_req + 255) / 256, 256, 0, s>>>(d_slot, n_req, d_slot + n_req, max_rows * n_req);
+  LlamaShape m{};
+  m.n_q = n_q;
+  m.n_kv = n_kv;
+  m.hd = hd;
+  RowsDev rows{};
+  rows.n_rows = d_slot + n_req;
+  rows.req_first = const_cast<int*>(req_first);
+  rows.req_n = const_cast<int*>(req_n);
+  rows.req_slot = d_slot;
+  rows.req_pos0 = const_cast<int*>(req_pos0);
+  KvDev kvd{};
+  kvd.pool = static_cast<__nv_bfloat16*>(const_cast<void*>(kv));
+  kvd.ptab = ptab;
+  kvd.max_pages = max_pages;
+  kvd.layer_stride = 0;
+  cudaError_t e = lm_attention(m, rows, n_req, max_rows, max_ctx, kvd, 0, static_cast<const __nv_bfloat16*>(q),
+                               static_cast<__nv_bfloat16*>(out), static_cast<float*>(scratch),
+                               static_cast<size_t>(scratch_bytes), s);
+  return e == cudaSuccess ? FASER_OK : FASER_ECUDA;
 }

@@ -29,6 +29,10 @@ namespace faser {
 namespace {
 
 constexpr float kNegBig = -1e30f;
+constexpr int kMaxPagesPerCta = 256;
+// pipeline depth (pages of K+V in flight): latency-bound decode wants many pages in flight
+template <int HD>
+constexpr int kAttnStages = 3;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
                                                    __nv_bfloat16* __restrict__ obuf, float* __restrict__ part_o,
                                                    float2* __restrict__ part_ml, int* __restrict__ counters,
                                                    int n_split, int rows_cap, int n_blocks, float scale_log2) {
-  constexpr int kStages = 3;
+  constexpr int kStages = kAttnStages<HD>;
   constexpr int kChunks = HD / 8;          // 16-byte chunks per K/V row
   constexpr int kTileBytes = 64 * HD * 2;  // one K (or V) page
   constexpr int kKS = HD / 16;             // k-steps over head_dim
@@ -134,8 +138,14 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   float m_lo = kNegBig, m_hi = kNegBig, l_lo = 0.f, l_hi = 0.f;
 
   const __nv_bfloat16* kvl = kv.pool + layer * kv.layer_stride;
+  // page ids of this CTA's key range, fetched once (a global load per page would sit on the
+  // critical path of every pipeline step)
+  __shared__ int s_page[kMaxPagesPerCta];
+  for (int i = threadIdx.x; i < t1 - t0 && i < kMaxPagesPerCta; i += 128)
+    s_page[i] = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t0 + i];
+  __syncthreads();
   auto load_tile = [&](int t, int buf) {
-    const int page = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t];
+    const int page = t - t0 < kMaxPagesPerCta ? s_page[t - t0] : kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t];
     const uint8_t* gk = reinterpret_cast<const uint8_t*>(kvl + (static_cast<int64_t>(page) * n_kv + kvh) * 2 * 64 * HD);
     const uint8_t* gv = gk + kTileBytes;
     uint8_t* sk = smem + buf * 2 * kTileBytes;
@@ -355,7 +365,7 @@ cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int
                    float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s) {
   constexpr int kTile = 64 * HD * 2;
   constexpr int kMerge = (4 * 16 * HD + 128) * 4;
-  constexpr int kSmem = 6 * kTile > kMerge ? 6 * kTile : kMerge;  // 3 stages x (K + V)
+  constexpr int kSmem = 2 * kAttnStages<HD> * kTile > kMerge ? 2 * kAttnStages<HD> * kTile : kMerge;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_kernel<HD, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
