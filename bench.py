@@ -375,8 +375,14 @@ def kernel_roofline(kstats):
         return None, table
     top = max(table, key=lambda n: table[n]["total_ms"])
     t = table[top]
+    traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f)["classes"][top]["traffic_bytes_per_launch"]
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": t["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": t["achieved_GBs"] / pk["hbm_gbs"], "traffic": None, "peak_source": src,
+            "frac": t["achieved_GBs"] / pk["hbm_gbs"], "traffic": traffic, "peak_source": src,
             "kernel": top, "avg_launch_us": t["avg_us"], "bytes_per_launch": t["bytes_per_launch"],
             "share_of_timed_kernels": t["total_ms"] / sum(x["total_ms"] for x in table.values())}
     return roof, table
