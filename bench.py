@@ -168,14 +168,33 @@ def make_engine(desc, args, local_rank):
 
 
 def gate_plan(desc, args):
-    if args.mode != "ee":
+    """Fixed gate (--gate-layer l: gate exactly layer l) or None = per-step make_gate_plan
+    (exitctl.cpp:70-82) on the B200-fitted latency models."""
+    if args.mode != "ee" or not args.gate_layer:
         return None
+    return abi.GatePlan(args.gate_layer, args.gate_layer + 1, 1.0)
+
+
+def step_plan_hook(desc, args, models):
+    """Per-step controller decisions that need the batch: the early-exit gate (make_gate_plan,
+    r pinned at 0.5 as should_prune requires r in (0,1)) and the overlap plan (plan_overlap)."""
+    from paper_2604_20503_b200 import engine
     L = desc.target.layers
-    lo = args.gate_layer if args.gate_layer else L // 2
-    return abi.GatePlan(lo, lo + 1, 1.0)
+
+    def hook(eng, live, ks):
+        if args.mode == "ee" and not args.gate_layer:
+            eng.set_gate(engine.make_gate_plan(abi.ExitPolicy.default(), [(k, 0.6) for k in ks],
+                                               float(len(ks)), 0.5, L, models))
+        if args.mode in ("ov", "full"):
+            if args.chunk:
+                eng.set_overlap(True, args.chunk)
+            else:
+                p = engine.plan_overlap(max(ks), len(ks), models=models)
+                eng.set_overlap(bool(p.enabled), max(p.chunk, 1), p.r)
+    return hook
 
 
-def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=None, chunk=0):
+def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=None, chunk=0, hook=None):
     """n_steps serving iterations; per-request first/last commit times on `clock`. With a
     drafter (AdaptiveDrafter) the per-request k_i come from assign_lengths before each step and
     the round is fed back with observe_round after it (the reference loop)."""
@@ -186,12 +205,14 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
         live = eng.live_requests()
         if not live:
             break
+        ks = None
         if drafter is not None:
-            eng.set_spec_lengths(live, drafter.assign_lengths(live, len(live), 1.0))
+            ks = drafter.assign_lengths(live, len(live), 1.0)
+            eng.set_spec_lengths(live, ks)
         if gate is not None:
             eng.set_gate(gate)
-        if chunk:
-            eng.set_overlap(True, chunk)
+        if hook is not None:
+            hook(eng, live, ks or [eng.cfg.default_spec_length] * len(live))
         res = eng.step()
         for r in res:
             state["acc"] = state.get("acc", 0) + r.outcome.accepted_count
@@ -223,13 +244,15 @@ def llama_ours(args, rank, world, local_rank):
     base = shard_base(rank, n_req)  # request-sharded replicas: each rank owns its own requests
     prompts, outl = prompts_for(base, n_req, V, IN_RANGE, OUT_RANGE)
     gate = gate_plan(desc, args)
-    chunk = args.chunk if args.mode in ("ov", "full") else 0
+    from paper_2604_20503_b200 import llama as _llama
+    models = _llama.fitted_latency_model()  # B200 stage latencies (profiles/r01_latency_model.json)
+    hook = step_plan_hook(desc, args, models)
 
     def new_drafter():
         if args.mode in ("vsd", "ov"):
             return None
         from paper_2604_20503_b200 import controller
-        return controller.AdaptiveDrafter()
+        return controller.AdaptiveDrafter(models=models)
 
     def sync_all():
         torch.cuda.synchronize()
@@ -248,7 +271,7 @@ def llama_ours(args, rank, world, local_rank):
         return dev_clock[0]
 
     drafter = new_drafter()
-    run_llama_steps(eng, args.warmup, clock, st, gate=gate, drafter=drafter, chunk=chunk)
+    run_llama_steps(eng, args.warmup, clock, st, gate=gate, drafter=drafter, hook=hook)
     stream = torch.cuda.ExternalStream(eng.stream_ptr())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st = {"first": {}, "last": {}}
@@ -269,7 +292,7 @@ def llama_ours(args, rank, world, local_rank):
     with Clocks(local_rank) as clk:
         ev0.record(stream)
         t0 = time.perf_counter()
-        tokens = run_llama_steps(eng, args.steps, clock_acc, st, gate=gate, drafter=drafter, chunk=chunk)
+        tokens = run_llama_steps(eng, args.steps, clock_acc, st, gate=gate, drafter=drafter, hook=hook)
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -281,7 +304,7 @@ def llama_ours(args, rank, world, local_rank):
     # perturb the programmatic-dependent-launch overlap being measured)
     eng.set_kernel_timing(True)
     run_llama_steps(eng, max(args.steps // 2, 3), clock, {"first": {}, "last": {}}, gate=gate,
-                    drafter=drafter, chunk=chunk)
+                    drafter=drafter, hook=hook)
     kstats = eng.kernel_stats()
     eng.set_kernel_timing(False)
     eng.close()
@@ -302,7 +325,7 @@ def llama_ours(args, rank, world, local_rank):
 
     st2 = {"first": {}, "last": {}}
     drafter2 = new_drafter()
-    run_llama_steps(eng, args.warmup, time.perf_counter, st2, feeder, gate=gate, drafter=drafter2, chunk=chunk)
+    run_llama_steps(eng, args.warmup, time.perf_counter, st2, feeder, gate=gate, drafter=drafter2, hook=hook)
 
     def feeder_counting():
         a, b = eng.last_step_bytes()
@@ -315,7 +338,7 @@ def llama_ours(args, rank, world, local_rank):
     st2 = {"first": {}, "last": {}}
     t0 = time.perf_counter()
     tokens2 = run_llama_steps(eng, args.steps, time.perf_counter, st2, feeder_counting, gate=gate,
-                              drafter=drafter2, chunk=chunk)
+                              drafter=drafter2, hook=hook)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     e2e_tpot = p50_tpot_ms(st2["first"], st2["last"])
@@ -541,7 +564,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--mode", default="vsd", choices=["vsd", "ad", "ee", "ov", "full"])
-    ap.add_argument("--chunk", type=int, default=2)
+    ap.add_argument("--chunk", type=int, default=0, help="overlap chunk (0: plan_overlap decides)")
     ap.add_argument("--gate-layer", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

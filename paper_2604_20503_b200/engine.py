@@ -184,6 +184,15 @@ def make_gate_plan(policy, entries, b, r, num_layers, models=None):
     return g
 
 
+def plan_overlap(s, b, r_grid=(0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9), models=None):
+    """plan_overlap (overlap.cpp:23-42): chunk / SM share that beats the serial estimate, if any."""
+    rg = np.ascontiguousarray(r_grid, np.float64)
+    out = abi.OverlapPlan()
+    _check(lib().faser_plan_overlap(int(s), int(b), C.byref(models) if models else None, _ptr(rg), len(rg),
+                                    C.byref(out)))
+    return out
+
+
 class ServingEngine:
     """Stateful GPU engine: submit() requests, step() one draft->verify->commit round."""
 

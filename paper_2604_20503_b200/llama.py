@@ -60,3 +60,21 @@ def tiny(target_bigram=None, draft_bigram=None, vocab=512, hard=None):
 
 
 PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4}
+
+
+def fitted_latency_model(path=None):
+    """abi.LatencyModel from the B200 stage-latency fit (tools/profile_latency.py ->
+    profiles/r01_latency_model.json); None when the file is absent."""
+    import json
+    import os
+    path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "profiles", "r01_latency_model.json")
+    if not os.path.exists(path):
+        return None
+    m = json.load(open(path))["model"]
+    out = abi.LatencyModel()
+    for name in ("draft", "target", "ee_check", "prune"):
+        p = getattr(out, name)
+        for k, v in m[name].items():
+            setattr(p, k, int(v) if k == "stage" else float(v))
+    return out
