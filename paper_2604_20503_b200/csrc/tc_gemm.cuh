@@ -18,6 +18,7 @@ struct GemmOperand {
 
 cudaError_t make_weight_operand(GemmOperand* op, const void* w, int n_out, int k);  // box 128 rows
 cudaError_t make_act_operand(GemmOperand* op, const void* x, int rows_cap, int k);  // box 32 rows
+cudaError_t make_operand(GemmOperand* op, const void* base, int rows, int k, int box_rows);
 
 enum EpiMode : int {
   kEpiStore = 0,   // out[t][n] = acc * rs[t]                        (fp32)
