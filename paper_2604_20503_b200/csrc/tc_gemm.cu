@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(128, 1)
   float* s_rs = reinterpret_cast<float*>(aux + 256);  // [256] per-token RMSNorm scale
   float* s_red = s_rs + 256;                          // [4][BN] per-warp partials
   int* s_i0 = reinterpret_cast<int*>(s_red + 4 * 256);  // [4][BN] per-warp argmax ids
+  int* s_pos = s_i0 + 4 * 256;  // [256] per-token position (QKV epilogue)
+  int* s_page = s_pos + 256;    // [256] per-token KV page
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kBM;
@@ -167,6 +169,31 @@ __global__ void __launch_bounds__(128, 1)
       sm100::mma_commit(&empty[s]);
     }
     sm100::mma_commit(accum);
+  } else if (warp >= 2) {
+    // Per-token prologue, computed by the two otherwise idle warps while the mainloop streams:
+    // RMSNorm scale of the un-normalised residual input and, for the QKV epilogue, the token's
+    // position and KV page (a dependent load chain that would otherwise sit after the MMAs).
+    const int tn0 = min(BN, T - n0);
+    for (int t = threadIdx.x - 64; t < tn0; t += 64) {
+      float rs = 1.f;
+      if (ea.ss_in) {
+        float part[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < ea.ss_chunks; c += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c + u < ea.ss_chunks) part[u] += ea.ss_in[static_cast<size_t>(c + u) * ea.t_stride + n0 + t];
+        }
+        rs = rsqrtf(((part[0] + part[1]) + (part[2] + part[3])) / ea.d_norm + ea.eps);
+      }
+      s_rs[t] = rs;
+      if (ea.mode == kEpiQkv) {
+        const int row = n0 + t;
+        const int pos = ea.rows.row_pos[row];
+        const int slot = ea.rows.req_slot[ea.rows.row_req[row]];
+        s_pos[t] = pos;
+        s_page[t] = ea.kv.ptab[static_cast<size_t>(slot) * ea.kv.max_pages + pos / kPage];
+      }
+    }
   }
   __syncwarp();
 
@@ -177,12 +204,12 @@ __global__ void __launch_bounds__(128, 1)
   const int r = warp * 32 + lane;          // tile row owned in the TMEM read-out
   float* S = reinterpret_cast<float*>(smem);  // [BN][128] fp32 staging (pipeline smem is free now)
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
+  for (int c0 = 0; c0 < BN; c0 += 32) {
     if (c0 >= tn) break;
-    float v[16];
-    sm100::tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+    float v[32];
+    sm100::tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);  // one wait per 32 columns
 #pragma unroll
-    for (int i = 0; i < 16; ++i) S[(c0 + i) * kBM + r] = v[i];
+    for (int i = 0; i < 32; ++i) S[(c0 + i) * kBM + r] = v[i];
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -219,28 +246,7 @@ __global__ void __launch_bounds__(128, 1)
     }
     __syncthreads();
   }
-  // Per-token prologue (one thread per token of the slice): RMSNorm scale of the un-normalised
-  // residual input, and for the QKV epilogue the token's position and KV page.
-  int* s_pos = s_i0 + 4 * 256;  // [256]
-  int* s_page = s_pos + 256;    // [256]
-  for (int t = ts + threadIdx.x; t < te; t += 128) {
-    float rs = 1.f;
-    if (ea.ss_in) {
-      float ss = 0.f;
-#pragma unroll 4
-      for (int c = 0; c < ea.ss_chunks; ++c) ss += ea.ss_in[static_cast<size_t>(c) * ea.t_stride + n0 + t];
-      rs = rsqrtf(ss / ea.d_norm + ea.eps);
-    }
-    s_rs[t] = rs;
-    if (ea.mode == kEpiQkv) {
-      const int row = n0 + t;
-      const int pos = ea.rows.row_pos[row];
-      const int slot = ea.rows.req_slot[ea.rows.row_req[row]];
-      s_pos[t] = pos;
-      s_page[t] = ea.kv.ptab[static_cast<size_t>(slot) * ea.kv.max_pages + pos / kPage];
-    }
-  }
-  __syncthreads();
+  __syncthreads();  // (the per-token prologue was written by warps 2-3 during the mainloop)
 
   // Token-per-warp passes: lane owns 4 consecutive tile rows (float4), a warp covers the 128
   // rows of one token, 4 tokens per pass.
