@@ -356,6 +356,17 @@ faser_status faser_drafter_objective(double t_hat_ms, int32_t s, double a_hat, d
 /* Deterministic workload inputs (workload.cpp:116-122): synth_prompt. */
 faser_status faser_synth_prompt(uint64_t seed, int32_t index, int32_t len, int32_t vocab,
                                 int32_t* out);
+/* Poisson arrivals over piecewise-constant rate segments (workload.cpp:73-98, synth_workload):
+ * substreams "arrv" (exponential gaps) and "lens" (input then output length per record,
+ * next_int modulo rule, rng.hpp:61-70). Writes min(n, cap) records, *n = total count. */
+faser_status faser_synth_workload(const double* seg_duration_ms, const double* seg_rate_per_s,
+                                  int32_t n_seg, int32_t in_lo, int32_t in_hi, int32_t out_lo,
+                                  int32_t out_hi, uint64_t seed, double* arrival_ms,
+                                  int32_t* in_len, int32_t* out_len, int32_t cap, int32_t* n);
+/* Bursty sinusoidal rate profile (workload.cpp:100-114, sine_segments): `steps` segments of
+ * duration_ms/steps at mean*(1 + a*sin(2*pi*(i+0.5)/steps)), a = (ptv-1)/(ptv+1). */
+faser_status faser_sine_segments(double mean_rate_per_s, double peak_to_valley, double duration_ms,
+                                 int32_t steps, double* seg_duration_ms, double* seg_rate_per_s);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,8 @@
 //   predict_pipeline_ms, plan_overlap
 //                             overlap.cpp:9-42
 //   synth_prompt              workload.cpp:116-122 (+ rng.hpp:41-79)
+//   synth_workload, sine_segments
+//                             workload.cpp:73-114 (+ SplitMixStream::next_exp, rng.hpp:55-59)
 // All double arithmetic is written in the reference's evaluation order; this TU is built
 // without FMA contraction (-ffp-contract=off) so results are bit-identical to the x86-64
 // reference build (tests/test_controllers.py checks against oracle/_ref).
@@ -189,6 +191,68 @@ faser_status faser_synth_prompt(uint64_t seed, int32_t index, int32_t len, int32
   for (int i = 0; i < n; ++i) {
     state += kGamma;
     out[i] = static_cast<int32_t>(mix64(state) % span);
+  }
+  return FASER_OK;
+}
+
+faser_status faser_synth_workload(const double* seg_duration_ms, const double* seg_rate_per_s,
+                                  int32_t n_seg, int32_t in_lo, int32_t in_hi, int32_t out_lo,
+                                  int32_t out_hi, uint64_t seed, double* arrival_ms,
+                                  int32_t* in_len, int32_t* out_len, int32_t cap, int32_t* n) {
+  if (!n || n_seg < 0 || (n_seg > 0 && (!seg_duration_ms || !seg_rate_per_s)) || cap < 0 ||
+      (cap > 0 && (!arrival_ms || !in_len || !out_len)) || in_hi < in_lo || out_hi < out_lo)
+    return FASER_EINVAL;
+  // two counter streams (SplitMixStream: state = mix64(seed); draw = mix64(state += gamma))
+  uint64_t arrv = mix64(substream(seed, 0x61727276ull));  // "arrv"
+  uint64_t lens = mix64(substream(seed, 0x6c656e73ull));  // "lens"
+  auto next_u64 = [](uint64_t& st) {
+    st += kGamma;
+    return mix64(st);
+  };
+  auto next_exp = [&](double rate) {
+    double u = static_cast<double>(next_u64(arrv) >> 11) * 0x1.0p-53;
+    if (u <= 0.0) u = 0x1.0p-53;
+    return -std::log(u) / rate;
+  };
+  auto next_int = [&](int lo, int hi) {
+    const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
+    return lo + static_cast<int>(next_u64(lens) % span);
+  };
+  int32_t count = 0;
+  double seg_start = 0.0;
+  for (int i = 0; i < n_seg; ++i) {
+    if (seg_duration_ms[i] < 0) return FASER_EINVAL;  // std::invalid_argument in the reference
+    const double seg_end = seg_start + seg_duration_ms[i];
+    if (seg_rate_per_s[i] > 0.0) {
+      const double rate_per_ms = seg_rate_per_s[i] / 1000.0;
+      double t = seg_start + next_exp(rate_per_ms);
+      while (t < seg_end) {
+        const int a = next_int(in_lo, in_hi);
+        const int b = next_int(out_lo, out_hi);
+        if (count < cap) {
+          arrival_ms[count] = t;
+          in_len[count] = a;
+          out_len[count] = b;
+        }
+        ++count;
+        t += next_exp(rate_per_ms);
+      }
+    }
+    seg_start = seg_end;
+  }
+  *n = count;
+  return FASER_OK;
+}
+
+faser_status faser_sine_segments(double mean_rate_per_s, double peak_to_valley, double duration_ms,
+                                 int32_t steps, double* seg_duration_ms, double* seg_rate_per_s) {
+  if (steps < 1 || !(mean_rate_per_s > 0) || !(peak_to_valley >= 1) || !seg_duration_ms || !seg_rate_per_s)
+    return FASER_EINVAL;
+  const double a = (peak_to_valley - 1.0) / (peak_to_valley + 1.0);
+  for (int i = 0; i < steps; ++i) {
+    const double phase = 2.0 * 3.14159265358979323846 * (i + 0.5) / steps;
+    seg_duration_ms[i] = duration_ms / steps;
+    seg_rate_per_s[i] = mean_rate_per_s * (1.0 + a * std::sin(phase));
   }
   return FASER_OK;
 }

@@ -156,6 +156,13 @@ class SpeculativeEngine:
         return self._verify(contexts, drafted, committed_len, exempt, policy, gate)
 
 
+def synth_prompt(seed, index, length, vocab):
+    """synth_prompt (workload.cpp:116-122): seeded prompt tokens in [0, vocab-2] (never EOS)."""
+    buf = np.zeros(max(int(length), 1), np.int32)
+    _check(lib().faser_synth_prompt(C.c_uint64(seed), int(index), int(length), int(vocab), _ptr(buf)))
+    return buf.tolist()
+
+
 def default_engine_cfg(**kw):
     cfg = abi.EngineCfg(device=0, max_batch=256, max_seq_len=4096, mode=abi.MODE_VSD,
                         default_spec_length=4, exempt_rule=1,

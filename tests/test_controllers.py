@@ -94,3 +94,45 @@ def test_synth_prompt_matches_oracle():
             out = np.zeros(max(ln, 1), np.int32)
             assert L.faser_synth_prompt(C.c_uint64(1), idx, ln, 64, out.ctypes.data_as(C.c_void_p)) == 0
             assert out.tolist() == P.synth_prompt(1, idx, ln, 64)
+
+
+def _segments(L, fn_prefix, mean, ptv, dur, steps):
+    import numpy as np
+    d, r = np.zeros(steps), np.zeros(steps)
+    rc = getattr(L, fn_prefix + "sine_segments")(C.c_double(mean), C.c_double(ptv), C.c_double(dur), steps,
+                                                  d.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p))
+    assert rc == 0
+    return d, r
+
+
+@needs_ref
+@pytest.mark.parametrize("mean,ptv,dur,steps,seed", [(26.0, 10.0, 60000.0, 12, 1), (5.0, 1.0, 2000.0, 1, 7),
+                                                      (100.0, 3.0, 3000.0, 7, 123)])
+def test_sine_segments_and_synth_workload_match_reference(mean, ptv, dur, steps, seed):
+    """Bursty config-4 arrivals (workload.cpp:73-114) bit-exact against the reference TUs."""
+    import numpy as np
+    L = engine.lib()
+    R = po.ref().lib
+    d, r = _segments(L, "faser_", mean, ptv, dur, steps)
+    d2, r2 = _segments(R, "specref_", mean, ptv, dur, steps)
+    assert d.tobytes() == d2.tobytes() and r.tobytes() == r2.tobytes()
+    cap = 20000
+    outs = []
+    for lib, pre in ((L, "faser_"), (R, "specref_")):
+        a, i, o, n = np.zeros(cap), np.zeros(cap, np.int32), np.zeros(cap, np.int32), C.c_int32()
+        rc = getattr(lib, pre + "synth_workload")(
+            d.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p), steps, 128, 1024, 64, 256,
+            C.c_uint64(seed), a.ctypes.data_as(C.c_void_p), i.ctypes.data_as(C.c_void_p),
+            o.ctypes.data_as(C.c_void_p), cap, C.byref(n))
+        assert rc == 0
+        outs.append((a[:n.value].tobytes(), i[:n.value].tolist(), o[:n.value].tolist()))
+    assert outs[0] == outs[1] and len(outs[0][1]) > 0
+
+
+def test_synth_workload_rejects_bad_input():
+    import numpy as np
+    L = engine.lib()
+    d, r = np.array([-1.0]), np.array([1.0])
+    n = C.c_int32()
+    assert L.faser_synth_workload(d.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p), 1, 1, 2, 1, 2,
+                                  C.c_uint64(1), None, None, None, 0, C.byref(n)) == abi.EINVAL

@@ -59,3 +59,16 @@ def test_sharded_replicas_and_reduction():
 def test_single_rank_reduction_is_identity():
     stats = torch.tensor([1.5, 2.0, 3.0, 4.0], dtype=torch.float64)
     assert bench.aggregate(stats, None) == [1.5, 2.0, 3.0, 4.0]
+
+
+def test_trace_shards_partition_the_arrivals():
+    """Request-sharded trace replay: rank r replays trace indices r, r+N, ... (disjoint, union =
+    the whole trace, arrival order kept within a shard)."""
+    import bench
+    trace = [(float(i), 10 + i % 5, 4) for i in range(37)]
+    for world in (1, 2, 4, 8):
+        shards = [bench.shard_trace(trace, r, world) for r in range(world)]
+        seen = sorted(j for s in shards for j, _ in s)
+        assert seen == list(range(len(trace)))
+        for s in shards:
+            assert [rec[0] for _, rec in s] == sorted(rec[0] for _, rec in s)

@@ -1,0 +1,39 @@
+"""GPU tier: arrival-trace replay (the missing serving loop) over the Llama
+path — bursty sine_segments arrivals (workload.cpp:73-114), iteration-boundary admission,
+every request completes and every output is the target's greedy decode (lossless)."""
+import numpy as np
+import pytest
+
+from oracle import lmoracle
+from paper_2604_20503_b200 import abi, engine, llama, serving
+
+pytestmark = pytest.mark.gpu
+LOGIT_TOL = 2e-2  # bf16 vs the fp32 oracle, relative to the row's logit range (BASELINE north star)
+
+
+def test_bursty_trace_replay_lossless():
+    desc = llama.tiny()
+    V = desc.target.vocab
+    trace = serving.synth_trace(mean_rate_per_s=400.0, peak_to_valley=10.0, duration_ms=60.0, steps=6,
+                                in_range=(4, 24), out_range=(4, 20), seed=3)
+    assert 5 <= len(trace) <= 60
+    assert all(trace[i][0] <= trace[i + 1][0] for i in range(len(trace) - 1))
+    with engine.ServingEngine(desc=desc, max_batch=6, max_seq_len=64, mode=abi.MODE_VSD,
+                              default_spec_length=4, max_spec_length=8, prefill_rows=512) as eng:
+        m = serving.run_trace(eng, trace, V, prompt_seed=1, fixed_k=4)
+        outs = [eng.committed(j) for j in range(len(trace))]
+    assert m["requests"] == len(trace) and m["completed"] == len(trace)
+    assert m["tokens"] == sum(len(o) for o in outs)
+    assert m["throughput_tok_s"] > 0 and m["p50_tpot_ms"] > 0 and m["p99_latency_ms"] >= m["p50_latency_ms"]
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b, threads=2)
+    try:
+        for j in range(0, len(trace), max(1, len(trace) // 6)):
+            prompt = engine.synth_prompt(1, j, trace[j][1], V)
+            ref = tgt.greedy(prompt, trace[j][2], V - 1)
+            if outs[j] != ref:  # only a near-tie of the fp32 oracle may explain a bf16 divergence
+                q = next(q for q in range(min(len(outs[j]), len(ref))) if outs[j][q] != ref[q])
+                z = tgt.logits(prompt + ref[:q + 1], len(prompt) + q - 1)[0][0]
+                s = np.sort(z)
+                assert (s[-1] - s[-2]) / (s[-1] - s[0]) <= LOGIT_TOL, (j, q)
+    finally:
+        tgt.close()
