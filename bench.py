@@ -217,13 +217,76 @@ def llama_desc(name):
     return llama.PRESETS[name]()
 
 
-def make_engine(desc, args, local_rank):
+def make_engine(desc, args, local_rank, **tp):
     from paper_2604_20503_b200 import engine
     mode = {"vsd": abi.MODE_VSD, "ad": abi.MODE_VSD_AD, "ee": abi.MODE_VSD_AD_EE,
             "ov": abi.MODE_FULL, "full": abi.MODE_FULL}[args.mode]
     return engine.ServingEngine(desc=desc, max_batch=args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
                                 mode=mode, default_spec_length=args.k, max_spec_length=16,
-                                prefill_rows=8192, device=local_rank)
+                                prefill_rows=8192, device=local_rank, **tp)
+
+
+def tp_bootstrap(dist, rank, make_uid):
+    """NCCL TP group bootstrap: rank 0 makes the 128-byte ncclUniqueId, every rank receives it
+    through the launcher's process group (torch.distributed is plumbing only)."""
+    obj = [make_uid() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def llama_tp(args, rank, world, local_rank):
+    """Config 5 (BASELINE.json configs[4]): TP=world verification of the 70B-shaped target, one
+    process per GPU, NCCL all-reduce after O / down and all-gathered vocab-parallel argmax. All
+    ranks serve the SAME requests (tensor parallel, not request-sharded); tokens are counted once,
+    time = max over ranks of the device time."""
+    import torch
+    torch.cuda.set_device(local_rank)
+    import torch.distributed as dist
+    dist.init_process_group("nccl" if world > 1 else "gloo", init_method=None if world > 1 else "tcp://127.0.0.1:29533",
+                            rank=rank, world_size=world)
+    from paper_2604_20503_b200 import engine
+    uid = tp_bootstrap(dist, rank, engine.TpGroup.nccl_unique_id)
+    group = engine.TpGroup.nccl(uid, world, rank, local_rank)
+    desc = llama_desc(args.workload)
+    V = desc.target.vocab
+    B = args.batch
+    n_req = B * (args.steps + args.warmup) // 40 + 2 * B
+    prompts, outl = prompts_for(0, n_req, V, IN_RANGE, OUT_RANGE)
+    eng = make_engine(desc, args, local_rank, tp_size=world, tp_rank=rank, tp_group=group)
+    for i, (p, m) in enumerate(zip(prompts, outl)):
+        eng.submit(i, p, m)
+    for _ in range(args.warmup):
+        eng.step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms, tokens, first, last, clock = 0.0, 0, {}, {}, 0.0
+    for _ in range(args.steps):
+        res = eng.step()
+        dt = eng.last_step_timing()[2]
+        dev_ms += dt
+        clock += dt
+        for r in res:
+            tokens += r.committed
+            if r.committed:
+                first.setdefault(r.req_id, clock)
+                last[r.req_id] = clock
+    torch.cuda.synchronize()
+    t = torch.tensor([dev_ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tp50 = sorted((last[i] - first[i]) / max(1, len(eng.committed(i)) - 1) for i in first if len(eng.committed(i)) > 1)
+    if rank == 0:
+        ms = float(t[0])
+        print(json.dumps({
+            "metric": METRIC, "value": tokens / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic prompts (synth_prompt), random-init weights",
+            "p50_tpot_ms": tp50[len(tp50) // 2] if tp50 else 0.0,
+            "config": {"workload": f"{args.workload}: TP={world} verification (NCCL all-reduce after O/down, "
+                       f"vocab-parallel argmax), replicated draft, B={B}, k={args.k}", "global_batch": B,
+                       "parallelism": f"tp{world}"}}), flush=True)
+    eng.close()
+    group.close()
+    dist.destroy_process_group()
 
 
 def gate_plan(desc, args):
@@ -619,7 +682,8 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "tiny", "toy"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "tiny", "tp_tiny", "toy"])
+    ap.add_argument("--tp", action="store_true", help="tensor-parallel verification over the launched ranks")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--mode", default="vsd", choices=["vsd", "ad", "ee", "ov", "full"])
@@ -641,6 +705,8 @@ def main():
         llama_reference(args, rank, world)
     elif args.trace > 0:
         llama_trace(args, rank, world, local_rank)
+    elif args.tp or args.workload == "cfg5":
+        llama_tp(args, rank, world, local_rank)
     else:
         llama_ours(args, rank, world, local_rank)
 

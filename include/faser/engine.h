@@ -200,6 +200,13 @@ typedef struct faser_engine_cfg {
   int32_t prefill_rows;    /* LLAMA: rows per prefill forward chunk; 0 = 8192 */
   int32_t debug_capture;   /* LLAMA: 1 = keep per-stage logits of the last step for validation */
   int32_t reserved1;
+  /* Tensor-parallel verification (config 5): the TARGET is split over tp_size
+   * ranks (column-parallel QKV / gate-up, row-parallel O / down + all-reduce, vocab-parallel LM
+   * head + all-gathered argmax); the draft is replicated. tp_size <= 1: no TP. Modes VSD and
+   * VSD_AD only. Every rank drives its own engine with the same submits and plans. */
+  int32_t tp_size;
+  int32_t tp_rank;
+  struct faser_tp_group* tp_group; /* from faser_tp_*_group_create; not owned by the engine */
 } faser_engine_cfg;
 
 typedef struct faser_step_plan {
@@ -222,6 +229,18 @@ typedef struct faser_round_result {
 } faser_round_result;
 
 typedef struct faser_engine faser_engine;
+
+/* ---- tensor-parallel groups (no reference counterpart: SPEC.md:8 puts TP out of the
+ * simulator's scope; the paper ran TP=2 inside vLLM) */
+typedef struct faser_tp_group faser_tp_group;
+/* NCCL group, one process per GPU: rank 0 makes the 128-byte id, every rank joins with it. */
+faser_status faser_tp_nccl_unique_id(uint8_t* id128);
+faser_status faser_tp_nccl_group_create(const uint8_t* id128, int32_t size, int32_t rank, int32_t device,
+                                        faser_tp_group** out);
+/* In-process group on ONE device: the ranks' engines are driven from `size` host threads
+ * (single-GPU validation backend of the sharded math). */
+faser_status faser_tp_local_group_create(int32_t size, faser_tp_group** out);
+void faser_tp_group_destroy(faser_tp_group* g);
 
 faser_status faser_engine_create(const faser_model_desc* model, const faser_engine_cfg* cfg,
                                  faser_engine** out);

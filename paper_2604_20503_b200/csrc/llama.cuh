@@ -78,11 +78,16 @@ struct KvDev {
 };
 
 // ------------------------------------------------------------------ launchers
+// elements [offset, offset + n) of the tensor (offset: a TP row shard)
 cudaError_t lm_init_matrix(__nv_bfloat16* w, int64_t n, uint64_t seed, uint32_t tag, float std,
-                           cudaStream_t s);
-// wgu in the interleaved order (gate rows tagged kTagGate, up rows kTagUp, both [ffn][d]).
+                           cudaStream_t s, int64_t offset = 0);
+// columns [c0, c0 + kl) of a row-major [rows][k_full] tensor (row-parallel TP shard)
+cudaError_t lm_init_cols(__nv_bfloat16* w, int64_t rows, int64_t k_full, int64_t c0, int64_t kl, uint64_t seed,
+                         uint32_t tag, float std, cudaStream_t s);
+// wgu in the interleaved order (gate rows tagged kTagGate, up rows kTagUp, both [ffn][d]); `ffn`
+// local rows starting at global FFN row f0 (TP column shard).
 cudaError_t lm_init_gate_up(__nv_bfloat16* wgu, int ffn, int d, uint64_t seed, uint32_t tag_layer,
-                            float std, cudaStream_t s);
+                            float std, cudaStream_t s, int64_t f0 = 0);
 // emb[t] = bf16(bigram_scale * lm[g(t)] + noise(t))
 cudaError_t lm_init_embedding(__nv_bfloat16* emb, const __nv_bfloat16* lm, const LlamaShape& m,
                               uint32_t ga, uint32_t gb, cudaStream_t s);

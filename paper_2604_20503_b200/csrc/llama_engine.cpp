@@ -32,6 +32,7 @@
 #include "llama_engine.cuh"
 #include "llama_step.cuh"
 #include "mega.cuh"
+#include "tp.cuh"
 #include "tc_gemm.cuh"
 
 namespace faser {
@@ -113,18 +114,40 @@ struct LmModel {
   int64_t kv_layer_stride = 0;
   Mem rope;  // float2 [max_pos][hd/2]
 
-  void build(const LlamaShape& s, uint32_t ga, uint32_t gb, int n_pages, int max_pos, cudaStream_t st) {
+  int tp = 1, rank = 0;
+  // `full` = the model's shape; with tp > 1 this rank holds the Megatron shard of the target:
+  // n_q/tp query heads, n_kv/tp KV heads, ffn/tp FFN rows, vocab/tp LM-head rows (sh = local).
+  void build(const LlamaShape& full, uint32_t ga, uint32_t gb, int n_pages, int max_pos, cudaStream_t st,
+             int tp_ = 1, int rank_ = 0) {
+    tp = tp_;
+    rank = rank_;
+    LlamaShape s = full;
+    s.n_q /= tp;
+    s.n_kv /= tp;
+    s.ffn /= tp;
+    s.vocab /= tp;
     sh = s;
     const int64_t d = s.d, qkv = s.qkv_out(), qd = static_cast<int64_t>(s.n_q) * s.hd, F = s.ffn, V = s.vocab;
+    const int64_t Vf = full.vocab, hd = s.hd;
     const int64_t per_layer = qkv * d + d * qd + 2 * F * d + d * F;
-    const int64_t total = 2 * V * d + per_layer * s.layers;
+    const int64_t total = V * d + Vf * d + per_layer * s.layers;
     arena.alloc(total * 2);
     __nv_bfloat16* p = arena.as<__nv_bfloat16>();
     lm = p;
     emb = p + V * d;
-    p += 2 * V * d;
-    LCK(lm_init_matrix(lm, V * d, s.seed, kTagLm * 4096u, s.init_std, st));
-    LCK(lm_init_embedding(emb, lm, s, ga, gb, st));
+    p += V * d + Vf * d;
+    if (tp == 1) {
+      LCK(lm_init_matrix(lm, V * d, s.seed, kTagLm * 4096u, s.init_std, st));
+      LCK(lm_init_embedding(emb, lm, full, ga, gb, st));
+    } else {  // the embedding needs the whole LM head (bigram construction); keep this rank's rows
+      Mem full_lm;
+      full_lm.alloc(static_cast<size_t>(Vf) * d * 2);
+      LCK(lm_init_matrix(full_lm.as<__nv_bfloat16>(), Vf * d, s.seed, kTagLm * 4096u, s.init_std, st));
+      LCK(lm_init_embedding(emb, full_lm.as<__nv_bfloat16>(), full, ga, gb, st));
+      LCK(cudaMemcpyAsync(lm, full_lm.as<__nv_bfloat16>() + rank * V * d, V * d * 2, cudaMemcpyDeviceToDevice, st));
+      LCK(cudaStreamSynchronize(st));
+    }
+    const int64_t nqf = full.n_q, nkvf = full.n_kv;
     for (int l = 0; l < s.layers; ++l) {
       LayerW w;
       __nv_bfloat16* wqkv = p;
@@ -135,10 +158,17 @@ struct LmModel {
       p += 2 * F * d;
       __nv_bfloat16* wd = p;
       p += d * F;
-      LCK(lm_init_matrix(wqkv, qkv * d, s.seed, kTagQkv * 4096u + l, s.init_std, st));
-      LCK(lm_init_matrix(wo, d * qd, s.seed, kTagO * 4096u + l, s.init_std, st));
-      LCK(lm_init_gate_up(wgu, s.ffn, s.d, s.seed, l, s.init_std, st));
-      LCK(lm_init_matrix(wd, d * F, s.seed, kTagDown * 4096u + l, s.init_std, st));
+      const uint32_t tq = kTagQkv * 4096u + l;
+      // column-parallel QKV: this rank's q rows, then its k rows, then its v rows
+      LCK(lm_init_matrix(wqkv, s.n_q * hd * d, s.seed, tq, s.init_std, st, rank * s.n_q * hd * d));
+      LCK(lm_init_matrix(wqkv + s.n_q * hd * d, s.n_kv * hd * d, s.seed, tq, s.init_std, st,
+                         (nqf * hd + rank * s.n_kv * hd) * d));
+      LCK(lm_init_matrix(wqkv + (s.n_q + s.n_kv) * hd * d, s.n_kv * hd * d, s.seed, tq, s.init_std, st,
+                         (nqf * hd + nkvf * hd + rank * s.n_kv * hd) * d));
+      // row-parallel O and down: this rank's input columns
+      LCK(lm_init_cols(wo, d, nqf * hd, rank * qd, qd, s.seed, kTagO * 4096u + l, s.init_std, st));
+      LCK(lm_init_gate_up(wgu, s.ffn, s.d, s.seed, l, s.init_std, st, static_cast<int64_t>(rank) * F));
+      LCK(lm_init_cols(wd, d, static_cast<int64_t>(full.ffn), rank * F, F, s.seed, kTagDown * 4096u + l, s.init_std, st));
       w.wqkv = wqkv;
       w.wo = wo;
       w.wgu = wgu;
@@ -312,8 +342,11 @@ class LlamaEngine {
   LlamaShape dsh{}, tsh{};
   LmModel draft, target;
   LmWork wd, wt;
-  MegaCtx md, mtg;
+  MegaCtx md, mtg;          // persistent single-launch forwards (draft step / verify), opt-in
   Mem mega_trace;
+  int tp = 1, tp_rank = 0;  // tensor-parallel verification of the target (tp.cuh)
+  TpGroup* tpg = nullptr;
+  Mem tp_part, tp_loc, tp_all;  // row-parallel partial [rows][d] fp32; argmax partials (float2)
   void dump_mega_trace(int layers, int G) {
     LCK(cudaStreamSynchronize(fs));
     const int P = mega_phases(layers);
@@ -464,14 +497,34 @@ class LlamaEngine {
     const int prefill_rows = cfg.prefill_rows > 0 ? cfg.prefill_rows : 8192;
     const int verify_rows = B * max_spec;
     const int cap = std::max({prefill_rows, verify_rows, cfg.max_seq_len});
+    tp = cfg.tp_size > 1 ? cfg.tp_size : 1;
+    tp_rank = tp > 1 ? cfg.tp_rank : 0;
+    if (tp > 1) {
+      tpg = tp_group_of(cfg.tp_group);
+      if (!tpg || tpg->size != tp) throw LFail{FASER_EINVAL, "tp_group missing or of a different size"};
+      if (tp_rank < 0 || tp_rank >= tp) throw LFail{FASER_EINVAL, "tp_rank out of range"};
+      if (cfg.mode != FASER_MODE_VSD && cfg.mode != FASER_MODE_VSD_AD)
+        throw LFail{FASER_EINVAL, "tensor-parallel verification supports modes VSD and VSD_AD"};
+      if (cfg.debug_capture) throw LFail{FASER_EINVAL, "debug_capture is not available with tp_size > 1"};
+      const faser_llama_shape& t = m->target;
+      if (t.n_heads % tp || t.n_kv_heads % tp || t.ffn % (64 * tp) || t.vocab % (128 * tp) ||
+          ((t.n_heads + 2 * t.n_kv_heads) / tp * t.head_dim) % 128 || (t.n_heads / tp * t.head_dim) % 128)
+        throw LFail{FASER_EINVAL, "target shape does not split over tp_size ranks"};
+    }
     draft.build(dsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream);
-    target.build(tsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream);
+    target.build(tsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream, tp, tp_rank);
     wd.build(dsh, cap, B);
-    wt.build(tsh, cap, verify_rows);
+    wt.build(target.sh, cap, verify_rows);
+    if (tp > 1) {
+      tp_part.alloc(static_cast<size_t>(cap) * tsh.d * 4);
+      tp_loc.alloc(static_cast<size_t>(cap) * 8);
+      tp_all.alloc(static_cast<size_t>(cap) * 8 * tp);
+    }
     LCK(cudaDeviceSynchronize());
     // persistent single-launch forward: opt-in (FASER_MEGA=1) until it beats the per-layer
     // launches (its split-K partial exchange is latency-bound at T ~ 128)
     mega_on = getenv("FASER_MEGA") && getenv("FASER_MEGA")[0] == '1';
+    if (tp > 1) mega_on = false;
     if (mega_on) {
       md.build(draft, wd, nsm, stream);
       mtg.build(target, wt, nsm, stream);
@@ -657,7 +710,12 @@ class LlamaEngine {
     e_glu.ss_in = w.ss.as<float>();
     e_glu.h = w.h.as<__nv_bfloat16>();
     e_glu.ffn = s.ffn;
+    const bool is_tp_target = tp > 1 && &m == &target;
+    EpiArgs e_part = base;  // row-parallel TP partial (fp32 [T][d], summed over ranks afterwards)
+    e_part.mode = kEpiStore;
+    e_part.out = tp_part.as<float>();
     EpiArgs e_lm = base;
+    if (is_tp_target) e_lm.id_off = tp_rank * s.vocab;  // global token ids of this vocab shard
     e_lm.mode = kEpiLogits;
     e_lm.ss_in = w.ss.as<float>();
     e_lm.logits = w.logits.as<float>();
@@ -715,9 +773,22 @@ class LlamaEngine {
         LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
                          w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, fs));
       });
-      timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); });
+      const bool tp_rows = is_tp_target;  // row-parallel: partial sums -> all-reduce -> residual add
+      auto row_parallel = [&](const GemmOperand& wop, const GemmOperand& xop, const GemmPlan& pl) {
+        LCK(gemm_fused(wop, xop, T, pl, e_part, fs));
+        LCK(tpg->allreduce_sum(tp_rank, tp_part.as<float>(), static_cast<size_t>(T) * s.d, fs));
+        LCK(tp_resid_add(tp_part.as<float>(), w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), T, s.d, fs));
+        launches += 2;
+      };
+      if (tp_rows)
+        row_parallel(m.op_o[l], w.op_ob, p_o);
+      else
+        timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); });
       timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); });
-      timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); });
+      if (tp_rows)
+        row_parallel(m.op_d[l], w.op_h, p_d);
+      else
+        timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); });
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
@@ -734,7 +805,14 @@ class LlamaEngine {
     if (f.logits) {
       timed(is_target ? 4 : 2, gbytes(s.vocab, s.d, 2 * s.vocab),
             [&] { LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs)); });
-      LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, fs));
+      if (is_tp_target) {  // vocab-parallel greedy argmax: all-gather (max, lowest global id) per row
+        LCK(tp_local_argmax(s.vocab / 128, T, w.amax.as<float2>(), tp_loc.as<float2>(), fs));
+        LCK(tpg->allgather_f2(tp_rank, tp_loc.as<float2>(), tp_all.as<float2>(), static_cast<size_t>(T), fs));
+        LCK(tp_merge_argmax(tp, T, tp_all.as<float2>(), f.argmax_out, fs));
+        launches += 2;
+      } else {
+        LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, fs));
+      }
       launches += 2;
       if (f.capture) capture_stage(0, m, w, f);
     }

@@ -28,22 +28,33 @@ __host__ __device__ inline uint64_t tensor_base(uint64_t seed, uint32_t tag) {
 
 float scale_for(float std) { return static_cast<float>(static_cast<double>(std) / kIrwinHallStd); }
 
-__global__ void init_matrix_kernel(__nv_bfloat16* w, int64_t n, uint64_t base, float c) {
+__global__ void init_matrix_kernel(__nv_bfloat16* w, int64_t n, uint64_t base, float c, int64_t off) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    w[i] = __float2bfloat16_rn(gen_value(base, i, c));
+    w[i] = __float2bfloat16_rn(gen_value(base, off + i, c));
+}
+
+// Column slice [c0, c0 + kl) of a row-major [rows][k_full] tensor (row-parallel TP shards).
+__global__ void init_cols_kernel(__nv_bfloat16* w, int64_t rows, int64_t k_full, int64_t c0, int64_t kl,
+                                 uint64_t base, float c) {
+  const int64_t n = rows * kl;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / kl, col = i % kl;
+    w[i] = __float2bfloat16_rn(gen_value(base, r * k_full + c0 + col, c));
+  }
 }
 
 // Interleaved gate/up: output row n of wgu = group n/128; within < 64 -> gate row, else up row.
 __global__ void init_gate_up_kernel(__nv_bfloat16* w, int ffn, int d, uint64_t base_g,
-                                    uint64_t base_u, float c) {
+                                    uint64_t base_u, float c, int64_t f0) {
   const int64_t n = 2ll * ffn * d;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t row = i / d, col = i % d;
     const int64_t grp = row / 128, within = row % 128;
     const bool up = within >= 64;
-    const int64_t j = grp * 64 + (up ? within - 64 : within);
+    const int64_t j = f0 + grp * 64 + (up ? within - 64 : within);  // global FFN row (TP shard offset f0)
     w[i] = __float2bfloat16_rn(gen_value(up ? base_u : base_g, j * d + col, c));
   }
 }
@@ -119,16 +130,23 @@ __global__ void argmax_reduce_kernel(int n_tiles, RowsDev rows, int t_stride, co
 }  // namespace
 
 cudaError_t lm_init_matrix(__nv_bfloat16* w, int64_t n, uint64_t seed, uint32_t tag, float std,
-                           cudaStream_t s) {
-  init_matrix_kernel<<<grid_for(n), 256, 0, s>>>(w, n, tensor_base(seed, tag), scale_for(std));
+                           cudaStream_t s, int64_t offset) {
+  init_matrix_kernel<<<grid_for(n), 256, 0, s>>>(w, n, tensor_base(seed, tag), scale_for(std), offset);
+  return cudaGetLastError();
+}
+
+cudaError_t lm_init_cols(__nv_bfloat16* w, int64_t rows, int64_t k_full, int64_t c0, int64_t kl, uint64_t seed,
+                         uint32_t tag, float std, cudaStream_t s) {
+  init_cols_kernel<<<grid_for(rows * kl), 256, 0, s>>>(w, rows, k_full, c0, kl, tensor_base(seed, tag),
+                                                       scale_for(std));
   return cudaGetLastError();
 }
 
 cudaError_t lm_init_gate_up(__nv_bfloat16* wgu, int ffn, int d, uint64_t seed, uint32_t tag_layer,
-                            float std, cudaStream_t s) {
+                            float std, cudaStream_t s, int64_t f0) {
   init_gate_up_kernel<<<grid_for(2ll * ffn * d), 256, 0, s>>>(
       wgu, ffn, d, tensor_base(seed, kTagGate * 4096u + tag_layer),
-      tensor_base(seed, kTagUp * 4096u + tag_layer), scale_for(std));
+      tensor_base(seed, kTagUp * 4096u + tag_layer), scale_for(std), f0);
   return cudaGetLastError();
 }
 

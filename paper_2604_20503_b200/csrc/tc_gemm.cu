@@ -276,10 +276,11 @@ __global__ void __launch_bounds__(128, 1)
         a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
         *reinterpret_cast<float4*>(ea.logits + idx) = a;
         float bv = a.x;
-        int bi = m0 + c4;
-        if (a.y > bv) { bv = a.y; bi = m0 + c4 + 1; }
-        if (a.z > bv) { bv = a.z; bi = m0 + c4 + 2; }
-        if (a.w > bv) { bv = a.w; bi = m0 + c4 + 3; }
+        const int id0 = ea.id_off + m0 + c4;
+        int bi = id0;
+        if (a.y > bv) { bv = a.y; bi = id0 + 1; }
+        if (a.z > bv) { bv = a.z; bi = id0 + 2; }
+        if (a.w > bv) { bv = a.w; bi = id0 + 3; }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
           const float ov = __shfl_xor_sync(0xffffffffu, bv, o);

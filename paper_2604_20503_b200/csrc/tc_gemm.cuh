@@ -50,6 +50,7 @@ struct EpiArgs {
   int ffn = 0;
   float* logits = nullptr;               // kEpiLogits [t][n_out]
   float2* amax = nullptr;                // kEpiLogits [n_out/128][t_stride] (value, idx bits)
+  int id_off = 0;                        // kEpiLogits: id of output row 0 (vocab-parallel shard)
 };
 
 // Launch plan: token-tile width and K split (the splits of a tile form one thread-block cluster

@@ -163,12 +163,47 @@ def synth_prompt(seed, index, length, vocab):
     return buf.tolist()
 
 
+class TpGroup:
+    """Tensor-parallel group handle (faser_tp_group): ``TpGroup.local(n)`` = n in-process ranks on
+    one device (each rank's engine stepped from its own thread), ``TpGroup.nccl(uid, n, rank,
+    device)`` = one process per GPU over NCCL (uid from ``TpGroup.nccl_unique_id()`` on rank 0)."""
+
+    def __init__(self, h, size):
+        self.h, self.size = h, size
+
+    @classmethod
+    def local(cls, size):
+        h = C.c_void_p()
+        _check(lib().faser_tp_local_group_create(int(size), C.byref(h)))
+        return cls(h, size)
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = (C.c_uint8 * 128)()
+        _check(lib().faser_tp_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, uid, size, rank, device):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(lib().faser_tp_nccl_group_create(buf, int(size), int(rank), int(device), C.byref(h)))
+        return cls(h, size)
+
+    def close(self):
+        if self.h:
+            lib().faser_tp_group_destroy(self.h)
+            self.h = None
+
+
 def default_engine_cfg(**kw):
     cfg = abi.EngineCfg(device=0, max_batch=256, max_seq_len=4096, mode=abi.MODE_VSD,
                         default_spec_length=4, exempt_rule=1,
                         exit_policy=abi.ExitPolicy.default(), max_pending=1 << 20,
                         pending_tokens=1 << 24)
     for k, v in kw.items():
+        if k == "tp_group" and isinstance(v, TpGroup):
+            v = v.h
         setattr(cfg, k, v)
     return cfg
 

@@ -59,7 +59,27 @@ def tiny(target_bigram=None, draft_bigram=None, vocab=512, hard=None):
                  shape(256, 4, 4, 2, 64, 512, vocab, seed=32, bigram=tb, hard=hf))
 
 
-PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4}
+def config5(target_bigram=None, draft_bigram=None, hard=None):
+    """Llama-3.2-1B-shaped draft / Llama-3.1-70B-shaped target (d8192, L80, 64q/8kv x 128,
+    FFN 28672), V=128256 (config 5: TP=8 verification, ~17.4 GB of target weights per rank)."""
+    tb = TARGET_BIGRAM["cfg4"] if target_bigram is None else target_bigram
+    db = DRAFT_BIGRAM if draft_bigram is None else draft_bigram
+    hf = TARGET_HARD["cfg4"] if hard is None else hard
+    return _pair(shape(2048, 16, 32, 8, 64, 8192, 128256, seed=21, theta=500000.0, bigram=db),
+                 shape(8192, 80, 64, 8, 128, 28672, 128256, seed=52, theta=500000.0, bigram=tb, hard=hf))
+
+
+def tp_tiny(target_bigram=None, draft_bigram=None, hard=None):
+    """Small pair whose target splits over 1/2/4/8 tensor-parallel ranks (16q/8kv heads, FFN 512,
+    V 1024) for the TP parity tests."""
+    tb = TARGET_BIGRAM["tiny"] if target_bigram is None else target_bigram
+    db = DRAFT_BIGRAM if draft_bigram is None else draft_bigram
+    hf = 0.0 if hard is None else hard
+    return _pair(shape(128, 2, 2, 2, 64, 256, 1024, seed=41, bigram=db),
+                 shape(256, 3, 16, 8, 64, 512, 1024, seed=42, bigram=tb, hard=hf))
+
+
+PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4, "cfg5": config5, "tp_tiny": tp_tiny}
 
 
 def fitted_latency_model(path=None):

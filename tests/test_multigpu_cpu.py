@@ -72,3 +72,26 @@ def test_trace_shards_partition_the_arrivals():
         assert seen == list(range(len(trace)))
         for s in shards:
             assert [rec[0] for _, rec in s] == sorted(rec[0] for _, rec in s)
+
+
+def _tp_boot(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    uid = bench.tp_bootstrap(dist, rank, lambda: bytes(range(128)))
+    q.put((rank, uid))
+    dist.destroy_process_group()
+
+
+def test_tp_bootstrap_broadcasts_the_nccl_id():
+    """Config-5 TP bring-up: every rank receives rank 0's 128-byte ncclUniqueId (gloo, world 2)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_tp_boot, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert got[0] == got[1] == bytes(range(128))

@@ -1,0 +1,87 @@
+"""GPU tier: tensor-parallel verification (config 5's TP=8 path) validated on ONE
+device with the in-process TP group: tp ranks hold Megatron shards of the target (column-
+parallel QKV / gate-up, row-parallel O / down + all-reduce, vocab-parallel LM head + all-gathered
+argmax), each rank's engine is stepped from its own thread. Every rank must emit identical
+round results, and the sharded engine must match the unsharded one (lossless; a divergence is
+only allowed where the fp32 oracle's top-2 gap is inside the bf16 tolerance)."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import lmoracle
+from paper_2604_20503_b200 import abi, engine, llama
+
+pytestmark = pytest.mark.gpu
+LOGIT_TOL = 2e-2
+
+
+def serve(eng, prompts, max_out, ks, out, idx):
+    for i, (p, m) in enumerate(zip(prompts, max_out)):
+        eng.submit(i, p, m)
+    rounds = []
+    s = 0
+    while eng.live_requests():
+        live = eng.live_requests()
+        eng.set_spec_lengths(live, [ks[(r + s) % len(ks)] for r in live])
+        rounds.append([r.as_tuple() for r in eng.step()])
+        s += 1
+    out[idx] = ([eng.committed(i) for i in range(len(prompts))], rounds)
+
+
+def make(desc, **kw):
+    return engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=128, mode=abi.MODE_VSD, default_spec_length=4,
+                                max_spec_length=8, prefill_rows=1024, **kw)
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tensor_parallel_verify_matches_unsharded(tp):
+    desc = llama.tp_tiny()
+    V = desc.target.vocab
+    rng = np.random.default_rng(tp)
+    prompts = [rng.integers(0, V - 1, size=int(rng.integers(3, 40))).tolist() for _ in range(7)]
+    max_out = [int(rng.integers(4, 30)) for _ in range(7)]
+    ks = [1, 2, 3, 4, 6, 8]
+    ref = [None]
+    with make(desc) as e1:
+        serve(e1, prompts, max_out, ks, ref, 0)
+    group = engine.TpGroup.local(tp)
+    engines = [make(desc, tp_size=tp, tp_rank=r, tp_group=group) for r in range(tp)]
+    outs = [None] * tp
+    th = [threading.Thread(target=serve, args=(engines[r], prompts, max_out, ks, outs, r)) for r in range(tp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for e in engines:
+        e.close()
+    group.close()
+    assert all(o is not None for o in outs), "a TP rank failed"
+    for r in range(1, tp):  # ranks agree bit-exactly (same drafted tokens, same all-gathered argmax)
+        assert outs[r] == outs[0]
+    got = outs[0][0]
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b, threads=2)
+    try:
+        for i, (p, m) in enumerate(zip(prompts, max_out)):
+            want = tgt.greedy(p, m, V - 1)
+            for seq in (got[i], ref[0][0][i]):
+                if seq != want:
+                    q = next(q for q in range(min(len(seq), len(want))) if seq[q] != want[q])
+                    z = tgt.logits(p + want[:q + 1], len(p) + q - 1)[0][0]
+                    srt = np.sort(z)
+                    assert (srt[-1] - srt[-2]) / (srt[-1] - srt[0]) <= LOGIT_TOL, (i, q)
+    finally:
+        tgt.close()
+
+
+def test_tensor_parallel_rejects_bad_configs():
+    desc = llama.tp_tiny()
+    g2 = engine.TpGroup.local(2)
+    with pytest.raises(engine.FaserError):  # group size != tp_size
+        make(desc, tp_size=4, tp_rank=0, tp_group=g2)
+    with pytest.raises(engine.FaserError):  # early exit is not available under TP
+        engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=128, mode=abi.MODE_VSD_AD_EE,
+                             default_spec_length=4, tp_size=2, tp_rank=0, tp_group=g2)
+    with pytest.raises(engine.FaserError):  # tiny's target (4q/2kv heads) does not split 4 ways
+        make(llama.tiny(), tp_size=4, tp_rank=0, tp_group=engine.TpGroup.local(4))
+    g2.close()
