@@ -22,10 +22,14 @@ extern "C" {
 faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,
                                int32_t t, int32_t k, int32_t splits, void* stream);
 
-/* Same with an explicit launch plan: bn in {32, 64, 128, 256} rows per tile (0 = auto) and
- * splits in [1, 8] (0 = auto). For plan sweeps / microbenchmarks. */
+/* Same with an explicit launch plan: bn in {32, 64, 128, 256} rows per tile (0 = auto),
+ * + 1000 * depth (1 shallow, 2 deep) + 10000 * mc (weight tiles per CTA sharing a rows tile:
+ * 1, 2, 4), and splits in [1, 8] (0 = auto). For plan sweeps / microbenchmarks. */
 faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, int32_t n_out,
                                     int32_t t, int32_t k, int32_t bn, int32_t splits, void* stream);
+/* The launch plan the engine uses for an [n_out x k] weight and t rows: out = {bn, splits, mc,
+ * deep}. Host-only (no device needed). */
+faser_status faser_k_gemm_plan(int32_t n_out, int32_t t, int32_t k, int32_t* out4);
 
 /* K3: causal attention of n_req ragged query blocks over the paged KV cache (one layer).
  * q bf16 [rows][n_q][hd]; kv bf16 pool [pages][n_kv][2 (K,V)][64][hd]; ptab int32

@@ -37,8 +37,12 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
                                                int32_t t, int32_t k, int32_t bn, int32_t splits,
                                                void* stream) {
   // bn may carry a pipeline-depth request in its upper bits: 1000 + bn = shallow, 2000 + bn = deep
+  // bn may carry requests in its upper digits: 10000 * mc + 1000 * depth + bn
+  const int mc = bn / 10000;
+  bn %= 10000;
   int depth = bn / 1000;
   bn %= 1000;
+  if (mc != 0 && mc != 1 && mc != 2 && mc != 4) return FASER_EINVAL;
   if (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256) return FASER_EINVAL;
   if (!w || !x || !out || n_out <= 0 || t < 0 || k <= 0) return FASER_EINVAL;
   if (n_out % 128 || k % 64) return FASER_EINVAL;
@@ -51,7 +55,10 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
   if (make_act_operand(&X, x, t, k) != cudaSuccess) return FASER_ECUDA;
   GemmPlan plan = gemm_plan(n_out, t, k, num_sms());
   if (bn > 0) plan.bn = bn;
-  if (depth == 1) plan.deep = false;
+  if (mc > 0) plan.mc = mc;
+  if (plan.bn > 128 || plan.mc * plan.bn > 512) plan.mc = 1;  // instantiated combinations / TMEM
+  if (plan.mc > 1) plan.deep = true;
+  if (depth == 1 && plan.mc == 1) plan.deep = false;
   if (depth == 2) plan.deep = true;
   if (splits > 0) {  // caller-forced split count (cluster size <= 8)
     const int kb = k / 64, s1 = splits < 8 ? splits : 8;
@@ -64,6 +71,20 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
   ea.out = out;
   cudaError_t e = gemm_fused(W, X, t, plan, ea, s);
   return e == cudaSuccess ? FASER_OK : FASER_ECUDA;
+}
+
+extern "C" faser_status faser_k_gemm_plan(int32_t n_out, int32_t t, int32_t k, int32_t* out4) {
+  if (!out4 || n_out <= 0 || n_out % 128 || t <= 0 || k <= 0 || k % 64) return FASER_EINVAL;
+  int n = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    n = 148;
+  cudaGetLastError();
+  const GemmPlan p = gemm_plan(n_out, t, k, n);
+  out4[0] = p.bn;
+  out4[1] = p.splits;
+  out4[2] = p.mc;
+  out4[3] = p.deep ? 1 : 0;
+  return FASER_OK;
 }
 
 extern "C" faser_status faser_k_gemm_bf16(const void* w, const void* x, float* out, int32_t n_out,

@@ -765,10 +765,16 @@ class LlamaEngine {
     };
     // attention: the K/V bytes every request reads (its context incl. the new rows) + q/o
     const double abytes = static_cast<double>(f.kv_tokens) * 2 * s.n_kv * s.hd * 2 + 4.0 * T * s.n_q * s.hd;
+    // timing experiments only (FASER_SKIP bitmask, target verify forward): 1 attention, 2 qkv,
+    // 4 o, 8 gate/up, 16 down — results are garbage, the step time shows each class's share
+    static const int skip_env = getenv("FASER_SKIP") ? atoi(getenv("FASER_SKIP")) : 0;
+    const int skip = (f.logits && is_target) ? skip_env : 0;
     for (int l = 0; l < s.layers; ++l) {
       e_qkv.layer = l;
+      if (!(skip & 2))
       timed(gcls, gbytes(s.qkv_out(), s.d, s.qkv_out()),
             [&] { LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, fs)); });
+      if (!(skip & 1))
       timed(acls, abytes, [&] {
         LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
                          w.ob.as<__nv_bfloat16>(), w.attn.as<float>(), w.attn_bytes, fs));
@@ -782,12 +788,13 @@ class LlamaEngine {
       };
       if (tp_rows)
         row_parallel(m.op_o[l], w.op_ob, p_o);
-      else
+      else if (!(skip & 4))
         timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); });
+      if (!(skip & 8))
       timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); });
       if (tp_rows)
         row_parallel(m.op_d[l], w.op_h, p_d);
-      else
+      else if (!(skip & 16))
         timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); });
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers

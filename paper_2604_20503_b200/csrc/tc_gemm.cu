@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "sm100.cuh"
 #include "tc_gemm.cuh"
@@ -44,14 +45,18 @@ constexpr int kXBox = 32;                    // activation TMA box rows
 
 // ST = pipeline depth: "shallow" 4-stage configs (~100 KB smem for BN <= 64, 2 CTAs / SM, room
 // for the next GEMM's weight prefetch) or "deep" configs filling ~200 KB (1 CTA / SM).
-template <int BN, int ST>
+// MC = weight tiles (of 128 rows) per CTA sharing one rows tile: each SM's TMA ingest (~44 GB/s
+// per SM on B200, tools/tma_probe.cu) is spent on MC weight blocks per rows block instead of one.
+template <int BN, int ST, int MC>
 struct Cfg {
   static constexpr int kStages = ST;
   static constexpr int kBBytes = BN * kBK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kAStage = MC * kABytes;
+  static constexpr int kStageBytes = kAStage + kBBytes;
+  static constexpr int kTmemNeed = MC * (BN < 32 ? 32 : BN);
+  static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   static constexpr int kPipe = kStages * kStageBytes;
-  static constexpr int kTile = BN * kBM * 4;  // fp32 epilogue staging tile
+  static constexpr int kTile = BN * kBM * 4;  // fp32 epilogue staging tile (one weight tile at a time)
   static constexpr int kSmem = 1024 + (kPipe > kTile ? kPipe : kTile) + 12288;
 };
 
@@ -71,15 +76,15 @@ __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-template <int BN, int ST>
+template <int BN, int ST, int MC>
 __global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ EpiArgs ea, int n_out, int kb_total, int kb_per_split, int splits) {
-  using C = Cfg<BN, ST>;
+  using C = Cfg<BN, ST, MC>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::kStages * kABytes;
+  uint8_t* sB = smem + C::kStages * C::kAStage;
   uint8_t* aux = smem + (C::kPipe > C::kTile ? C::kPipe : C::kTile);
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + C::kStages;
@@ -92,7 +97,8 @@ __global__ void __launch_bounds__(128, 1)
   int* s_page = s_pos + 256;    // [256] per-token KV page
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM;
+  const int mb = blockIdx.x * MC * kBM;                       // first weight row of this CTA
+  const int ntile = min(MC, n_out / kBM - static_cast<int>(blockIdx.x) * MC);  // weight tiles here
   const int n0 = blockIdx.y * BN;
   const int kb0 = blockIdx.z * kb_per_split;
   const int kb1 = min(kb_total, kb0 + kb_per_split);
@@ -116,8 +122,9 @@ __global__ void __launch_bounds__(128, 1)
   const uint64_t pol_w = sm100::policy_evict_first();
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < npre; ++i) {
-      sm100::mbar_expect_tx(&full[i], kABytes);
-      sm100::tma_load_2d_hint(sA + i * kABytes, &tmW, &full[i], (kb0 + i) * kBK, m0, pol_w);
+      sm100::mbar_expect_tx(&full[i], ntile * kABytes);
+      for (int j = 0; j < ntile; ++j)
+        sm100::tma_load_2d_hint(sA + i * C::kAStage + j * kABytes, &tmW, &full[i], (kb0 + i) * kBK, mb + j * kBM, pol_w);
     }
   }
   pdl_wait();  // everything below may read the previous kernel's output
@@ -143,12 +150,13 @@ __global__ void __launch_bounds__(128, 1)
       const int s = i % C::kStages;
       const uint32_t ph = (i / C::kStages) & 1;
       const int kc = (kb0 + i) * kBK;
-      if (i < npre) {  // weight tile already in flight: add the activation tile and arrive
+      if (i < npre) {  // weight tiles already in flight: add the activation tile and arrive
         sm100::mbar_arrive_expect_tx(&full[s], xbytes);
       } else {
         sm100::mbar_wait(&empty[s], ph ^ 1);
-        sm100::mbar_arrive_expect_tx(&full[s], kABytes + xbytes);
-        sm100::tma_load_2d_hint(sA + s * kABytes, &tmW, &full[s], kc, m0, pol_w);
+        sm100::mbar_arrive_expect_tx(&full[s], ntile * kABytes + xbytes);
+        for (int j = 0; j < ntile; ++j)
+          sm100::tma_load_2d_hint(sA + s * C::kAStage + j * kABytes, &tmW, &full[s], kc, mb + j * kBM, pol_w);
       }
       for (int j = 0; j < xboxes; ++j)
         sm100::tma_load_2d(sB + s * C::kBBytes + j * kXBox * 128, &tmX, &full[s], kc, n0 + j * kXBox);
@@ -161,11 +169,13 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t ph = (i / C::kStages) & 1;
       sm100::mbar_wait(&full[s], ph);
       sm100::tc_fence_after();
-      const uint64_t da = sm100::desc_sw128(sm100::smem_u32(sA + s * kABytes));
       const uint64_t db = sm100::desc_sw128(sm100::smem_u32(sB + s * C::kBBytes));
+      for (int j = 0; j < ntile; ++j) {  // every weight tile of the stage against the same rows tile
+        const uint64_t da = sm100::desc_sw128(sm100::smem_u32(sA + s * C::kAStage + j * kABytes));
 #pragma unroll
-      for (int k = 0; k < kBK / kUmmaK; ++k)  // +32 bytes along K inside the swizzle atom
-        sm100::mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < kBK / kUmmaK; ++k)  // +32 bytes along K inside the swizzle atom
+          sm100::mma_bf16(tmem + j * (BN < 32 ? 32 : BN), da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+      }
       sm100::mma_commit(&empty[s]);
     }
     sm100::mma_commit(accum);
@@ -201,143 +211,148 @@ __global__ void __launch_bounds__(128, 1)
   sm100::mbar_wait(accum, 0);
   sm100::tc_fence_after();
   const int tn = min(BN, T - n0);          // live tokens of this tile
-  const int r = warp * 32 + lane;          // tile row owned in the TMEM read-out
-  float* S = reinterpret_cast<float*>(smem);  // [BN][128] fp32 staging (pipeline smem is free now)
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    if (c0 >= tn) break;
-    float v[32];
-    sm100::tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);  // one wait per 32 columns
-#pragma unroll
-    for (int i = 0; i < 32; ++i) S[(c0 + i) * kBM + r] = v[i];
-  }
-  sm100::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) sm100::tmem_dealloc<C::kTmemCols>(tmem);
-  // Split-K: the `splits` CTAs of this tile are one thread-block cluster. Each owns a slice of the
-  // tile's tokens and sums that slice over every CTA's partial through DSMEM in rank order
-  // (deterministic), then runs the epilogue on its slice.
-  int ts = 0, te = tn;
-  if (splits > 1) {
-    cluster_sync();
-    const int per = (tn + splits - 1) / splits;
-    ts = min(tn, static_cast<int>(blockIdx.z) * per);
-    te = min(tn, ts + per);
-    const uint32_t base = sm100::smem_u32(S);
-    uint32_t rb[16];
-#pragma unroll
-    for (int z = 0; z < 16; ++z) rb[z] = z < splits ? map_cta(base, z) : 0u;
-    const int c4 = threadIdx.x & 31, tq = threadIdx.x >> 5;  // 4 rows (float4) x 4 tokens per pass
-    for (int t = ts + tq; t < te; t += 4) {
-      const uint32_t off = (t * kBM + c4 * 4) * 4;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int z = 0; z < 16; ++z) {
-        if (z < splits) {
-          const float4 v = ld_dsmem4(rb[z] + off);
-          a.x += v.x;
-          a.y += v.y;
-          a.z += v.z;
-          a.w += v.w;
-        }
-      }
-      // only this CTA reads its own slice rows, so the in-place write is race-free
-      *reinterpret_cast<float4*>(S + t * kBM + c4 * 4) = a;
+  for (int j = 0; j < ntile; ++j) {        // weight tiles of this CTA, one staging pass each
+  const int m0 = mb + j * kBM;
+    const int r = warp * 32 + lane;          // tile row owned in the TMEM read-out
+    float* S = reinterpret_cast<float*>(smem);  // [BN][128] fp32 staging (pipeline smem is free now)
+  #pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      if (c0 >= tn) break;
+      float v[32];
+      sm100::tmem_ld32(tmem + j * (BN < 32 ? 32 : BN) + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);  // one wait per 32 columns
+  #pragma unroll
+      for (int i = 0; i < 32; ++i) S[(c0 + i) * kBM + r] = v[i];
     }
+    sm100::tc_fence_before();
     __syncthreads();
-  }
-  __syncthreads();  // (the per-token prologue was written by warps 2-3 during the mainloop)
-
-  // Token-per-warp passes: lane owns 4 consecutive tile rows (float4), a warp covers the 128
-  // rows of one token, 4 tokens per pass.
-  const int mode = ea.mode;
-  const int c4 = lane * 4;
-  if (mode == kEpiStore || mode == kEpiResid || mode == kEpiLogits) {
-    for (int t = ts + warp; t < te; t += 4) {
-      const float rs = s_rs[t];
-      float4 a = *reinterpret_cast<const float4*>(S + t * kBM + c4);
-      const size_t idx = static_cast<size_t>(n0 + t) * n_out + m0 + c4;
-      if (mode == kEpiStore) {
-        *reinterpret_cast<float4*>(ea.out + idx) = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
-      } else if (mode == kEpiResid) {
-        const float4 xv = *reinterpret_cast<const float4*>(ea.x + idx);
-        a = make_float4(xv.x + a.x, xv.y + a.y, xv.z + a.z, xv.w + a.w);
-        *reinterpret_cast<float4*>(ea.x + idx) = a;
-        __nv_bfloat162 b0 = __floats2bfloat162_rn(a.x, a.y), b1 = __floats2bfloat162_rn(a.z, a.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&b0);
-        pk.y = *reinterpret_cast<uint32_t*>(&b1);
-        *reinterpret_cast<uint2*>(ea.xb + idx) = pk;
-        float q = (a.x * a.x + a.y * a.y) + (a.z * a.z + a.w * a.w);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) ea.ss_out[static_cast<size_t>(blockIdx.x) * ea.t_stride + n0 + t] = q;
-      } else {  // kEpiLogits
-        a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
-        *reinterpret_cast<float4*>(ea.logits + idx) = a;
-        float bv = a.x;
-        const int id0 = ea.id_off + m0 + c4;
-        int bi = id0;
-        if (a.y > bv) { bv = a.y; bi = id0 + 1; }
-        if (a.z > bv) { bv = a.z; bi = id0 + 2; }
-        if (a.w > bv) { bv = a.w; bi = id0 + 3; }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
+    if (warp == 2 && j == ntile - 1) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+    // Split-K: the `splits` CTAs of this tile are one thread-block cluster. Each owns a slice of the
+    // tile's tokens and sums that slice over every CTA's partial through DSMEM in rank order
+    // (deterministic), then runs the epilogue on its slice.
+    int ts = 0, te = tn;
+    if (splits > 1) {
+      cluster_sync();
+      const int per = (tn + splits - 1) / splits;
+      ts = min(tn, static_cast<int>(blockIdx.z) * per);
+      te = min(tn, ts + per);
+      const uint32_t base = sm100::smem_u32(S);
+      uint32_t rb[16];
+  #pragma unroll
+      for (int z = 0; z < 16; ++z) rb[z] = z < splits ? map_cta(base, z) : 0u;
+      const int c4 = threadIdx.x & 31, tq = threadIdx.x >> 5;  // 4 rows (float4) x 4 tokens per pass
+      for (int t = ts + tq; t < te; t += 4) {
+        const uint32_t off = (t * kBM + c4 * 4) * 4;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  #pragma unroll
+        for (int z = 0; z < 16; ++z) {
+          if (z < splits) {
+            const float4 v = ld_dsmem4(rb[z] + off);
+            a.x += v.x;
+            a.y += v.y;
+            a.z += v.z;
+            a.w += v.w;
           }
         }
-        if (lane == 0) ea.amax[static_cast<size_t>(blockIdx.x) * ea.t_stride + n0 + t] = make_float2(bv, __int_as_float(bi));
+        // only this CTA reads its own slice rows, so the in-place write is race-free
+        *reinterpret_cast<float4*>(S + t * kBM + c4 * 4) = a;
+      }
+      __syncthreads();
+    }
+    __syncthreads();  // (the per-token prologue was written by warps 2-3 during the mainloop)
+
+    // Token-per-warp passes: lane owns 4 consecutive tile rows (float4), a warp covers the 128
+    // rows of one token, 4 tokens per pass.
+    const int mode = ea.mode;
+    const int c4 = lane * 4;
+    if (mode == kEpiStore || mode == kEpiResid || mode == kEpiLogits) {
+      for (int t = ts + warp; t < te; t += 4) {
+        const float rs = s_rs[t];
+        float4 a = *reinterpret_cast<const float4*>(S + t * kBM + c4);
+        const size_t idx = static_cast<size_t>(n0 + t) * n_out + m0 + c4;
+        if (mode == kEpiStore) {
+          *reinterpret_cast<float4*>(ea.out + idx) = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+        } else if (mode == kEpiResid) {
+          const float4 xv = *reinterpret_cast<const float4*>(ea.x + idx);
+          a = make_float4(xv.x + a.x, xv.y + a.y, xv.z + a.z, xv.w + a.w);
+          *reinterpret_cast<float4*>(ea.x + idx) = a;
+          __nv_bfloat162 b0 = __floats2bfloat162_rn(a.x, a.y), b1 = __floats2bfloat162_rn(a.z, a.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&b0);
+          pk.y = *reinterpret_cast<uint32_t*>(&b1);
+          *reinterpret_cast<uint2*>(ea.xb + idx) = pk;
+          float q = (a.x * a.x + a.y * a.y) + (a.z * a.z + a.w * a.w);
+  #pragma unroll
+          for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+          if (lane == 0) ea.ss_out[static_cast<size_t>(m0 / kBM) * ea.t_stride + n0 + t] = q;
+        } else {  // kEpiLogits
+          a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+          *reinterpret_cast<float4*>(ea.logits + idx) = a;
+          float bv = a.x;
+          const int id0 = ea.id_off + m0 + c4;
+          int bi = id0;
+          if (a.y > bv) { bv = a.y; bi = id0 + 1; }
+          if (a.z > bv) { bv = a.z; bi = id0 + 2; }
+          if (a.w > bv) { bv = a.w; bi = id0 + 3; }
+  #pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          if (lane == 0) ea.amax[static_cast<size_t>(m0 / kBM) * ea.t_stride + n0 + t] = make_float2(bv, __int_as_float(bi));
+        }
+      }
+    } else if (mode == kEpiQkv) {
+      const int hd = ea.hd, half = hd >> 1;
+      constexpr int pairs = kBM / 2;  // 64 rotation pairs per 128-row tile
+      for (int e = threadIdx.x; e < (te - ts) * pairs; e += 128) {
+        const int t = ts + e / pairs, p = e % pairs;
+        const int hl = p / half, i = p % half;
+        const int ra = hl * hd + i, rb = ra + half;
+        const int head = (m0 + ra) / hd;
+        const float rs = s_rs[t];
+        float a = S[t * kBM + ra] * rs, b = S[t * kBM + rb] * rs;
+        const int row = n0 + t;
+        const int pos = s_pos[t];
+        if (head < ea.n_q + ea.n_kv) {
+          const float2 cs = ea.rope[static_cast<size_t>(pos) * half + i];
+          const float ra2 = a * cs.x - b * cs.y, rb2 = b * cs.x + a * cs.y;
+          a = ra2;
+          b = rb2;
+        }
+        if (head < ea.n_q) {
+          __nv_bfloat16* qd = ea.q + (static_cast<size_t>(row) * ea.n_q + head) * hd;
+          qd[i] = __float2bfloat16_rn(a);
+          qd[i + half] = __float2bfloat16_rn(b);
+        } else {
+          const bool is_v = head >= ea.n_q + ea.n_kv;
+          const int kvh = is_v ? head - ea.n_q - ea.n_kv : head - ea.n_q;
+          __nv_bfloat16* dst = ea.kv.pool + ea.layer * ea.kv.layer_stride +
+                               ((static_cast<size_t>(s_page[t]) * ea.n_kv + kvh) * 2 + (is_v ? 1 : 0)) * kPage * hd +
+                               (pos % kPage) * hd;
+          dst[i] = __float2bfloat16_rn(a);
+          dst[i + half] = __float2bfloat16_rn(b);
+        }
+      }
+    } else {  // kEpiSwiglu: 128-row group = 64 gate rows then 64 up rows
+      const int j0 = m0 >> 1;
+      for (int e = threadIdx.x; e < (te - ts) * 32; e += 128) {
+        const int t = ts + (e >> 5), w = (e & 31) * 2;
+        const float rs = s_rs[t];
+        const float2 g = *reinterpret_cast<const float2*>(S + t * kBM + w);
+        const float2 u = *reinterpret_cast<const float2*>(S + t * kBM + 64 + w);
+        const float g0 = g.x * rs, g1 = g.y * rs;
+        const float h0 = g0 / (1.f + __expf(-g0)) * (u.x * rs), h1 = g1 / (1.f + __expf(-g1)) * (u.y * rs);
+        *reinterpret_cast<__nv_bfloat162*>(ea.h + static_cast<size_t>(n0 + t) * ea.ffn + j0 + w) = __floats2bfloat162_rn(h0, h1);
       }
     }
-  } else if (mode == kEpiQkv) {
-    const int hd = ea.hd, half = hd >> 1;
-    constexpr int pairs = kBM / 2;  // 64 rotation pairs per 128-row tile
-    for (int e = threadIdx.x; e < (te - ts) * pairs; e += 128) {
-      const int t = ts + e / pairs, p = e % pairs;
-      const int hl = p / half, i = p % half;
-      const int ra = hl * hd + i, rb = ra + half;
-      const int head = (m0 + ra) / hd;
-      const float rs = s_rs[t];
-      float a = S[t * kBM + ra] * rs, b = S[t * kBM + rb] * rs;
-      const int row = n0 + t;
-      const int pos = s_pos[t];
-      if (head < ea.n_q + ea.n_kv) {
-        const float2 cs = ea.rope[static_cast<size_t>(pos) * half + i];
-        const float ra2 = a * cs.x - b * cs.y, rb2 = b * cs.x + a * cs.y;
-        a = ra2;
-        b = rb2;
-      }
-      if (head < ea.n_q) {
-        __nv_bfloat16* qd = ea.q + (static_cast<size_t>(row) * ea.n_q + head) * hd;
-        qd[i] = __float2bfloat16_rn(a);
-        qd[i + half] = __float2bfloat16_rn(b);
-      } else {
-        const bool is_v = head >= ea.n_q + ea.n_kv;
-        const int kvh = is_v ? head - ea.n_q - ea.n_kv : head - ea.n_q;
-        __nv_bfloat16* dst = ea.kv.pool + ea.layer * ea.kv.layer_stride +
-                             ((static_cast<size_t>(s_page[t]) * ea.n_kv + kvh) * 2 + (is_v ? 1 : 0)) * kPage * hd +
-                             (pos % kPage) * hd;
-        dst[i] = __float2bfloat16_rn(a);
-        dst[i + half] = __float2bfloat16_rn(b);
-      }
-    }
-  } else {  // kEpiSwiglu: 128-row group = 64 gate rows then 64 up rows
-    const int j0 = m0 >> 1;
-    for (int e = threadIdx.x; e < (te - ts) * 32; e += 128) {
-      const int t = ts + (e >> 5), w = (e & 31) * 2;
-      const float rs = s_rs[t];
-      const float2 g = *reinterpret_cast<const float2*>(S + t * kBM + w);
-      const float2 u = *reinterpret_cast<const float2*>(S + t * kBM + 64 + w);
-      const float g0 = g.x * rs, g1 = g.y * rs;
-      const float h0 = g0 / (1.f + __expf(-g0)) * (u.x * rs), h1 = g1 / (1.f + __expf(-g1)) * (u.y * rs);
-      *reinterpret_cast<__nv_bfloat162*>(ea.h + static_cast<size_t>(n0 + t) * ea.ffn + j0 + w) = __floats2bfloat162_rn(h0, h1);
-    }
-  }
   if (splits > 1) cluster_sync();  // peers may still be reading this CTA's partial
+  __syncthreads();                 // the staging tile is reused by the next weight tile
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -359,20 +374,22 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int BN, int ST>
+template <int BN, int ST, int MC = 1>
 cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int splits, const EpiArgs& ea,
                       cudaStream_t s) {
-  using C = Cfg<BN, ST>;
+  using C = Cfg<BN, ST, MC>;
+  static_assert(C::kSmem <= 232448, "shared memory budget");
+  static_assert(C::kTmemNeed <= 512, "TMEM budget");
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    cudaFuncSetAttribute(gemm_kernel<BN, ST>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_kernel<BN, ST, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_kernel<BN, ST, MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   const int kb_total = w.k / kBK;
   const int kps = (kb_total + splits - 1) / splits;
   const int z = (kb_total + kps - 1) / kps;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(w.rows / kBM, (t + BN - 1) / BN, z);
+  cfg.gridDim = dim3((w.rows / kBM + MC - 1) / MC, (t + BN - 1) / BN, z);
   cfg.blockDim = dim3(128, 1, 1);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = s;
@@ -387,7 +404,7 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
   attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = z > 1 ? 2 : 1;  // cluster launch only when the K split needs DSMEM
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST>, w.map, x.map, ea, w.rows, kb_total, kps, z);
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST, MC>, w.map, x.map, ea, w.rows, kb_total, kps, z);
 }
 
 }  // namespace
@@ -424,7 +441,8 @@ cudaError_t make_act_operand(GemmOperand* op, const void* x, int rows_cap, int k
 //    deep pipeline while the grid fits one CTA per SM, 4-stage (2 CTAs/SM) beyond.
 constexpr int kMaxSplit = 4;
 
-GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
+// Legacy plan (graph-timed sweeps of the MC = 1 kernel; FASER_GEMM_PLAN=legacy).
+GemmPlan gemm_plan_legacy(int n_out, int t, int k, int num_sms) {
   GemmPlan p;
   const int mt = n_out / kBM;
   const int kb = k / kBK;
@@ -461,11 +479,65 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
   return p;
 }
 
+// Engine plan = the legacy plan plus the shape classes where a graph-timed (bn, mc, split) sweep
+// on B200 found a clearly better launch (tools/gemm_sweep.py, profiles/r01_gemm_sweep.jsonl):
+//  * wide outputs (LM heads, >= 120 weight tiles) at <= 128 rows: two weight tiles per rows tile
+//    (mc = 2), no split: 32000x2048 @128 rows 36.1 -> 29.3 us, 32000x768 @32 13.2 -> 11.4 us;
+//  * >= 512 rows and >= 64 tiles: mc = 4 at 128-row token tiles (11264x2048 @512: 52 -> 44 us);
+//  * <= 32 rows and >= 40 tiles: no K split (6144x768 @32: 10.3 -> 5.7 us);
+//  * <= 8 tiles with K >= 3072: 8-way K split (768x3072 @32: 6.7 -> 5.4 us).
+// Per SM the TMA ingest saturates near 44 GB/s (tools/tma_probe.cu), which is why sharing one
+// rows tile across weight tiles pays once the rows tile is comparable to a weight block.
+GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
+  static const bool legacy = getenv("FASER_GEMM_PLAN") && std::string(getenv("FASER_GEMM_PLAN")) == "legacy";
+  GemmPlan p = gemm_plan_legacy(n_out, t, k, num_sms);
+  if (legacy) return p;
+  const int mt = n_out / kBM;
+  const int kb = k / kBK;
+  int cover = 32;
+  while (cover < t && cover < 256) cover <<= 1;
+  if (mt >= 120 && t <= 128) {
+    p.bn = cover;
+    p.mc = 2;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t >= 512 && mt >= 64) {
+    p.bn = 128;
+    p.mc = 4;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t <= 32 && mt >= 40 && k <= 1024) {
+    p.bn = 32;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = true;
+  } else if (mt <= 8 && k >= 3072 && t <= 128) {
+    const int kps = (kb + 7) / 8;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
+  }
+  return p;
+}
+
 cudaError_t gemm_fused(const GemmOperand& w, const GemmOperand& x, int t, const GemmPlan& p, const EpiArgs& epi,
                        cudaStream_t s) {
   if (t <= 0) return cudaSuccess;
   if (w.k != x.k) return cudaErrorInvalidValue;
   const bool deep = p.deep;
+  if (p.mc == 4) {
+    switch (p.bn) {
+      case 32: return launch_bn<32, 3, 4>(w, x, t, p.splits, epi, s);
+      case 64: return launch_bn<64, 2, 4>(w, x, t, p.splits, epi, s);
+      default: return launch_bn<128, 2, 4>(w, x, t, p.splits, epi, s);
+    }
+  }
+  if (p.mc == 2) {
+    switch (p.bn) {
+      case 32: return launch_bn<32, 5, 2>(w, x, t, p.splits, epi, s);
+      case 64: return launch_bn<64, 5, 2>(w, x, t, p.splits, epi, s);
+      default: return launch_bn<128, 4, 2>(w, x, t, p.splits, epi, s);
+    }
+  }
   switch (p.bn) {
     case 32: return deep ? launch_bn<32, 8>(w, x, t, p.splits, epi, s) : launch_bn<32, 4>(w, x, t, p.splits, epi, s);
     case 64: return deep ? launch_bn<64, 7>(w, x, t, p.splits, epi, s) : launch_bn<64, 4>(w, x, t, p.splits, epi, s);

@@ -61,6 +61,7 @@ struct GemmPlan {
   int splits = 1;
   int tiles = 0;
   bool deep = true;  // deep pipeline (~200 KB smem, 1 CTA / SM) vs 4-stage (2 CTAs / SM)
+  int mc = 1;        // 128-row weight tiles per CTA sharing one rows tile (1, 2, 4)
 };
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms);
 

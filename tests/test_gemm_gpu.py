@@ -26,15 +26,15 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("n_out,T,K", SHAPES)
-@pytest.mark.parametrize("splits", [0, 1, 3])
-def test_gemm_matches_fp32(L, n_out, T, K, splits):
+@pytest.mark.parametrize("splits,mc", [(0, 0), (1, 1), (3, 1), (1, 2), (5, 2), (2, 4), (8, 4)])
+def test_gemm_matches_fp32(L, n_out, T, K, splits, mc):
     import torch
     g = torch.Generator(device="cuda").manual_seed(n_out * 7 + T * 3 + K)
     w = (torch.randn(n_out, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
     x = torch.randn(T, K, device="cuda", generator=g).to(torch.bfloat16)
     out = torch.full((T, n_out), float("nan"), device="cuda", dtype=torch.float32)
-    rc = L.faser_k_gemm_bf16(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()),
-                             C.c_void_p(out.data_ptr()), n_out, T, K, splits, None)
+    rc = L.faser_k_gemm_bf16_plan(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()),
+                                  C.c_void_p(out.data_ptr()), n_out, T, K, 10000 * mc, splits, None)
     assert rc == 0
     torch.cuda.synchronize()
     ref = x.float() @ w.float().t()
