@@ -37,6 +37,12 @@ sys.path.insert(0, ROOT)
 from paper_2604_20503_b200 import abi  # noqa: E402
 
 METRIC = "accepted tokens/sec (committed output tokens per second)"
+WORKLOAD_NAMES = {
+    "cfg3": "config 3: llama-68m-shape draft / TinyLlama-1.1B-shape target",
+    "cfg4": "config 4: Llama-3.2-1B-shape draft / Llama-3.1-8B-shape target",
+    "cfg5": "config 5: Llama-3.2-1B-shape draft / Llama-3.1-70B-shape target",
+    "tiny": "tiny test pair", "tp_tiny": "tiny TP test pair",
+}
 UNIT = "tokens/s"
 
 
@@ -220,7 +226,7 @@ def llama_desc(name):
 def make_engine(desc, args, local_rank, **tp):
     from paper_2604_20503_b200 import engine
     mode = {"vsd": abi.MODE_VSD, "ad": abi.MODE_VSD_AD, "ee": abi.MODE_VSD_AD_EE,
-            "ov": abi.MODE_FULL, "full": abi.MODE_FULL}[args.mode]
+            "ov": abi.MODE_FULL, "full": abi.MODE_FULL, "vsd_ee": abi.MODE_VSD_AD_EE}[args.mode]
     return engine.ServingEngine(desc=desc, max_batch=args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
                                 mode=mode, default_spec_length=args.k, max_spec_length=16,
                                 prefill_rows=8192, device=local_rank, **tp)
@@ -292,7 +298,7 @@ def llama_tp(args, rank, world, local_rank):
 def gate_plan(desc, args):
     """Fixed gate (--gate-layer l: gate exactly layer l) or None = per-step make_gate_plan
     (exitctl.cpp:70-82) on the B200-fitted latency models."""
-    if args.mode != "ee" or not args.gate_layer:
+    if args.mode not in ("ee", "vsd_ee") or not args.gate_layer:
         return None
     return abi.GatePlan(args.gate_layer, args.gate_layer + 1, 1.0)
 
@@ -304,7 +310,7 @@ def step_plan_hook(desc, args, models):
     L = desc.target.layers
 
     def hook(eng, live, ks):
-        if args.mode == "ee" and not args.gate_layer:
+        if args.mode in ("ee", "vsd_ee") and not args.gate_layer:
             eng.set_gate(engine.make_gate_plan(abi.ExitPolicy.default(), [(k, 0.6) for k in ks],
                                                float(len(ks)), 0.5, L, models))
         if args.mode in ("ov", "full"):
@@ -371,7 +377,7 @@ def llama_ours(args, rank, world, local_rank):
     hook = step_plan_hook(desc, args, models)
 
     def new_drafter():
-        if args.mode in ("vsd", "ov"):
+        if args.mode in ("vsd", "ov", "vsd_ee"):  # fixed k (vsd_ee: early exit without the k controller)
             return None
         from paper_2604_20503_b200 import controller
         return controller.AdaptiveDrafter(models=models)
@@ -480,11 +486,11 @@ def llama_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts (synth_prompt), random-init weights",
         "p50_tpot_ms": tpot,
-        "config": {"workload": f"config 3: llama-68m-shape draft / TinyLlama-1.1B-shape target, "
+        "config": {"workload": f"{WORKLOAD_NAMES.get(args.workload, args.workload)}, "
                                f"continuous batching B={B}/GPU, k={args.k}, mode={args.mode}",
                    "global_batch": B * world, "seq_len": f"in U{list(IN_RANGE)} out U{list(OUT_RANGE)}",
                    "parallelism": f"replicas x{world} (request-sharded)",
-                   "l2": "weights 2.2 GB per verify >> 126 MB L2 (inputs larger than L2)"},
+                   "l2": "target weights per verify >> 126 MB L2 (inputs larger than L2)"},
         "e2e": {"value": tokens2 / e2e_s, "unit": UNIT, "p50_tpot_ms": e2e_tpot,
                 "h2d_bytes_per_step": int((h2d[0] + sub_bytes[0]) / max(args.steps, 1)),
                 "d2h_bytes_per_step": int(d2h[0] / max(args.steps, 1))},
@@ -686,7 +692,7 @@ def main():
     ap.add_argument("--tp", action="store_true", help="tensor-parallel verification over the launched ranks")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--k", type=int, default=4)
-    ap.add_argument("--mode", default="vsd", choices=["vsd", "ad", "ee", "ov", "full"])
+    ap.add_argument("--mode", default="vsd", choices=["vsd", "ad", "ee", "ov", "full", "vsd_ee"])
     ap.add_argument("--chunk", type=int, default=0, help="overlap chunk (0: plan_overlap decides)")
     ap.add_argument("--gate-layer", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)

@@ -11,6 +11,7 @@ preset = sys.argv[1]
 B = int(sys.argv[2])
 k = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 mode = int(sys.argv[4]) if len(sys.argv) > 4 else abi.MODE_VSD
+gate_layer = int(sys.argv[5]) if len(sys.argv) > 5 else 8
 desc = llama.PRESETS[preset]()
 V = desc.target.vocab
 rng = np.random.default_rng(2)
@@ -22,9 +23,9 @@ eng.step()
 print("prefill+first step ms", eng.last_step_timing(), flush=True)
 ts = []
 tok = 0
-for s in range(10):
+for s in range(int(os.environ.get('PERF_STEPS', 10))):
     if mode >= abi.MODE_VSD_AD_EE:
-        eng.set_gate(abi.GatePlan(8, 9, 1.0))
+        eng.set_gate(abi.GatePlan(gate_layer, gate_layer + 1, 1.0))
     res = eng.step()
     tok += sum(r.committed for r in res)
     ts.append(eng.last_step_timing())
