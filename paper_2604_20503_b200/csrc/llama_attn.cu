@@ -71,8 +71,10 @@ __device__ __forceinline__ int swz(int row, int chunk) {
   return row * (HD * 2) + ((chunk ^ (row & 7)) << 4);
 }
 
-template <int HD, bool ROWS>
-__global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int layer, int n_q, int n_kv,
+// MT = 16-row M tiles per CTA in GROUP mode (128 threads per tile): the tiles of one (request,
+// kv head) share every K/V page load instead of re-reading it per tile.
+template <int HD, bool ROWS, int MT = 1>
+__global__ void __launch_bounds__(128 * MT) attn_kernel(RowsDev rows, KvDev kv, int layer, int n_q, int n_kv,
                                                    const __nv_bfloat16* __restrict__ qbuf,
                                                    __nv_bfloat16* __restrict__ obuf, float* __restrict__ part_o,
                                                    float2* __restrict__ part_ml, int* __restrict__ counters,
@@ -95,14 +97,15 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   const int M = nr << gs;
   const int blk = blockIdx.z / n_split, sp = blockIdx.z % n_split;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta_m0 = ROWS ? blk * 64 : blk * 16;
+  constexpr int NT = 128 * MT;  // threads
+  const int cta_m0 = ROWS ? blk * 64 : blk * 16 * MT;
   if (cta_m0 >= M) return;
-  const int cta_m1 = min(M, cta_m0 + (ROWS ? 64 : 16));
-  // GROUP mode: one 16-row M tile per CTA, the 4 warps split each page's four 16-key chunks
-  // (latency-bound decode: short per-warp dependency chains beat reading each page once)
+  const int cta_m1 = min(M, cta_m0 + (ROWS ? 64 : 16 * MT));
+  // GROUP mode: MT 16-row M tiles per CTA, 4 warps per tile split each page's four 16-key
+  // chunks (latency-bound decode: short per-warp dependency chains)
   const int nmt = ROWS ? 4 : 1;
   const int nkg = 4 / nmt;
-  const int mt = warp % nmt, kg = warp / nmt;
+  const int mt = ROWS ? warp % 4 : warp / 4, kg = ROWS ? 0 : warp % 4;
   const int first = rows.req_first[req], pos0 = rows.req_pos0[req];
   const int slot = rows.req_slot[req];
   const int key_end = pos0 + ((cta_m1 - 1) >> gs) + 1;
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   // page ids of this CTA's key range, fetched once (a global load per page would sit on the
   // critical path of every pipeline step)
   __shared__ int s_page[kMaxPagesPerCta];
-  for (int i = threadIdx.x; i < t1 - t0 && i < kMaxPagesPerCta; i += 128)
+  for (int i = threadIdx.x; i < t1 - t0 && i < kMaxPagesPerCta; i += NT)
     s_page[i] = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t0 + i];
   __syncthreads();
   auto load_tile = [&](int t, int buf) {
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
     uint8_t* sk = smem + buf * 2 * kTileBytes;
     uint8_t* sv = sk + kTileBytes;
 #pragma unroll
-    for (int i = threadIdx.x; i < 64 * kChunks; i += 128) {
+    for (int i = threadIdx.x; i < 64 * kChunks; i += NT) {
       const int r = i / kChunks, c = i % kChunks;
       cp_async16(sk + swz<HD>(r, c), gk + i * 16);
       cp_async16(sv + swz<HD>(r, c), gv + i * 16);
@@ -253,9 +256,9 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   }
 
   // ---- merge the warps that share an M tile (GROUP mode) through smem: per-row (m, l, O)
-  float* so = reinterpret_cast<float*>(smem);  // [4 warps][16][HD]
-  float* sm = so + 4 * 16 * HD;                // [4][16]
-  float* sl_ = sm + 64;                        // [4][16]
+  float* so = reinterpret_cast<float*>(smem);  // [4*MT warps][16][HD]
+  float* sm = so + 4 * MT * 16 * HD;           // [4*MT][16]
+  float* sl_ = sm + 64 * MT;                   // [4*MT][16]
   {
     const int rl = lane >> 2, rh = rl + 8;
 #pragma unroll
@@ -275,17 +278,17 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   }
   __syncthreads();
   // each (packed row, dim) of this CTA: combine its warps -> final (n_split == 1) or partial
-  const int ntiles = ROWS ? 4 : nmt;
+  const int ntiles = ROWS ? 4 : MT;
   const int wpt = ROWS ? 1 : nkg;  // warps per tile
-  for (int e = threadIdx.x; e < ntiles * 16 * HD; e += 128) {
+  for (int e = threadIdx.x; e < ntiles * 16 * HD; e += NT) {
     const int tl = e / (16 * HD), r = (e / HD) % 16, col = e % HD;
     const int m = cta_m0 + tl * 16 + r;
     if (m >= cta_m1) continue;
     float mm = kNegBig;
-    for (int g = 0; g < wpt; ++g) mm = fmaxf(mm, sm[(tl + g * nmt) * 16 + r]);
+    for (int g = 0; g < wpt; ++g) mm = fmaxf(mm, sm[(ROWS ? tl : tl * 4 + g) * 16 + r]);
     float l = 0.f, acc = 0.f;
     for (int g = 0; g < wpt; ++g) {
-      const int w = tl + g * nmt;
+      const int w = ROWS ? tl : tl * 4 + g;
       const float f = exp2f(sm[w * 16 + r] - mm);
       l += sl_[w * 16 + r] * f;
       acc += so[(w * 16 + r) * HD + col] * f;
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   // per packed row: merged max, and each split's weight exp2(m_s - m) / l  (fixed split order)
   float* sfac = reinterpret_cast<float*>(smem);  // [64 rows][16 splits]
   const int nrow = cta_m1 - cta_m0;
-  for (int mr = threadIdx.x; mr < nrow; mr += 128) {
+  for (int mr = threadIdx.x; mr < nrow; mr += NT) {
     const int m = cta_m0 + mr;
     const int row = first + (m >> gs), head = kvh * G + (m & gm);
     float2 ml[16];
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
       if (sp2 < n_split) sfac[mr * 16 + sp2] = exp2f(ml[sp2].x - mm) * inv;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nrow * (HD / 4); e += 128) {
+  for (int e = threadIdx.x; e < nrow * (HD / 4); e += NT) {
     const int mr = e / (HD / 4), c4 = (e % (HD / 4)) * 4;
     const int m = cta_m0 + mr;
     const int row = first + (m >> gs), head = kvh * G + (m & gm);
@@ -359,21 +362,21 @@ __global__ void __launch_bounds__(128) attn_kernel(RowsDev rows, KvDev kv, int l
   }
 }
 
-template <int HD, bool ROWS>
+template <int HD, bool ROWS, int MT = 1>
 cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int n_split, KvDev kv,
                    int layer, const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, float* part_o,
                    float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s) {
   constexpr int kTile = 64 * HD * 2;
-  constexpr int kMerge = (4 * 16 * HD + 128) * 4;
+  constexpr int kMerge = (4 * MT * 16 * HD + 128 * MT) * 4;
   constexpr int kSmem = 2 * kAttnStages<HD> * kTile > kMerge ? 2 * kAttnStages<HD> * kTile : kMerge;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_kernel<HD, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(attn_kernel<HD, ROWS, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
   dim3 grid(n_req, m.n_kv, blocks * n_split);
-  attn_kernel<HD, ROWS><<<grid, 128, kSmem, s>>>(rows, kv, layer, m.n_q, m.n_kv, qbuf, obuf, part_o,
-                                                 part_ml, counters, n_split, rows_cap, blocks, scale_log2);
+  attn_kernel<HD, ROWS, MT><<<grid, 128 * MT, kSmem, s>>>(rows, kv, layer, m.n_q, m.n_kv, qbuf, obuf, part_o,
+                                                          part_ml, counters, n_split, rows_cap, blocks, scale_log2);
   return cudaGetLastError();
 }
 
@@ -388,7 +391,10 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   if (G & (G - 1)) return cudaErrorInvalidValue;  // GQA group must be a power of two
   const int Mmax = max_rows_per_req * G;
   const bool rows_mode = Mmax > 64;
-  const int blocks = rows_mode ? (Mmax + 63) / 64 : (Mmax + 15) / 16;
+  // GROUP mode with > 16 packed rows: two M tiles per CTA (256 threads) share each page load
+  static const bool mt1 = getenv("FASER_ATTN_MT1") != nullptr;
+  const int mt = (!rows_mode && Mmax > 16 && !mt1) ? 2 : 1;
+  const int blocks = rows_mode ? (Mmax + 63) / 64 : (Mmax + 16 * mt - 1) / (16 * mt);
   const int rows_cap = n_req * max_rows_per_req;  // row indices are < sum of req_n <= this
   // scratch = [counters (1 MiB, zeroed at allocation, self-resetting)][part_o][part_ml]
   constexpr size_t kCounterBytes = size_t(1) << 20;
@@ -410,11 +416,14 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   float* part_o = body;
   float2* part_ml = reinterpret_cast<float2*>(body + static_cast<size_t>(n_split) * rows_cap * m.n_q * m.hd);
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(m.hd));
-  if (m.hd == 64)
-    return rows_mode ? launch<64, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s)
-                     : launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
-  return rows_mode ? launch<128, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s)
-                   : launch<128, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+  if (m.hd == 64) {
+    if (rows_mode) return launch<64, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+    if (mt == 2) return launch<64, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+    return launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+  }
+  if (rows_mode) return launch<128, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+  if (mt == 2) return launch<128, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+  return launch<128, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
 }
 
 }  // namespace faser
