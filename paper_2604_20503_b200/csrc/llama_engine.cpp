@@ -597,6 +597,8 @@ class LlamaEngine {
     const int* k_table = nullptr;
     bool capture = false;
     int64_t kv_tokens = 0;  // sum over requests of the context each attention call reads
+    bool pre_embedded = false;  // rows' embeddings already written (fused draft control kernel)
+    bool skip_argmax = false;   // leave the LM head's per-tile (max, id) partials for the caller
   };
 
   GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, nsm); }
@@ -753,8 +755,10 @@ class LlamaEngine {
       if (st.trace) dump_mega_trace(s.layers, mc.grid);
       return;
     }
-    LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), fs));
-    ++launches;
+    if (!f.pre_embedded) {
+      LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), fs));
+      ++launches;
+    }
     // kernel classes for timing: target verify (logits) vs draft model; prefill untimed
     const bool is_target = &m == &target;
     const int gcls = f.logits ? (is_target ? 0 : 2) : -1;
@@ -817,7 +821,7 @@ class LlamaEngine {
         LCK(tpg->allgather_f2(tp_rank, tp_loc.as<float2>(), tp_all.as<float2>(), static_cast<size_t>(T), fs));
         LCK(tp_merge_argmax(tp, T, tp_all.as<float2>(), f.argmax_out, fs));
         launches += 2;
-      } else {
+      } else if (!f.skip_argmax) {
         LCK(lm_argmax_reduce(s.vocab / 128, rows, T, w.amax.as<float2>(), f.argmax_out, fs));
       }
       launches += 2;
@@ -1180,9 +1184,41 @@ class LlamaEngine {
         throw LFail{FASER_EINVAL, "invalid exit policy"};
       }
     }
+    // fused draft control (one launch between draft forwards) unless the persistent forward,
+    // which embeds and reduces the argmax itself, is on
+    const bool fuse_draft = !mega_on && !(getenv("FASER_UNFUSED_DRAFT") && getenv("FASER_UNFUSED_DRAFT")[0] == '1');
+    auto rows_at = [&](int t) {
+      int c = 0;
+      while (c < n && ents[c].k > t) ++c;
+      return c;
+    };
     auto draft_step = [&](int t) {
-      int nt = 0;
-      while (nt < n && ents[nt].k > t) ++nt;
+      const int nt = rows_at(t);
+      if (fuse_draft) {
+        if (t == 0) {
+          LCK(lm_draft_begin(sl, q, wd.rows, nt, draft.emb, dsh.d, wd.x.as<float>(), wd.xb.as<__nv_bfloat16>(),
+                             wd.ss.as<float>(), stream));
+          ++launches;
+        }
+        Fwd f;
+        f.rows = wd.rows;
+        f.T = nt;
+        f.n_req = nt;
+        f.max_rows = 1;
+        f.max_ctx = maxctx;
+        f.logits = true;
+        f.argmax_out = wd.argmax.as<int>();
+        f.kv_tokens = ctx_sum + static_cast<int64_t>(nt) * (t + 1);
+        f.pre_embedded = true;
+        f.skip_argmax = true;
+        fs = stream;
+        forward(draft, wd, f);
+        const int n_next = t + 1 < kmax ? rows_at(t + 1) : 0;
+        LCK(lm_draft_advance(sl, q, wd.rows, wd.amax.as<float2>(), dsh.vocab / 128, nt, t, n_next, draft.emb, dsh.d,
+                             wd.x.as<float>(), wd.xb.as<__nv_bfloat16>(), wd.ss.as<float>(), stream));
+        ++launches;
+        return;
+      }
       LCK(lm_draft_prep(sl, q, wd.rows, nt, t, stream));
       Fwd f;
       f.rows = wd.rows;

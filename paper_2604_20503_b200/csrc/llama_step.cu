@@ -43,6 +43,90 @@ __global__ void draft_prep_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int n
                            : rq.drafted[r * kMS + t - 1];
 }
 
+// Embedding of one row by one warp: x = emb[tok] (fp32), xb = bf16 copy, ss[c][r] = sum of
+// squares of 128-column chunk c (the next GEMM folds RMSNorm from it).
+__device__ __forceinline__ void embed_row_warp(const __nv_bfloat16* __restrict__ emb, int tok, int r, int d,
+                                               int t_stride, float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                                               float* __restrict__ ss, int lane) {
+  for (int c = 0; c < d / 128; ++c) {
+    const int col = c * 128 + lane * 4;
+    const uint2 e = *reinterpret_cast<const uint2*>(emb + static_cast<int64_t>(tok) * d + col);
+    const __nv_bfloat162 e0 = *reinterpret_cast<const __nv_bfloat162*>(&e.x);
+    const __nv_bfloat162 e1 = *reinterpret_cast<const __nv_bfloat162*>(&e.y);
+    const float4 v = make_float4(__low2float(e0), __high2float(e0), __low2float(e1), __high2float(e1));
+    *reinterpret_cast<float4*>(x + static_cast<int64_t>(r) * d + col) = v;
+    *reinterpret_cast<uint2*>(xb + static_cast<int64_t>(r) * d + col) = e;
+    float q = (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (lane == 0) ss[static_cast<int64_t>(c) * t_stride + r] = q;
+  }
+}
+
+__device__ __forceinline__ void set_draft_row(LmSlots sl, LmReqState rq, RowsDev rows, int r, int t, int tok) {
+  const int slot = rq.slot[r];
+  const int pos = sl.len[slot] - 1 + t;
+  rows.row_req[r] = r;
+  rows.row_pos[r] = pos;
+  rows.row_j[r] = t;
+  rows.req_first[r] = r;
+  rows.req_n[r] = 1;
+  rows.req_slot[r] = slot;
+  rows.req_pos0[r] = pos;
+  rows.row_tok[r] = tok;
+}
+
+// Draft step 0 (one warp per row): the step's rows + their embeddings (draft_prep + embed fused).
+__global__ void draft_begin_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, const __nv_bfloat16* emb,
+                                   int d, float* x, __nv_bfloat16* xb, float* ss) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *rows.n_rows = n_t;
+  if (r >= n_t) return;
+  const int slot = rq.slot[r];
+  const int tok = sl.tok[static_cast<int64_t>(slot) * sl.max_seq + sl.len[slot] - 1];
+  if (lane == 0) set_draft_row(sl, rq, rows, r, 0, tok);
+  embed_row_warp(emb, tok, r, d, n_t, x, xb, ss, lane);
+}
+
+// After draft step t (one warp per row): argmax_lowest over the LM head's per-tile partials ->
+// drafted[r][t]; rows that draft again get step t+1's row and embedding (argmax_reduce +
+// draft_post + draft_prep + embed fused into one launch).
+__global__ void draft_advance_kernel(LmSlots sl, LmReqState rq, RowsDev rows, const float2* __restrict__ amax,
+                                     int n_tiles, int n_t, int t, int n_next, const __nv_bfloat16* emb, int d,
+                                     float* x, __nv_bfloat16* xb, float* ss) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= n_t) return;
+  float bv = -3.402823466e38f;
+  int bi = 0x7fffffff;
+  for (int m = lane; m < n_tiles; m += 32) {
+    const float2 p = amax[static_cast<int64_t>(m) * n_t + r];
+    const int pi = __float_as_int(p.y);
+    if (p.x > bv || (p.x == bv && pi < bi)) {
+      bv = p.x;
+      bi = pi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) rq.drafted[r * kMS + t] = bi;
+  if (r < n_next) {  // rows are sorted by k' descending: the first n_next rows draft again
+    if (lane == 0) set_draft_row(sl, rq, rows, r, t + 1, bi);
+    embed_row_warp(emb, bi, r, d, n_next, x, xb, ss, lane);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n_next > 0) *rows.n_rows = n_next;
+}
+
 __global__ void draft_post_kernel(LmReqState rq, const int* argmax, int n_t, int t) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n_t) rq.drafted[r * kMS + t] = argmax[r];
@@ -347,6 +431,34 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 cudaError_t lm_draft_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int t, cudaStream_t s) {
   draft_prep_kernel<<<cdiv(n_t > 0 ? n_t : 1, 256), 256, 0, s>>>(sl, rq, rows, n_t, t);
   return cudaGetLastError();
+}
+namespace {
+template <class K, class... A>
+cudaError_t launch_pdl(K kern, int blocks, int threads, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // namespace
+
+cudaError_t lm_draft_begin(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, const __nv_bfloat16* emb, int d,
+                           float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s) {
+  const int n = n_t > 0 ? n_t : 1;
+  return launch_pdl(draft_begin_kernel, cdiv(n * 32, 256), 256, s, sl, rq, rows, n_t, emb, d, x, xb, ss);
+}
+cudaError_t lm_draft_advance(LmSlots sl, LmReqState rq, RowsDev rows, const float2* amax, int n_tiles, int n_t,
+                             int t, int n_next, const __nv_bfloat16* emb, int d, float* x, __nv_bfloat16* xb,
+                             float* ss, cudaStream_t s) {
+  if (n_t <= 0) return cudaSuccess;
+  return launch_pdl(draft_advance_kernel, cdiv(n_t * 32, 256), 256, s, sl, rq, rows, amax, n_tiles, n_t, t,
+                    n_next, emb, d, x, xb, ss);
 }
 cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s) {
   if (n_t <= 0) return cudaSuccess;

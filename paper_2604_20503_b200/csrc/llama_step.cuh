@@ -53,6 +53,14 @@ struct StepCtl {
 // draft step t: rows = sorted requests [0, n_t); row r = request r, 1 row each at position
 // len_r - 1 + t, input token = last committed (t == 0) or drafted[r][t-1].
 cudaError_t lm_draft_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int t, cudaStream_t s);
+// fused draft step control (one warp per row, PDL launches): step 0's rows + embeddings; and
+// after step t: argmax over the LM head's per-tile partials -> drafted[r][t], then step t+1's
+// rows + embeddings for the first n_next rows (argmax_reduce + draft_post + draft_prep + embed).
+cudaError_t lm_draft_begin(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, const __nv_bfloat16* emb, int d,
+                           float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s);
+cudaError_t lm_draft_advance(LmSlots sl, LmReqState rq, RowsDev rows, const float2* amax, int n_tiles, int n_t,
+                             int t, int n_next, const __nv_bfloat16* emb, int d, float* x, __nv_bfloat16* xb,
+                             float* ss, cudaStream_t s);
 // after draft step t: drafted[r][t] = argmax[r].
 cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s);
 // verify rows (whole verify or one overlap chunk): row tokens from ctx.back() / drafted.
