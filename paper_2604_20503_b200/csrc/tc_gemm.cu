@@ -484,6 +484,8 @@ GemmPlan gemm_plan_legacy(int n_out, int t, int k, int num_sms) {
 //  * wide outputs (LM heads, >= 120 weight tiles) at <= 128 rows: two weight tiles per rows tile
 //    (mc = 2), no split: 32000x2048 @128 rows 36.1 -> 29.3 us, 32000x768 @32 13.2 -> 11.4 us;
 //  * >= 512 rows and >= 64 tiles: mc = 4 at 128-row token tiles (11264x2048 @512: 52 -> 44 us);
+//    (the same-shape sweep's other wins at >= 256 rows did NOT survive in-stream: B=64 verify
+//    2.77 -> 3.57 ms, so they are not applied);
 //  * <= 32 rows and >= 40 tiles: no K split (6144x768 @32: 10.3 -> 5.7 us);
 //  * <= 8 tiles with K >= 3072: 8-way K split (768x3072 @32: 6.7 -> 5.4 us).
 // Per SM the TMA ingest saturates near 44 GB/s (tools/tma_probe.cu), which is why sharing one
