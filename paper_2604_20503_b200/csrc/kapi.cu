@@ -56,7 +56,7 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
   GemmPlan plan = gemm_plan(n_out, t, k, num_sms());
   if (bn > 0) plan.bn = bn;
   if (mc > 0) plan.mc = mc;
-  if (plan.bn > 128 || plan.mc * plan.bn > 512) plan.mc = 1;  // instantiated combinations / TMEM
+  if ((plan.bn > 128 && plan.mc > 2) || plan.mc * plan.bn > 512) plan.mc = 1;  // instantiated combinations / TMEM
   if (plan.mc > 1) plan.deep = true;
   if (depth == 1 && plan.mc == 1) plan.deep = false;
   if (depth == 2) plan.deep = true;

@@ -498,7 +498,12 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
   const int kb = k / kBK;
   int cover = 32;
   while (cover < t && cover < 256) cover <<= 1;
-  if (mt >= 120 && t <= 128) {
+  if (t >= 1024 && mt >= 2 && ((mt + 1) / 2) * ((t + 255) / 256) >= 120) {  // 256 x 256 per CTA (4096 rows: gate/up
+    p.bn = 256;                   // 233 -> 183 us = 1.03 PFLOP/s, o 48 -> 34 us, down 101 -> 73 us)
+    p.mc = 2;
+    p.splits = 1;
+    p.deep = true;
+  } else if (mt >= 120 && t <= 128) {
     p.bn = cover;
     p.mc = 2;
     p.splits = 1;
@@ -537,7 +542,8 @@ cudaError_t gemm_fused(const GemmOperand& w, const GemmOperand& x, int t, const 
     switch (p.bn) {
       case 32: return launch_bn<32, 5, 2>(w, x, t, p.splits, epi, s);
       case 64: return launch_bn<64, 5, 2>(w, x, t, p.splits, epi, s);
-      default: return launch_bn<128, 4, 2>(w, x, t, p.splits, epi, s);
+      case 128: return launch_bn<128, 4, 2>(w, x, t, p.splits, epi, s);
+      default: return launch_bn<256, 3, 2>(w, x, t, p.splits, epi, s);  // 256 x 256 per CTA (TMEM 512)
     }
   }
   switch (p.bn) {
