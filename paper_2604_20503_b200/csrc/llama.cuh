@@ -18,6 +18,7 @@
 //               per-request (first row, n rows); n_rows lives in device memory so early-exit
 //               compaction can shrink it without a host round trip.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -75,6 +76,9 @@ struct KvDev {
   const int* ptab;      // [slots][max_pages]
   int max_pages;
   int64_t layer_stride;  // elements per layer
+  // TMA view of the pool as [rows = layers*pages*n_kv*2*64][hd] with 64x64 boxes and the 128 B
+  // swizzle the attention kernel's shared-memory layout uses (hd 64 only; nullptr = cp.async)
+  const CUtensorMap* tma = nullptr;
 };
 
 // ------------------------------------------------------------------ launchers

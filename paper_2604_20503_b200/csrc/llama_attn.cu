@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "llama.cuh"
+#include "sm100.cuh"
 
 namespace faser {
 namespace {
@@ -74,7 +75,8 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 // MT = 16-row M tiles per CTA in GROUP mode (128 threads per tile): the tiles of one (request,
 // kv head) share every K/V page load instead of re-reading it per tile.
 template <int HD, bool ROWS, int MT = 1>
-__global__ void __launch_bounds__(128 * MT) attn_kernel(RowsDev rows, KvDev kv, int layer, int n_q, int n_kv,
+__global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ CUtensorMap kvmap, int use_tma,
+                                                        RowsDev rows, KvDev kv, int layer, int n_q, int n_kv,
                                                    const __nv_bfloat16* __restrict__ qbuf,
                                                    __nv_bfloat16* __restrict__ obuf, float* __restrict__ part_o,
                                                    float2* __restrict__ part_ml, int* __restrict__ counters,
@@ -84,8 +86,12 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(RowsDev rows, KvDev kv, 
   constexpr int kTileBytes = 64 * HD * 2;  // one K (or V) page
   constexpr int kKS = HD / 16;             // k-steps over head_dim
   constexpr int kDT = HD / 8;              // 8-wide dim tiles of O
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned: the TMA 128-byte swizzle atom (same XOR pattern as swz<64>)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int s_last;
+  __shared__ __align__(8) uint64_t full[kAttnStages<HD>];
+  const bool tma = HD == 64 && use_tma;
   // let the next (PDL-launched) GEMM start streaming its weights while attention runs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -146,9 +152,23 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(RowsDev rows, KvDev kv, 
   __shared__ int s_page[kMaxPagesPerCta];
   for (int i = threadIdx.x; i < t1 - t0 && i < kMaxPagesPerCta; i += NT)
     s_page[i] = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t0 + i];
+  if (tma && threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) sm100::mbar_init(&full[st], 1);
+    sm100::fence_mbar_init();
+  }
   __syncthreads();
+  const int64_t layer_rows = kv.layer_stride / HD;
   auto load_tile = [&](int t, int buf) {
     const int page = t - t0 < kMaxPagesPerCta ? s_page[t - t0] : kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t];
+    if (tma) {  // one thread, two 8 KB boxes (K, V) with the hardware swizzle
+      if (threadIdx.x == 0) {
+        const int row = static_cast<int>(layer * layer_rows + (static_cast<int64_t>(page) * n_kv + kvh) * 2 * 64);
+        sm100::mbar_arrive_expect_tx(&full[buf], 2 * kTileBytes);
+        sm100::tma_load_2d(smem + buf * 2 * kTileBytes, &kvmap, &full[buf], 0, row);
+        sm100::tma_load_2d(smem + buf * 2 * kTileBytes + kTileBytes, &kvmap, &full[buf], 0, row + 64);
+      }
+      return;
+    }
     const uint8_t* gk = reinterpret_cast<const uint8_t*>(kvl + (static_cast<int64_t>(page) * n_kv + kvh) * 2 * 64 * HD);
     const uint8_t* gv = gk + kTileBytes;
     uint8_t* sk = smem + buf * 2 * kTileBytes;
@@ -167,7 +187,10 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(RowsDev rows, KvDev kv, 
     cp_async_commit();
   }
   for (int t = t0; t < t1; ++t) {
-    cp_async_wait<kStages - 2>();
+    if (tma)
+      sm100::mbar_wait(&full[(t - t0) % kStages], ((t - t0) / kStages) & 1);
+    else
+      cp_async_wait<kStages - 2>();
     __syncthreads();  // tile t landed for everyone; tile t-1's buffer is free
     {
       const int nt = t + kStages - 1;
@@ -368,15 +391,21 @@ cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int
                    float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s) {
   constexpr int kTile = 64 * HD * 2;
   constexpr int kMerge = (4 * MT * 16 * HD + 128 * MT) * 4;
-  constexpr int kSmem = 2 * kAttnStages<HD> * kTile > kMerge ? 2 * kAttnStages<HD> * kTile : kMerge;
+  constexpr int kSmem = (2 * kAttnStages<HD> * kTile > kMerge ? 2 * kAttnStages<HD> * kTile : kMerge) + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_kernel<HD, ROWS, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
   dim3 grid(n_req, m.n_kv, blocks * n_split);
-  attn_kernel<HD, ROWS, MT><<<grid, 128 * MT, kSmem, s>>>(rows, kv, layer, m.n_q, m.n_kv, qbuf, obuf, part_o,
-                                                          part_ml, counters, n_split, rows_cap, blocks, scale_log2);
+  static CUtensorMap dummy{};
+  // TMA page loads (one thread, hardware swizzle) measured equal to the cp.async path on B200
+  // (config 3, B = 1/32/128): opt-in FASER_ATTN_TMA=1
+  static const bool want_tma = getenv("FASER_ATTN_TMA") && getenv("FASER_ATTN_TMA")[0] == '1';
+  const bool use_tma = want_tma && kv.tma != nullptr && HD == 64;
+  attn_kernel<HD, ROWS, MT><<<grid, 128 * MT, kSmem, s>>>(use_tma ? *kv.tma : dummy, use_tma ? 1 : 0, rows, kv, layer,
+                                                          m.n_q, m.n_kv, qbuf, obuf, part_o, part_ml, counters,
+                                                          n_split, rows_cap, blocks, scale_log2);
   return cudaGetLastError();
 }
 

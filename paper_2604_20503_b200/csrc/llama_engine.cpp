@@ -188,6 +188,10 @@ struct LmModel {
     kv_layer_stride = static_cast<int64_t>(n_pages) * s.n_kv * 2 * kPage * s.hd;
     kv.alloc(static_cast<size_t>(kv_layer_stride) * s.layers * 2);
     LCK(cudaMemsetAsync(kv.p, 0, kv.bytes, st));  // stale pages must be finite (masked P*V)
+    if (s.hd == 64) {  // TMA view of the pool for the attention kernel's page loads
+      const int64_t rows = kv_layer_stride * s.layers / s.hd;
+      kv_tma = rows < (int64_t(1) << 31) && make_operand(&kv_op, kv.p, static_cast<int>(rows), s.hd, 64) == cudaSuccess;
+    }
     // RoPE table (rotate-half), computed in double on the host; the oracle uses the same formula.
     const int half = s.hd / 2;
     std::vector<float> tab(static_cast<size_t>(max_pos) * half * 2);
@@ -202,12 +206,15 @@ struct LmModel {
     LCK(cudaMemcpyAsync(rope.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st));
     LCK(cudaStreamSynchronize(st));  // tab is a host temporary
   }
+  GemmOperand kv_op;
+  bool kv_tma = false;
   KvDev kvdev(const int* ptab, int max_pages) const {
     KvDev k;
     k.pool = kv.as<__nv_bfloat16>();
     k.ptab = ptab;
     k.max_pages = max_pages;
     k.layer_stride = kv_layer_stride;
+    k.tma = kv_tma ? &kv_op.map : nullptr;
     return k;
   }
 };
