@@ -192,7 +192,8 @@ def llama_trace(args, rank, world, local_rank):
                        f"{args.trace} s, 12 segments, k={args.k}, B_max={args.batch}/GPU",
                        "global_batch": args.batch * world, "requests": len(trace),
                        "parallelism": f"replicas x{world} (request-sharded trace)", "clock": "device time of the steps"},
-            "trace_rank0": m}), flush=True)
+            "trace_rank0": {k: v for k, v in m.items() if k != "summary"},
+            "summary_rank0": m["summary"].as_json()}), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 

@@ -28,6 +28,7 @@
 #include "oracle.h"
 #include "specsim/exitctl.hpp"
 #include "specsim/latmodel.hpp"
+#include "specsim/metrics.hpp"
 #include "specsim/overlap.hpp"
 #include "specsim/rng.hpp"
 #include "specsim/sdcore.hpp"
@@ -300,6 +301,73 @@ int specref_eval_latency(int32_t stage, double b, double s, double r, double* ou
     auto m = LatencyModel::default_ground_truth();
     const PiecewiseLatencyParams* ps[4] = {&m.draft, &m.target, &m.ee_check, &m.prune};
     *out = eval_latency(*ps[stage], b, s, r);
+  });
+}
+
+// ---- wire formats (workload.cpp:34-71, metrics.cpp:68-113): reference writers / parser, for the
+// product's byte-for-byte format tests
+int specref_write_trace(const char* path, int32_t n, const double* arrival_ms, const int32_t* in_len,
+                        const int32_t* out_len) {
+  return guard([&] {
+    std::vector<TraceRecord> recs(n);
+    for (int i = 0; i < n; ++i) recs[i] = {arrival_ms[i], in_len[i], out_len[i]};
+    write_trace(path, recs);
+  });
+}
+int specref_ingest_trace(const char* path, int32_t cap, double* arrival_ms, int32_t* in_len, int32_t* out_len,
+                         int32_t* n) {
+  return guard([&] {
+    auto recs = ingest_trace(path);
+    *n = static_cast<int32_t>(recs.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+      arrival_ms[i] = recs[i].arrival_ms;
+      in_len[i] = recs[i].input_len;
+      out_len[i] = recs[i].output_len;
+    }
+  });
+}
+// Summary (metrics.hpp:34-66): ints = {requests, finished, total_output_tokens, drafted,
+// submitted, accepted, wasted_draft_tokens, false_prunes, iterations, overlap_iterations},
+// dbls = {makespan, throughput, mean_lat, p50_lat, p99_lat, mean_tpot, global_tpot, draft_ms,
+// verify_ms, overhead_ms, verify_share, acceptance_ratio, layer_work, layer_work_full},
+// hist = spec_length_hist pairs (n_hist x 2); writes metrics JSONL (summary only) + CSV.
+int specref_write_summary(const char* jsonl_path, const char* csv_path, const char* mode, uint64_t seed,
+                          const int64_t* ints, const double* dbls, const int64_t* hist, int32_t n_hist,
+                          int32_t oracle_checked, int32_t oracle_ok) {
+  return guard([&] {
+    Metrics m;
+    MetricsSummary& s = m.summary;
+    s.mode = mode;
+    s.seed = seed;
+    s.requests = ints[0];
+    s.finished = ints[1];
+    s.total_output_tokens = ints[2];
+    s.drafted_tokens = ints[3];
+    s.submitted_tokens = ints[4];
+    s.accepted_tokens = ints[5];
+    s.wasted_draft_tokens = ints[6];
+    s.false_prunes = ints[7];
+    s.iterations = ints[8];
+    s.overlap_iterations = ints[9];
+    s.makespan_ms = dbls[0];
+    s.throughput_tok_s = dbls[1];
+    s.mean_request_latency_ms = dbls[2];
+    s.p50_request_latency_ms = dbls[3];
+    s.p99_request_latency_ms = dbls[4];
+    s.mean_tpot_ms = dbls[5];
+    s.global_tpot_ms = dbls[6];
+    s.draft_time_ms = dbls[7];
+    s.verify_time_ms = dbls[8];
+    s.overhead_time_ms = dbls[9];
+    s.verify_share = dbls[10];
+    s.acceptance_ratio = dbls[11];
+    s.layer_work = dbls[12];
+    s.layer_work_full = dbls[13];
+    for (int i = 0; i < n_hist; ++i) s.spec_length_hist.push_back({static_cast<int>(hist[2 * i]), hist[2 * i + 1]});
+    s.oracle_checked = oracle_checked != 0;
+    s.oracle_ok = oracle_ok != 0;
+    write_metrics_jsonl(m, jsonl_path);
+    write_summary_csv(s, csv_path);
   });
 }
 

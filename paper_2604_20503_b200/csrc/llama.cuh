@@ -23,12 +23,25 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "faser/engine.h"
 
 namespace faser {
 
 constexpr int kPage = 64;  // tokens per KV page
+
+// Cheap device-side range checks on data-dependent indices (token ids, page ids): a violation
+// prints the site and traps (a kernel error on the host) instead of corrupting memory.
+#define FASER_DCHECK(cond, ...)  \
+  do {                           \
+    if (!(cond)) {               \
+      printf(__VA_ARGS__);       \
+      __trap();                  \
+    }                            \
+  } while (0)
+constexpr unsigned kTokLimit = 1u << 20;   // > every vocabulary here
+constexpr unsigned kPageLimit = 1u << 24;
 
 struct LlamaShape {
   int d, layers, n_q, n_kv, hd, ffn, vocab;

@@ -150,8 +150,12 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   // page ids of this CTA's key range, fetched once (a global load per page would sit on the
   // critical path of every pipeline step)
   __shared__ int s_page[kMaxPagesPerCta];
-  for (int i = threadIdx.x; i < t1 - t0 && i < kMaxPagesPerCta; i += NT)
+  FASER_DCHECK(t1 <= kv.max_pages, "FASER check: attention req %d slot %d pages %d > %d (pos0 %d rows %d)\n", req,
+               slot, t1, kv.max_pages, pos0, nr);
+  for (int i = threadIdx.x; i < t1 - t0 && i < kMaxPagesPerCta; i += NT) {
     s_page[i] = kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t0 + i];
+    FASER_DCHECK(static_cast<unsigned>(s_page[i]) < kPageLimit, "FASER check: attention page %d\n", s_page[i]);
+  }
   if (tma && threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) sm100::mbar_init(&full[st], 1);
     sm100::fence_mbar_init();

@@ -1168,6 +1168,7 @@ class LlamaEngine {
       f.n_req = c.nreq;
       f.max_rows = c.maxrows;
       f.max_ctx = c.maxctx;
+      fs = stream;  // (fs may still name the verify lane of the previous overlapped step)
       forward(draft, wd, f);
       forward(target, wt, f);
     }
@@ -1252,9 +1253,9 @@ class LlamaEngine {
         for (int t = static_cast<int>(qi) * c; t < std::min(kmax, static_cast<int>(qi + 1) * c); ++t) draft_step(t);
         if (qi + 1 == chunks_v.size()) LCK(record_event(ev[1]));
         LCK(cudaEventRecord(ev_chunk[qi], stream));
-        LCK(cudaStreamWaitEvent(vstream, ev_chunk[qi], 0));
+        LCK(cudaStreamWaitEvent(vs, ev_chunk[qi], 0));
         const VChunk& vc = chunks_v[qi];
-        LCK(lm_verify_tokens(sl, q, vc.rows, vc.T, vstream));
+        LCK(lm_verify_tokens(sl, q, vc.rows, vc.T, vs));
         Fwd f;
         f.rows = vc.rows;
         f.T = vc.T;
@@ -1264,12 +1265,12 @@ class LlamaEngine {
         f.logits = true;
         f.argmax_out = rq.truth;
         f.kv_tokens = ctx_sum + vc.T;
-        fs = vstream;
+        fs = vs;
         forward(target, wt, f);
-        LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vstream));
+        LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vs));
         launches += 2;
       }
-      LCK(lm_verify_init(q, n, L, eos, vstream));
+      LCK(lm_verify_init(q, n, L, eos, vs));
       ++launches;
     } else {
       for (int t = 0; t < kmax; ++t) draft_step(t);

@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(128) embed_kernel(const __nv_bfloat16* __restr
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int r = blockIdx.x, c = blockIdx.y * 128 + threadIdx.x;
   if (r >= *rows.n_rows) return;
-  const __nv_bfloat16 e = emb[static_cast<int64_t>(rows.row_tok[r]) * d + c];
+  const int tok = rows.row_tok[r];
+  FASER_DCHECK(static_cast<unsigned>(tok) < kTokLimit, "FASER check: embed row %d token %d\n", r, tok);
+  const __nv_bfloat16 e = emb[static_cast<int64_t>(tok) * d + c];
   const float v = __bfloat162float(e);
   x[static_cast<int64_t>(r) * d + c] = v;
   xb[static_cast<int64_t>(r) * d + c] = e;

@@ -19,6 +19,7 @@
 #include <cstdint>
 
 #include "llama_step.cuh"
+#include "tc_gemm.cuh"
 
 namespace faser {
 namespace {
@@ -119,6 +120,8 @@ __global__ void draft_advance_kernel(LmSlots sl, LmReqState rq, RowsDev rows, co
       bi = oi;
     }
   }
+  FASER_DCHECK(static_cast<unsigned>(bi) < kTokLimit, "FASER check: draft_advance row %d t %d argmax %d (n_t %d)\n", r, t,
+               bi, n_t);
   if (lane == 0) rq.drafted[r * kMS + t] = bi;
   if (r < n_next) {  // rows are sorted by k' descending: the first n_next rows draft again
     if (lane == 0) set_draft_row(sl, rq, rows, r, t + 1, bi);
@@ -139,8 +142,11 @@ __global__ void verify_tokens_kernel(LmSlots sl, LmReqState rq, RowsDev rows, in
   if (i >= rows_cap || i >= *rows.n_rows) return;
   const int r = rows.row_req[i], j = rows.row_j[i];
   const int slot = rq.slot[r];
-  rows.row_tok[i] = j == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + sl.len[slot] - 1]
-                           : rq.drafted[r * kMS + j - 1];
+  const int tok = j == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + sl.len[slot] - 1]
+                         : rq.drafted[r * kMS + j - 1];
+  FASER_DCHECK(static_cast<unsigned>(tok) < kTokLimit, "FASER check: verify_tokens row %d req %d j %d slot %d token %d\n",
+               i, r, j, slot, tok);
+  rows.row_tok[i] = tok;
 }
 
 // Per-request verify state once every token is drafted: drafted length (EOS stop) and the
@@ -441,7 +447,7 @@ cudaError_t launch_pdl(K kern, int blocks, int threads, cudaStream_t s, A... arg
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);

@@ -202,6 +202,8 @@ __global__ void __launch_bounds__(128, 1)
         const int slot = ea.rows.req_slot[ea.rows.row_req[row]];
         s_pos[t] = pos;
         s_page[t] = ea.kv.ptab[static_cast<size_t>(slot) * ea.kv.max_pages + pos / kPage];
+        FASER_DCHECK(pos >= 0 && pos / kPage < ea.kv.max_pages && static_cast<unsigned>(s_page[t]) < kPageLimit,
+                     "FASER check: qkv epilogue row %d slot %d pos %d page %d\n", row, slot, pos, s_page[t]);
       }
     }
   }
@@ -400,14 +402,22 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
   attr[1].val.clusterDim.x = 1;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = z;
-  static const bool no_pdl = getenv("FASER_NO_PDL") != nullptr;
-  attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = z > 1 ? 2 : 1;  // cluster launch only when the K split needs DSMEM
   return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST, MC>, w.map, x.map, ea, w.rows, kb_total, kps, z);
 }
 
 }  // namespace
+
+namespace {
+thread_local bool t_pdl = true;
+}
+void set_pdl_enabled(bool on) { t_pdl = on; }
+bool pdl_enabled() {
+  static const bool no_pdl = getenv("FASER_NO_PDL") != nullptr;
+  return t_pdl && !no_pdl;
+}
 
 cudaError_t make_operand(GemmOperand* op, const void* base, int rows, int k, int box_rows) {
   EncodeTiledFn fn = encode_fn();

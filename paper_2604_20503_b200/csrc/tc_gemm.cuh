@@ -65,6 +65,11 @@ struct GemmPlan {
 };
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms);
 
+// Programmatic dependent launch for this host thread's subsequent launches (GEMMs and the fused
+// draft control kernels); on by default, FASER_NO_PDL=1 disables it process-wide.
+void set_pdl_enabled(bool on);
+bool pdl_enabled();
+
 // D[n][t] = sum_k W[n][k] X[t][k] over T = min(*n_rows, t) rows, epilogue per `epi`.
 // Launched with programmatic stream serialization: the prologue overlaps the previous kernel;
 // all dependent reads happen after griddepcontrol.wait.

@@ -90,27 +90,78 @@ def synth_trace(mean_rate_per_s=26.0, peak_to_valley=10.0, duration_ms=60000.0, 
     return [(float(a[j]), int(i[j]), int(o[j])) for j in range(cap)]
 
 
+class ModeController:
+    """Per-iteration decisions of one AblationMode (config.hpp:16) on top of the
+    engine: VSD = fixed k; VSD_AD = AdaptiveDrafter k_i (drafter.cpp:175-220); VSD_AD_EE = + the
+    Eq.10 gate (make_gate_plan, exitctl.cpp:70-82, r pinned at 0.5 since should_prune needs
+    r in (0,1)); FULL = + the overlap plan (plan_overlap, overlap.cpp:23-42). ``gate_layer`` > 0
+    replaces make_gate_plan by a fixed single gated layer; ``chunk`` > 0 forces the overlap chunk."""
+
+    def __init__(self, mode, num_layers, fixed_k=4, models=None, gate_layer=0, chunk=0):
+        from . import controller, engine
+        self.mode, self.L, self.k, self.models = mode, num_layers, fixed_k, models
+        self.gate_layer, self.chunk = gate_layer, chunk
+        self.engine = engine
+        self.drafter = controller.AdaptiveDrafter(models=models) if mode >= abi.MODE_VSD_AD else None
+        self.overlap_on = False
+
+    def plan(self, eng, live):
+        ks = self.drafter.assign_lengths(live, len(live), 1.0) if self.drafter else [self.k] * len(live)
+        eng.set_spec_lengths(live, ks)
+        if self.mode >= abi.MODE_VSD_AD_EE:
+            if self.gate_layer:
+                eng.set_gate(abi.GatePlan(self.gate_layer, self.gate_layer + 1, 1.0))
+            else:
+                eng.set_gate(self.engine.make_gate_plan(abi.ExitPolicy.default(), [(k, 0.6) for k in ks],
+                                                        float(len(ks)), 0.5, self.L, self.models))
+        self.overlap_on = False
+        if self.mode == abi.MODE_FULL:
+            if self.chunk:
+                eng.set_overlap(True, self.chunk)
+                self.overlap_on = self.chunk < max(ks)
+            else:
+                p = self.engine.plan_overlap(max(ks), len(ks), models=self.models)
+                eng.set_overlap(bool(p.enabled), max(p.chunk, 1), p.r)
+                self.overlap_on = bool(p.enabled) and p.chunk < max(ks)
+        return ks
+
+    def observe(self, res, b, step_ms):
+        if self.drafter:
+            self.drafter.observe_results(res, b, 1.0, max(step_ms, 1e-3))
+
+    def close(self):
+        if self.drafter:
+            self.drafter.close()
+
+
+MODE_NAMES = {abi.MODE_VSD: "VSD", abi.MODE_VSD_AD: "VSD_AD", abi.MODE_VSD_AD_EE: "VSD_AD_EE", abi.MODE_FULL: "FULL"}
+
+
 def run_trace(eng: ServingEngine, trace, vocab, prompt_seed=1, fixed_k=4, id_of=None, clock="device",
-              max_steps=0):
+              max_steps=0, controller=None, num_layers=0, seed=1):
     """Replay an arrival trace (the missing sim loop): requests are admitted at
     iteration boundaries once the serving clock has passed their arrival time (B_max =
     engine max_batch, FIFO), one step() per iteration, the clock advances by the step's device
     time (``clock="device"``, CUDA events on the engine stream) or host wall time ("wall"); an
     idle engine jumps to the next arrival. Prompts follow synth_prompt(prompt_seed, trace index).
+    ``controller`` (ModeController) makes the per-iteration mode decisions; default fixed k.
 
-    Returns per-request records and the MetricsSummary-style aggregates (metrics.hpp:34-66):
-    throughput (committed tokens / makespan), p50 TPOT (median over requests of
-    (t_last_commit - t_first_commit) / (n_out - 1)), mean TPOT reference-style
-    (mean latency_i / n_out_i), p50 / p99 request latency (arrival -> last commit)."""
+    Returns a dict with the headline numbers and ``summary`` = metrics.MetricsSummary
+    (metrics.hpp:34-66): throughput = committed tokens / makespan, p50 TPOT over requests of
+    (t_last_commit - t_first_commit) / (n_out - 1), mean TPOT reference-style (mean
+    latency_i / n_out_i), request latency arrival -> last commit."""
     import numpy as np
 
+    from . import metrics
     from .engine import synth_prompt
     ids = id_of or (lambda j: j)
     n = len(trace)
     t_clock = 0.0
     nxt = 0
-    arr, first, last, nout = {}, {}, {}, {}
+    arr, first, last, nout, fin = {}, {}, {}, {}, {}
     steps = 0
+    S = metrics.MetricsSummary(mode=MODE_NAMES.get(eng.cfg.mode, str(eng.cfg.mode)), seed=seed)
+    spec_hist, batch_hist = {}, {}
     t_wall0 = time.perf_counter()
     while nxt < n or eng.pending_work() > 0:
         while nxt < n and trace[nxt][0] <= t_clock:
@@ -126,17 +177,40 @@ def run_trace(eng: ServingEngine, trace, vocab, prompt_seed=1, fixed_k=4, id_of=
         if max_steps and steps >= max_steps:
             break
         live = eng.live_requests()
-        eng.set_spec_lengths(live, [fixed_k] * len(live))
+        if controller is not None:
+            ks = controller.plan(eng, live)
+        else:
+            ks = [fixed_k] * len(live)
+            eng.set_spec_lengths(live, ks)
         w0 = time.perf_counter()
         res = eng.step()
-        dt = eng.last_step_timing()[2] if clock == "device" else (time.perf_counter() - w0) * 1e3
+        d_ms, v_ms, s_ms = eng.last_step_timing()
+        dt = s_ms if clock == "device" else (time.perf_counter() - w0) * 1e3
+        if controller is not None:
+            controller.observe(res, len(live), s_ms)
+            S.overlap_iterations += int(controller.overlap_on)
         t_clock += dt
         steps += 1
+        S.draft_time_ms += d_ms
+        S.verify_time_ms += v_ms
+        S.overhead_time_ms += max(0.0, s_ms - d_ms - v_ms)
+        batch_hist[len(live)] = batch_hist.get(len(live), 0) + 1
+        for k in ks:
+            spec_hist[k] = spec_hist.get(k, 0) + 1
         for r in res:
+            S.drafted_tokens += r.drafted
+            S.submitted_tokens += r.outcome.submitted
+            S.accepted_tokens += r.outcome.accepted_count
+            S.wasted_draft_tokens += r.drafted - r.outcome.accepted_count
+            S.false_prunes += max(0, r.outcome.false_prune)
+            S.layer_work += r.outcome.full_layers_run
+            S.layer_work_full += num_layers * r.outcome.submitted
             if r.committed:
                 first.setdefault(r.req_id, t_clock)
                 last[r.req_id] = t_clock
                 nout[r.req_id] += r.committed
+            if r.done:
+                fin[r.req_id] = t_clock
     done = [rid for rid in arr if nout[rid] > 0]
     tokens = sum(nout.values())
     tpot = sorted((last[r] - first[r]) / (nout[r] - 1) for r in done if nout[r] >= 2)
@@ -144,10 +218,24 @@ def run_trace(eng: ServingEngine, trace, vocab, prompt_seed=1, fixed_k=4, id_of=
     t0 = min(arr.values()) if arr else 0.0
     makespan = (max(last.values()) - t0) if last else 0.0
     pct = lambda v, q: float(np.percentile(v, q)) if v else 0.0  # noqa: E731
+    S.requests, S.finished, S.total_output_tokens = len(arr), len(fin), tokens
+    S.makespan_ms = makespan
+    S.throughput_tok_s = tokens / (makespan / 1e3) if makespan > 0 else 0.0
+    S.mean_request_latency_ms = float(np.mean(lat)) if lat else 0.0
+    S.p50_request_latency_ms, S.p99_request_latency_ms = pct(lat, 50), pct(lat, 99)
+    S.mean_tpot_ms = float(np.mean([(last[r] - arr[r]) / nout[r] for r in done])) if done else 0.0
+    busy = S.draft_time_ms + S.verify_time_ms + S.overhead_time_ms
+    S.global_tpot_ms = busy / tokens if tokens else 0.0
+    dv = S.draft_time_ms + S.verify_time_ms
+    S.verify_share = S.verify_time_ms / dv if dv > 0 else 0.0
+    S.acceptance_ratio = S.accepted_tokens / S.submitted_tokens if S.submitted_tokens else 0.0
+    S.iterations = steps
+    S.spec_length_hist = sorted(spec_hist.items())
+    S.batch_size_hist = sorted(batch_hist.items())
     return {
         "requests": len(arr), "completed": len(done), "tokens": tokens, "steps": steps,
-        "makespan_ms": makespan, "throughput_tok_s": tokens / (makespan / 1e3) if makespan > 0 else 0.0,
-        "p50_tpot_ms": pct(tpot, 50), "mean_tpot_ms": float(np.mean([(last[r] - arr[r]) / nout[r] for r in done]))
-        if done else 0.0, "p50_latency_ms": pct(lat, 50), "p99_latency_ms": pct(lat, 99),
-        "wall_s": time.perf_counter() - t_wall0, "clock": clock,
+        "makespan_ms": makespan, "throughput_tok_s": S.throughput_tok_s,
+        "p50_tpot_ms": pct(tpot, 50), "mean_tpot_ms": S.mean_tpot_ms, "p50_latency_ms": S.p50_request_latency_ms,
+        "p99_latency_ms": S.p99_request_latency_ms, "wall_s": time.perf_counter() - t_wall0, "clock": clock,
+        "summary": S,
     }

@@ -37,3 +37,30 @@ def test_bursty_trace_replay_lossless():
                 assert (s[-1] - s[-2]) / (s[-1] - s[0]) <= LOGIT_TOL, (j, q)
     finally:
         tgt.close()
+
+
+def test_ablation_ladder_tiny(tmp_path):
+    """The four AblationModes on one trace through ModeController: every request finishes in
+    every mode, outputs are identical across modes (all lossless greedy), and the summary CSV
+    rows come out in the reference's order."""
+    from paper_2604_20503_b200 import metrics
+    desc = llama.tiny()
+    V, L = desc.target.vocab, desc.target.layers
+    trace = serving.synth_trace(mean_rate_per_s=300.0, peak_to_valley=4.0, duration_ms=50.0, steps=4,
+                                in_range=(4, 20), out_range=(4, 16), seed=2)
+    outs, sums = [], []
+    for mode in (abi.MODE_VSD, abi.MODE_VSD_AD, abi.MODE_VSD_AD_EE, abi.MODE_FULL):
+        with engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=64, mode=mode, default_spec_length=4,
+                                  max_spec_length=16, prefill_rows=512) as eng:  # AD draws k from S = {1..10}
+            ctl = serving.ModeController(mode, L, fixed_k=4, gate_layer=2 if mode >= abi.MODE_VSD_AD_EE else 0,
+                                         chunk=2 if mode == abi.MODE_FULL else 0)
+            m = serving.run_trace(eng, trace, V, controller=ctl, num_layers=L)
+            ctl.close()
+            outs.append([eng.committed(j) for j in range(len(trace))])
+        assert m["completed"] == len(trace) and m["summary"].finished == len(trace)
+        sums.append(m["summary"])
+    assert outs[1] == outs[0] and outs[2] == outs[0] and outs[3] == outs[0]
+    p = tmp_path / "ablate.csv"
+    metrics.write_summary_csv(p, sums)
+    rows = p.read_text().splitlines()
+    assert [r.split(",")[0] for r in rows[1:]] == ["VSD", "VSD_AD", "VSD_AD_EE", "FULL"]
