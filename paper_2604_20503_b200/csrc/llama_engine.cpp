@@ -690,8 +690,10 @@ class LlamaEngine {
     if (lm_head && T > w.lm_rows_cap) throw LFail{FASER_ECAPACITY, "LM-head rows exceed capacity"};
     const KvDev kv = m.kvdev(ptab.as<int>(), max_pages);
     const int qd = s.n_q * s.hd;
-    const GemmPlan p_qkv = plan(s.qkv_out(), T, s.d), p_o = plan(s.d, T, qd);
-    const GemmPlan p_gu = plan(2 * s.ffn, T, s.d), p_d = plan(s.d, T, s.ffn), p_lm = plan(s.vocab, T, s.d);
+    // prefill forwards (no logits) take the prefill plan
+    auto pl = [&](int n_out, int k) { return f.logits ? plan(n_out, T, k) : gemm_plan_prefill(n_out, T, k, nsm); };
+    const GemmPlan p_qkv = pl(s.qkv_out(), s.d), p_o = pl(s.d, qd);
+    const GemmPlan p_gu = pl(2 * s.ffn, s.d), p_d = pl(s.d, s.ffn), p_lm = plan(s.vocab, T, s.d);
     RowsDev rows = f.rows;
     EpiArgs base;
     base.t_stride = T;

@@ -64,6 +64,10 @@ struct GemmPlan {
   int mc = 1;        // 128-row weight tiles per CTA sharing one rows tile (1, 2, 4)
 };
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms);
+// Plan for a prefill forward (one or a few prompts, 128..8192 rows, no logits): 128-row token
+// tiles from 256 rows up (the same-shape sweep's winners, which did not survive in the verify
+// stream but are measured here on prefill separately).
+GemmPlan gemm_plan_prefill(int n_out, int t, int k, int num_sms);
 
 // Programmatic dependent launch for this host thread's subsequent launches (GEMMs and the fused
 // draft control kernels); on by default, FASER_NO_PDL=1 disables it process-wide.
