@@ -781,7 +781,8 @@ class LlamaEngine {
     // timing experiments only (FASER_SKIP bitmask, target verify forward): 1 attention, 2 qkv,
     // 4 o, 8 gate/up, 16 down — results are garbage, the step time shows each class's share
     static const int skip_env = getenv("FASER_SKIP") ? atoi(getenv("FASER_SKIP")) : 0;
-    const int skip = (f.logits && is_target) ? skip_env : 0;
+    // (bit 32: apply the mask to prefill forwards of both models instead)
+    const int skip = (skip_env & 32) ? (!f.logits ? (skip_env & 31) : 0) : ((f.logits && is_target) ? skip_env : 0);
     for (int l = 0; l < s.layers; ++l) {
       e_qkv.layer = l;
       if (!(skip & 2))
