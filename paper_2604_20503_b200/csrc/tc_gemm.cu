@@ -537,26 +537,29 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
 }
 
 GemmPlan gemm_plan_prefill(int n_out, int t, int k, int num_sms) {
+  // single-prompt prefill (256..1023 rows), from the 576-row sweep (profiles/r01_gemm_sweep_576rows.jsonl)
   static const bool off = getenv("FASER_PREFILL_PLAN") && getenv("FASER_PREFILL_PLAN")[0] == '0';
   GemmPlan p = gemm_plan(n_out, t, k, num_sms);
   if (off || t < 256 || t >= 1024) return p;
   const int mt = n_out / kBM;
   const int kb = k / kBK;
-  if (mt >= 64) {          // gate/up, LM-size: mc = 4 (11264x2048 @512: 52.6 -> 43.8 us)
-    p.bn = 128;
-    p.mc = 4;
-    p.splits = 1;
-  } else if (k >= 4096) {  // down: 128-row tiles, mc 2, 4-way split (26.1 -> 23.4 us)
-    p.bn = 128;
+  if (mt >= 64 && ((mt + 1) / 2) * ((t + 255) / 256) >= 100) {  // gate/up: 43.9 -> 34.6 us
+    p.bn = 256;
     p.mc = 2;
-    const int kps = (kb + 3) / 4;
-    p.splits = (kb + kps - 1) / kps;
-  } else if (mt >= 20) {   // qkv: one 128-row token tile per 64 (22.6 -> 17.9 us)
+    p.splits = 1;
+    p.deep = true;
+  } else if (mt >= 18 && k <= 2048) {  // qkv: 23.7 -> 18.6 us, draft qkv 13.5 -> 10.0 us
     p.bn = 128;
     p.mc = 1;
     p.splits = 1;
+    p.deep = true;
+  } else if (mt <= 8 && k >= 3072) {  // draft down: -> 11.8 us
+    p.bn = 128;
+    p.mc = 1;
+    const int kps = (kb + 3) / 4;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
   }
-  p.deep = true;
   return p;
 }
 

@@ -47,3 +47,23 @@ def test_gemm_matches_fp32(L, n_out, T, K, splits, mc):
 def test_gemm_rejects_bad_shapes(L):
     assert L.faser_k_gemm_bf16(C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), 100, 4, 64, 0, None) == 1
     assert L.faser_k_gemm_bf16(C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), 128, 4, 60, 0, None) == 1
+
+
+# the launch shapes the single-prompt prefill plan picks (gemm_plan_prefill, 256..1023 rows)
+@pytest.mark.parametrize("n_out,T,K,code,splits", [
+    (11264, 576, 2048, 20256, 1),   # gate/up: 256 x 256 per CTA
+    (2560, 576, 2048, 128, 1),      # qkv: one 128-row token tile
+    (768, 576, 3072, 128, 4),       # draft down: 4-way split
+    (2048, 300, 5632, 20256, 2),    # 256 x 256 with a split
+])
+def test_gemm_prefill_shapes_match_fp32(L, n_out, T, K, code, splits):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(n_out + T + K)
+    w = (torch.randn(n_out, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn(T, K, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.full((T, n_out), float("nan"), device="cuda", dtype=torch.float32)
+    assert L.faser_k_gemm_bf16_plan(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                                    n_out, T, K, code, splits, None) == 0
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().t()
+    assert (out - ref).abs().max().item() <= 1e-4 * max(ref.abs().max().item(), 1.0) + 1e-3

@@ -9,11 +9,11 @@ import gemm_stream  # noqa: E402
 shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
 for n, t, k in shapes:
     res = []
-    for bn in ((32, 64, 128) if t <= 512 else (128, 256)):
+    for bn in ((32, 64, 128) if t <= 512 and not os.environ.get('SWEEP_WIDE') else (64, 128, 256)):
         for mc in (1, 2, 4):
             if mc * bn > 512 or (n // 128) < mc:
                 continue
-            for sp in ((1, 2, 3, 4, 6, 8) if t <= 512 else (1, 2)):
+            for sp in ((1, 2, 3, 4, 6, 8) if t <= 512 else (1, 2, 4)):
                 if k // 64 // sp < 2:
                     continue
                 try:
