@@ -747,8 +747,6 @@ class LlamaEngine {
       const double wbytes = 2.0 * ((static_cast<double>(s.qkv_out()) * s.d + static_cast<double>(s.d) * qd +
                                     3.0 * s.ffn * s.d) * s.layers + static_cast<double>(s.vocab) * s.d);
       const double kvb = static_cast<double>(f.kv_tokens) * 2 * s.n_kv * s.hd * 2 * s.layers;
-      static const int mega_dbg = getenv("FASER_MEGA_DBG") ? atoi(getenv("FASER_MEGA_DBG")) : 0;
-      st.dbg = mega_dbg;
       MegaModelDev dv = mc.dev;
       static const int mega_minb = getenv("FASER_MEGA_MINB") ? atoi(getenv("FASER_MEGA_MINB")) : 4;
       dv.min_blocks = mega_minb;

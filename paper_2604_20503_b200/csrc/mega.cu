@@ -104,13 +104,6 @@ __device__ __forceinline__ void warp_wait(uint64_t* bar, uint32_t parity) {
     if (++n > (1ll << 28)) __trap();
   }
 }
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
-  long long n = 0;
-  while (!mbar_test(bar, parity)) {
-    if (++n > (1ll << 28)) __trap();
-  }
-}
-
 __device__ __forceinline__ int phase_kind(int p, int L, int* layer) {
   if (p == 0) {
     *layer = 0;
@@ -740,18 +733,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* st = ring + s * stage_bytes;
             const int nt = group_tiles(iw.g, iw.m);
             sm100::mbar_arrive_expect_tx(&full[s], nt * kWBytes + xbytes);  // the rows' tile lands later
-            for (int i = 0; i < nt; ++i) {
-              if (S.dbg == 3) {  // timing experiment: contiguous 16 KB bulk copies from a 131 MB region
-                const size_t nblk = static_cast<size_t>(M.vocab) * M.d * 2 / kWBytes;
-                const char* src = reinterpret_cast<const char*>(M.emb) +
-                                  ((static_cast<size_t>(iw.p * G + cta) * 97 + iw.b * 2 + i) % nblk) * kWBytes;
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             :: "r"(sm100::smem_u32(st + i * kWBytes)), "l"(src), "r"(kWBytes), "r"(sm100::smem_u32(&full[s])) : "memory");
-              } else {
+            for (int i = 0; i < nt; ++i)
               sm100::tma_load_2d_hint(st + i * kWBytes, &M.maps[iw.g.wmap], &full[s], iw.kk * 64,
                                       (iw.m * MC + i) * 128, pol_w);
-              }
-            }
             if (S.trace && cta == 0 && iw.p == 4 && iw.b - iw.b0 < 32) S.trace[(static_cast<size_t>(2 * P + 4)) * G + (iw.b - iw.b0) * 4 + 0] = gtimer();
           }
           __syncwarp();

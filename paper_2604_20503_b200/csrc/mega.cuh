@@ -58,8 +58,7 @@ struct MegaStep {
   float* att_part_o;
   float2* att_part_ml;
   int* att_counters;
-  unsigned long long* trace;
-  int dbg;  // debug: 1 = skip epilogue math, 2 = also skip MMAs  // optional [2][P][grid] globaltimer: phase done (workers), first X issue
+  unsigned long long* trace;  // optional (FASER_MEGA_TRACE): [2][P][grid] phase-end / first-rows-load globaltimer
 };
 
 // Number of phases and sync words for a model with `layers` layers.
