@@ -28,7 +28,9 @@
 #include "oracle.h"
 #include "specsim/exitctl.hpp"
 #include "specsim/latmodel.hpp"
+#ifdef SPECREF_METRICS
 #include "specsim/metrics.hpp"
+#endif
 #include "specsim/overlap.hpp"
 #include "specsim/rng.hpp"
 #include "specsim/sdcore.hpp"
@@ -326,6 +328,7 @@ int specref_ingest_trace(const char* path, int32_t cap, double* arrival_ms, int3
     }
   });
 }
+#ifdef SPECREF_METRICS
 // Summary (metrics.hpp:34-66): ints = {requests, finished, total_output_tokens, drafted,
 // submitted, accepted, wasted_draft_tokens, false_prunes, iterations, overlap_iterations},
 // dbls = {makespan, throughput, mean_lat, p50_lat, p99_lat, mean_tpot, global_tpot, draft_ms,
@@ -370,6 +373,8 @@ int specref_write_summary(const char* jsonl_path, const char* csv_path, const ch
     write_summary_csv(s, csv_path);
   });
 }
+
+#endif  // SPECREF_METRICS
 
 int specref_synth_prompt(uint64_t seed, int32_t index, int32_t len, int32_t vocab, int32_t* out) {
   return guard([&] {

@@ -493,7 +493,20 @@ class LlamaEngine {
     tsh = shape_of(m->target);
     eos = tsh.vocab - 1;
     LCK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    LCK(cudaStreamCreateWithFlags(&vstream, cudaStreamNonBlocking));
+    {
+      // verify lane priority (FASER_VERIFY_PRIO: 0 = same as the draft lane, 1 = verify first,
+      // 2 = draft first): decides whose CTAs the scheduler dispatches first when the two
+      // overlapped lanes both have work queued
+      int lo = 0, hi = 0;
+      LCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const int mode = getenv("FASER_VERIFY_PRIO") ? atoi(getenv("FASER_VERIFY_PRIO")) : 0;
+      if (mode == 2) {
+        LCK(cudaStreamDestroy(stream));
+        LCK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
+        fs = stream;
+      }
+      LCK(cudaStreamCreateWithPriority(&vstream, cudaStreamNonBlocking, mode == 1 ? hi : lo));
+    }
     fs = stream;
     for (auto& e : ev) LCK(cudaEventCreate(&e));
     for (auto& e : ev_chunk) LCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

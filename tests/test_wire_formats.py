@@ -80,6 +80,8 @@ def _random_summary(rng):
 
 @needs_ref
 def test_metrics_jsonl_and_summary_csv_bytes_match_reference(tmp_path):
+    if not hasattr(_ref(), "specref_write_summary"):
+        pytest.skip("oracle/_ref built without a json.hpp (metrics.cpp left out)")
     rng = random.Random(9)
     for trial in range(40):
         s = _random_summary(rng)
