@@ -79,7 +79,17 @@ def tp_tiny(target_bigram=None, draft_bigram=None, hard=None):
                  shape(256, 3, 16, 8, 64, 512, 1024, seed=42, bigram=tb, hard=hf))
 
 
-PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4, "cfg5": config5, "tp_tiny": tp_tiny}
+def tiny128(target_bigram=None, draft_bigram=None, hard=None):
+    """Small pair with the config-4/5 head geometry (head_dim 128, GQA 4, theta 5e5, tied-style
+    MHA draft with head_dim 64) for lossless parity tests of the hd-128 paths."""
+    tb = TARGET_BIGRAM["tiny"] if target_bigram is None else target_bigram
+    db = DRAFT_BIGRAM if draft_bigram is None else draft_bigram
+    hf = 0.0 if hard is None else hard
+    return _pair(shape(256, 2, 4, 4, 64, 512, 2048, seed=61, theta=500000.0, bigram=db),
+                 shape(512, 3, 8, 2, 128, 1024, 2048, seed=62, theta=500000.0, bigram=tb, hard=hf))
+
+
+PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4, "cfg5": config5, "tp_tiny": tp_tiny, "tiny128": tiny128}
 
 
 def fitted_latency_model(path=None):

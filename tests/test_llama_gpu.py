@@ -55,7 +55,7 @@ def check_rows_against_oracle(z_gpu, ref):
     return float(err.max())
 
 
-@pytest.mark.parametrize("preset", ["tiny", "cfg3"])
+@pytest.mark.parametrize("preset", ["tiny", "cfg3", "tiny128"])
 def test_weights_bitexact_with_oracle(preset):
     desc = llama.PRESETS[preset]()
     eng = make(desc, batch=2)
@@ -75,7 +75,7 @@ def test_weights_bitexact_with_oracle(preset):
     eng.close()
 
 
-@pytest.mark.parametrize("preset,nreq,k", [("tiny", 5, 4), ("tiny", 3, 7), ("cfg3", 3, 4)])
+@pytest.mark.parametrize("preset,nreq,k", [("tiny", 5, 4), ("tiny", 3, 7), ("cfg3", 3, 4), ("tiny128", 4, 5)])
 def test_verify_logits_and_integer_decisions(preset, nreq, k):
     """Per step: final verify logits vs the oracle; accepted / recovery / committed tokens
     recomputed from the GPU's own logits with the reference's rules (sdcore.cpp:61-81,182-197)
@@ -134,9 +134,11 @@ def test_verify_logits_and_integer_decisions(preset, nreq, k):
     eng.close()
 
 
-def test_lossless_tiny_to_completion():
-    """Every finished request equals greedy autoregressive decoding of the target (oracle)."""
-    desc = llama.tiny()
+@pytest.mark.parametrize("preset", ["tiny", "tiny128"])
+def test_lossless_tiny_to_completion(preset):
+    """Every finished request equals greedy autoregressive decoding of the target (oracle);
+    tiny128 runs the head_dim-128 / GQA-4 paths of configs 4-5."""
+    desc = llama.PRESETS[preset]()
     V = desc.target.vocab
     rng = np.random.default_rng(3)
     prompts = rand_prompts(V, 12, rng, 2, 80)
@@ -188,7 +190,7 @@ def test_oracle_sd_matches_engine_rounds_tiny():
     eng.close()
 
 
-@pytest.mark.parametrize("preset,lo,hi", [("tiny", 1, 4), ("cfg3", 8, 12)])
+@pytest.mark.parametrize("preset,lo,hi", [("tiny", 1, 4), ("cfg3", 8, 12), ("tiny128", 1, 3)])
 def test_early_exit_decisions_given_logits(preset, lo, hi):
     """verify_with_early_exit (sdcore.cpp:83-180) replayed on the GPU's captured gated-layer and
     final logits with the reference's token_exit_test / k_at must reproduce every pruning
