@@ -34,9 +34,9 @@ def make(desc, **kw):
                                 max_spec_length=8, prefill_rows=1024, **kw)
 
 
-@pytest.mark.parametrize("tp", [2, 4, 8])
-def test_tensor_parallel_verify_matches_unsharded(tp):
-    desc = llama.tp_tiny()
+@pytest.mark.parametrize("preset,tp", [("tp_tiny", 2), ("tp_tiny", 4), ("tp_tiny", 8), ("tiny128", 2)])
+def test_tensor_parallel_verify_matches_unsharded(preset, tp):
+    desc = llama.PRESETS[preset]()
     V = desc.target.vocab
     rng = np.random.default_rng(tp)
     prompts = [rng.integers(0, V - 1, size=int(rng.integers(3, 40))).tolist() for _ in range(7)]
