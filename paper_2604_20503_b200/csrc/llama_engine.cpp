@@ -1209,6 +1209,9 @@ class LlamaEngine {
     // fused draft control (one launch between draft forwards) unless the persistent forward,
     // which embeds and reduces the argmax itself, is on
     const bool fuse_draft = !mega_on && !(getenv("FASER_UNFUSED_DRAFT") && getenv("FASER_UNFUSED_DRAFT")[0] == '1');
+    // verify: tokens + embedding in one launch, argmax + truth scatter in one launch (not under
+    // TP, whose argmax is the all-gathered merge, nor with the persistent forward)
+    const bool fuse_verify = fuse_draft && tp == 1;
     auto rows_at = [&](int t) {
       int c = 0;
       while (c < n && ents[c].k > t) ++c;
@@ -1269,8 +1272,14 @@ class LlamaEngine {
         LCK(cudaEventRecord(ev_chunk[qi], stream));
         LCK(cudaStreamWaitEvent(vs, ev_chunk[qi], 0));
         const VChunk& vc = chunks_v[qi];
-        LCK(lm_verify_tokens(sl, q, vc.rows, vc.T, vs));
         Fwd f;
+        if (fuse_verify) {
+          LCK(lm_verify_begin(sl, q, vc.rows, vc.T, target.emb, tsh.d, wt.x.as<float>(), wt.xb.as<__nv_bfloat16>(),
+                              wt.ss.as<float>(), vs));
+          f.pre_embedded = f.skip_argmax = true;
+        } else {
+          LCK(lm_verify_tokens(sl, q, vc.rows, vc.T, vs));
+        }
         f.rows = vc.rows;
         f.T = vc.T;
         f.n_req = n;
@@ -1281,7 +1290,10 @@ class LlamaEngine {
         f.kv_tokens = ctx_sum + vc.T;
         fs = vs;
         forward(target, wt, f);
-        LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vs));
+        if (fuse_verify)
+          LCK(lm_verify_argmax(vc.rows, target.sh.vocab / 128, vc.T, wt.amax.as<float2>(), rq.truth, rq.truth_rj, vs));
+        else
+          LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vs));
         launches += 2;
       }
       LCK(lm_verify_init(q, n, L, eos, vs));
@@ -1291,8 +1303,14 @@ class LlamaEngine {
       LCK(record_event(ev[1]));
       // ---- verify (+ early exit)
       LCK(lm_verify_init(q, n, L, eos, stream));
-      LCK(lm_verify_tokens(sl, q, vrows, total, stream));
       Fwd f;
+      if (fuse_verify) {
+        LCK(lm_verify_begin(sl, q, vrows, total, target.emb, tsh.d, wt.x.as<float>(), wt.xb.as<__nv_bfloat16>(),
+                            wt.ss.as<float>(), stream));
+        f.pre_embedded = f.skip_argmax = true;
+      } else {
+        LCK(lm_verify_tokens(sl, q, vrows, total, stream));
+      }
       f.rows = vrows;
       f.T = total;
       f.n_req = n;
@@ -1308,7 +1326,10 @@ class LlamaEngine {
       f.capture = capture;
       fs = stream;
       forward(target, wt, f);
-      LCK(lm_truth_scatter(vrows, rq.truth, rq.truth_rj, total, stream));
+      if (fuse_verify)
+        LCK(lm_verify_argmax(vrows, target.sh.vocab / 128, total, wt.amax.as<float2>(), rq.truth, rq.truth_rj, stream));
+      else
+        LCK(lm_truth_scatter(vrows, rq.truth, rq.truth_rj, total, stream));
       launches += 3;
     }
     StepCtl ctl{n, L, eos, (ee && chunks_v.empty()) ? 1 : 0, cfg.exempt_rule};

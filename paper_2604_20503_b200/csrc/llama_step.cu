@@ -130,6 +130,55 @@ __global__ void draft_advance_kernel(LmSlots sl, LmReqState rq, RowsDev rows, co
   if (blockIdx.x == 0 && threadIdx.x == 0 && n_next > 0) *rows.n_rows = n_next;
 }
 
+// Verify rows' input tokens + their embeddings, one warp per row (verify_tokens + embed fused).
+__global__ void verify_begin_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, const __nv_bfloat16* emb,
+                                    int d, float* x, __nv_bfloat16* xb, float* ss) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= rows_cap || i >= *rows.n_rows) return;
+  const int r = rows.row_req[i], j = rows.row_j[i];
+  const int slot = rq.slot[r];
+  const int tok = j == 0 ? sl.tok[static_cast<int64_t>(slot) * sl.max_seq + sl.len[slot] - 1]
+                         : rq.drafted[r * kMS + j - 1];
+  FASER_DCHECK(static_cast<unsigned>(tok) < kTokLimit, "FASER check: verify_begin row %d req %d j %d slot %d token %d\n",
+               i, r, j, slot, tok);
+  if (lane == 0) rows.row_tok[i] = tok;
+  embed_row_warp(emb, tok, i, d, rows_cap, x, xb, ss, lane);
+}
+
+// Final argmax_lowest per verify row over the LM head's per-tile partials, written both per row
+// and per (request, drafted position) (argmax_reduce + truth_scatter fused), one warp per row.
+__global__ void verify_argmax_kernel(RowsDev rows, int n_tiles, int t_stride, const float2* __restrict__ amax,
+                                     int* __restrict__ truth, int* __restrict__ truth_rj) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= t_stride || i >= *rows.n_rows) return;
+  float bv = -3.402823466e38f;
+  int bi = 0x7fffffff;
+  for (int m = lane; m < n_tiles; m += 32) {
+    const float2 p = amax[static_cast<int64_t>(m) * t_stride + i];
+    const int pi = __float_as_int(p.y);
+    if (p.x > bv || (p.x == bv && pi < bi)) {
+      bv = p.x;
+      bi = pi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    truth[i] = bi;
+    truth_rj[rows.row_req[i] * kMS + rows.row_j[i]] = bi;
+  }
+}
+
 __global__ void draft_post_kernel(LmReqState rq, const int* argmax, int n_t, int t) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n_t) rq.drafted[r * kMS + t] = argmax[r];
@@ -465,6 +514,17 @@ cudaError_t lm_draft_advance(LmSlots sl, LmReqState rq, RowsDev rows, const floa
   if (n_t <= 0) return cudaSuccess;
   return launch_pdl(draft_advance_kernel, cdiv(n_t * 32, 256), 256, s, sl, rq, rows, amax, n_tiles, n_t, t,
                     n_next, emb, d, x, xb, ss);
+}
+cudaError_t lm_verify_begin(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, const __nv_bfloat16* emb, int d,
+                            float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  return launch_pdl(verify_begin_kernel, cdiv(rows_cap * 32, 256), 256, s, sl, rq, rows, rows_cap, emb, d, x, xb, ss);
+}
+cudaError_t lm_verify_argmax(RowsDev rows, int n_tiles, int rows_cap, const float2* amax, int* truth, int* truth_rj,
+                             cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  return launch_pdl(verify_argmax_kernel, cdiv(rows_cap * 32, 256), 256, s, rows, n_tiles, rows_cap, amax, truth,
+                    truth_rj);
 }
 cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s) {
   if (n_t <= 0) return cudaSuccess;

@@ -61,6 +61,12 @@ cudaError_t lm_draft_begin(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, con
 cudaError_t lm_draft_advance(LmSlots sl, LmReqState rq, RowsDev rows, const float2* amax, int n_tiles, int n_t,
                              int t, int n_next, const __nv_bfloat16* emb, int d, float* x, __nv_bfloat16* xb,
                              float* ss, cudaStream_t s);
+// verify rows' tokens + embeddings (verify_tokens + embed fused; one warp per row)
+cudaError_t lm_verify_begin(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, const __nv_bfloat16* emb, int d,
+                            float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s);
+// final per-row argmax of the verify LM head -> truth[row] and truth_rj[req][j] (fused scatter)
+cudaError_t lm_verify_argmax(RowsDev rows, int n_tiles, int rows_cap, const float2* amax, int* truth, int* truth_rj,
+                             cudaStream_t s);
 // after draft step t: drafted[r][t] = argmax[r].
 cudaError_t lm_draft_post(LmReqState rq, const int* argmax, int n_t, int t, cudaStream_t s);
 // verify rows (whole verify or one overlap chunk): row tokens from ctx.back() / drafted.
