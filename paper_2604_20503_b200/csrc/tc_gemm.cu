@@ -500,9 +500,34 @@ GemmPlan gemm_plan_legacy(int n_out, int t, int k, int num_sms) {
 //  * <= 8 tiles with K >= 3072: 8-way K split (768x3072 @32: 6.7 -> 5.4 us).
 // Per SM the TMA ingest saturates near 44 GB/s (tools/tma_probe.cu), which is why sharing one
 // rows tile across weight tiles pays once the rows tile is comparable to a weight block.
+// Experiment hook: FASER_PLAN_OVERRIDE="n_out,k,t_lo,t_hi,bn,mc,splits;..." forces a plan for
+// matching launches (in-stream A/B of plans without rebuilding).
+static bool plan_override(int n_out, int t, int k, GemmPlan* p) {
+  static const char* env = getenv("FASER_PLAN_OVERRIDE");
+  if (!env) return false;
+  const char* c = env;
+  while (*c) {
+    int v[7] = {0, 0, 0, 0, 0, 0, 0}, used = 0;
+    if (sscanf(c, "%d,%d,%d,%d,%d,%d,%d%n", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &used) != 7) return false;
+    if (v[0] == n_out && v[1] == k && t >= v[2] && t <= v[3]) {
+      const int kb = k / kBK, s1 = v[6] < 1 ? 1 : (v[6] > 8 ? 8 : v[6]);
+      const int kps = (kb + s1 - 1) / s1;
+      p->bn = v[4];
+      p->mc = v[5];
+      p->splits = (kb + kps - 1) / kps;
+      p->deep = true;
+      return true;
+    }
+    c += used;
+    while (*c == ';' || *c == ' ') ++c;
+  }
+  return false;
+}
+
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
   static const bool legacy = getenv("FASER_GEMM_PLAN") && std::string(getenv("FASER_GEMM_PLAN")) == "legacy";
   GemmPlan p = gemm_plan_legacy(n_out, t, k, num_sms);
+  if (plan_override(n_out, t, k, &p)) return p;
   if (legacy) return p;
   const int mt = n_out / kBM;
   const int kb = k / kBK;
