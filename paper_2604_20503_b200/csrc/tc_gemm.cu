@@ -538,9 +538,22 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 2;
     p.splits = 1;
     p.deep = true;
-  } else if (mt >= 120 && t <= 128) {
+  } else if (mt >= 200 && t <= 128) {  // LM heads (and config 4's 28672-row gate/up)
     p.bn = cover;
-    p.mc = 2;
+    p.mc = mt >= 512 ? 4 : 2;            // 128256x2048 @32 rows: mc 4 88.4 vs 95.2 us
+    p.splits = 1;
+    p.deep = true;
+  } else if (t > 64 && t <= 128 && k >= 4096 && n_out >= 4096 && mt <= 32) {
+    // config-4 o / down (4096 x 4096, 4096 x 14336) at 128 rows: one 128-row token tile, 4-way K
+    // split (in-stream, config 4 B=32: step 12.03 -> 11.29 ms for down alone)
+    p.bn = 128;
+    p.mc = 1;
+    const int kps = (kb + 3) / 4;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
+  } else if (t > 64 && t <= 128 && k >= 4096 && mt >= 40 && mt <= 64) {  // config-4 qkv (6144 x 4096)
+    p.bn = 64;
+    p.mc = 1;
     p.splits = 1;
     p.deep = true;
   } else if (t >= 512 && mt >= 64) {

@@ -55,6 +55,10 @@ def test_gemm_rejects_bad_shapes(L):
     (2560, 576, 2048, 128, 1),      # qkv: one 128-row token tile
     (768, 576, 3072, 128, 4),       # draft down: 4-way split
     (2048, 300, 5632, 20256, 2),    # 256 x 256 with a split
+    (4096, 128, 14336, 128, 4),     # config-4 down at 128 rows
+    (6144, 128, 4096, 64, 1),       # config-4 qkv
+    (128256, 32, 2048, 40032, 1),   # config-4 draft LM head: 4 weight tiles per rows tile
+    (28672, 128, 4096, 20128, 1),   # config-4 gate/up
 ])
 def test_gemm_prefill_shapes_match_fp32(L, n_out, T, K, code, splits):
     import torch
