@@ -551,6 +551,27 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     const int kps = (kb + 3) / 4;
     p.splits = (kb + kps - 1) / kps;
     p.deep = true;
+  } else if (t > 128 && t <= 256 && k >= 4096 && (mt >= 200 || (mt >= 40 && mt <= 64) || (n_out >= 4096 && mt <= 32 && k >= 8192))) {
+    // config-4 shapes at 129..256 rows (in-stream, config 4 B=64: step 15.63 -> 14.55 ms):
+    // gate/up 128-row tiles x 4 weight tiles, qkv one 128-row tile, down 128 x 2 tiles + 4-way split
+    p.bn = 128;
+    p.mc = mt >= 200 ? 4 : (mt <= 32 ? 2 : 1);
+    const int sp = mt <= 32 ? 4 : 1;
+    const int kps = (kb + sp - 1) / sp;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
+  } else if (t <= 64 && k >= 8192 && mt <= 16) {  // config-4 draft down (2048 x 8192): 6-way split
+    p.bn = t <= 32 ? 32 : 64;
+    p.mc = 1;
+    const int kps = (kb + 5) / 6;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
+  } else if (t > 32 && t <= 64 && k == 2048 && mt >= 24 && mt <= 32) {  // config-4 draft qkv (3072 x 2048)
+    p.bn = 64;
+    p.mc = 1;
+    const int kps = (kb + 3) / 4;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
   } else if (t > 64 && t <= 128 && k >= 4096 && mt >= 40 && mt <= 64) {  // config-4 qkv (6144 x 4096)
     p.bn = 64;
     p.mc = 1;
