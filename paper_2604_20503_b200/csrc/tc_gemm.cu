@@ -6,14 +6,16 @@
 // "Swap-AB": the weights fill the 128-wide UMMA M dimension and the verify/draft rows are the
 // N dimension, so a batch of T = 1..256 rows is one N tile and the weights stream from HBM
 // exactly once. Roles in a 128-thread CTA:
-//   warp 0 / lane 0 : TMA producer (W tile 128x64, X tile BNx64 per stage, SWIZZLE_128B)
+//   warp 0          : TMA producers, one lane group per pipeline stage (W tiles 128x64 x MC,
+//                     X tile BNx64 per stage, SWIZZLE_128B)
 //   warp 1 / lane 0 : tcgen05.mma issuer (UMMA 128xBNx16), commits free smem stages
 //   warp 2          : TMEM allocator
+//   warps 2-3       : per-token prologue (RMSNorm scale, positions, KV pages) during the mainloop
 //   warps 0-3       : epilogue
-// K is split over gridDim.z so small-T launches cover all SMs. Every split CTA writes its fp32
-// partial tile; the LAST CTA to arrive on the tile's counter sums the partials in split order
-// (deterministic, independent of which rows survive early-exit pruning because the split count
-// is fixed per forward) and runs the fused epilogue from a shared-memory copy of the tile:
+// K is split over gridDim.z so small-T launches cover all SMs; the split CTAs of a tile are one
+// thread-block cluster and reduce their fp32 partials through DSMEM in rank order (deterministic,
+// independent of which rows survive early-exit pruning because the split count is fixed per
+// forward), each CTA then runs the fused epilogue on its slice of the tile's tokens:
 //   store | residual add (+ per-tile sum of squares for the next RMSNorm) | RoPE + q write +
 //   paged KV append | SwiGLU | logits (+ per-tile argmax).
 // RMSNorm is folded: the GEMM consumes the un-normalised residual (bf16) and scales each token
@@ -79,7 +81,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 template <int BN, int ST, int MC>
 __global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                const __grid_constant__ EpiArgs ea, int n_out, int kb_total, int kb_per_split, int splits) {
+                const __grid_constant__ EpiArgs ea, int n_out, int kb_total, int kb_per_split, int splits,
+                int issue) {
   using C = Cfg<BN, ST, MC>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -118,21 +121,33 @@ __global__ void __launch_bounds__(128, 1)
   pdl_trigger();
   // Weights do not depend on the previous kernel: stream the first stages of this CTA's weight
   // slice now, overlapping the previous kernel's tail (programmatic dependent launch).
+  //
+  // TMA issue is spread over the producer warp: B200's TMA serves the box requests of one issuing
+  // thread one after another (tools/tma_probe.cu: one thread ~40 GB/s per SM, four threads
+  // ~105-160 GB/s). `issue` = ngrp * 100 + gsz: ngrp lane groups (1, or one per stage: a stage is
+  // only ever filled by one group, so the empty/full parity protocol is the single-producer one),
+  // gsz lanes per group splitting the stage's boxes. The group's leader (g == 0) owns the stage's
+  // mbarrier accounting (expect_tx for all of the stage's bytes, before its own arrive); the other
+  // lanes only issue boxes, whose complete_tx may land before the leader's expect_tx (tx-count may
+  // go transiently negative; the phase cannot complete before the arrive).
+  const int ngrp = issue / 100, gsz = issue % 100;
+  const int pst = lane / gsz, pg = lane % gsz;  // lane group (first stage) and box slot of this lane
+  const bool producer = warp == 0 && pst < ngrp;
   const int npre = nkb < C::kStages ? nkb : C::kStages;
   const uint64_t pol_w = sm100::policy_evict_first();
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < npre; ++i) {
-      sm100::mbar_expect_tx(&full[i], ntile * kABytes);
-      for (int j = 0; j < ntile; ++j)
+  if (producer) {
+    for (int i = pst; i < npre; i += ngrp) {
+      if (pg == 0) sm100::mbar_expect_tx(&full[i], ntile * kABytes);
+      for (int j = pg; j < ntile; j += gsz)
         sm100::tma_load_2d_hint(sA + i * C::kAStage + j * kABytes, &tmW, &full[i], (kb0 + i) * kBK, mb + j * kBM, pol_w);
     }
   }
   pdl_wait();  // everything below may read the previous kernel's output
   const int T = ea.n_rows ? min(*ea.n_rows, ea.t_stride) : ea.t_stride;
   if (n0 >= T) {  // uniform per CTA: tile entirely past the live rows (early-exit compaction)
-    if (warp == 0 && lane == 0) {  // drain the prefetched weight tiles before exiting
-      for (int i = 0; i < npre; ++i) sm100::mbar_arrive(&full[i]);
-      for (int i = 0; i < npre; ++i) sm100::mbar_wait(&full[i], 0);
+    if (producer && pg == 0) {  // drain the prefetched weight tiles before exiting
+      for (int i = pst; i < npre; i += ngrp) sm100::mbar_arrive(&full[i]);
+      for (int i = pst; i < npre; i += ngrp) sm100::mbar_wait(&full[i], 0);
     }
     return;
   }
@@ -142,24 +157,26 @@ __global__ void __launch_bounds__(128, 1)
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------------------------------------------------------- TMA producer
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producers (one lane group per stage)
     const int xboxes = (min(BN, T - n0) + kXBox - 1) / kXBox;  // skip all-padding activation boxes
     const uint32_t xbytes = xboxes * kXBox * kBK * 2;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::kStages;
-      const uint32_t ph = (i / C::kStages) & 1;
-      const int kc = (kb0 + i) * kBK;
-      if (i < npre) {  // weight tiles already in flight: add the activation tile and arrive
-        sm100::mbar_arrive_expect_tx(&full[s], xbytes);
-      } else {
-        sm100::mbar_wait(&empty[s], ph ^ 1);
-        sm100::mbar_arrive_expect_tx(&full[s], ntile * kABytes + xbytes);
-        for (int j = 0; j < ntile; ++j)
-          sm100::tma_load_2d_hint(sA + s * C::kAStage + j * kABytes, &tmW, &full[s], kc, mb + j * kBM, pol_w);
+    if (producer) {
+      for (int i = pst; i < nkb; i += ngrp) {
+        const int s = i % C::kStages;
+        const uint32_t ph = (i / C::kStages) & 1;
+        const int kc = (kb0 + i) * kBK;
+        const bool pre = i < npre;  // weight tiles already in flight from the prologue
+        if (!pre) sm100::mbar_wait(&empty[s], ph ^ 1);
+        if (pg == 0) sm100::mbar_arrive_expect_tx(&full[s], (pre ? 0 : ntile * kABytes) + xbytes);
+        const int nw = pre ? 0 : ntile;  // boxes of this stage: nw weight boxes, then xboxes rows boxes
+        for (int b = pg; b < nw + xboxes; b += gsz) {
+          if (b < nw)
+            sm100::tma_load_2d_hint(sA + s * C::kAStage + b * kABytes, &tmW, &full[s], kc, mb + b * kBM, pol_w);
+          else
+            sm100::tma_load_2d(sB + s * C::kBBytes + (b - nw) * kXBox * 128, &tmX, &full[s], kc, n0 + (b - nw) * kXBox);
+        }
       }
-      for (int j = 0; j < xboxes; ++j)
-        sm100::tma_load_2d(sB + s * C::kBBytes + j * kXBox * 128, &tmX, &full[s], kc, n0 + j * kXBox);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------------------------------------------------------- MMA issuer
@@ -405,7 +422,18 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = z > 1 ? 2 : 1;  // cluster launch only when the K split needs DSMEM
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST, MC>, w.map, x.map, ea, w.rows, kb_total, kps, z);
+  // TMA issue layout (FASER_TMA_ISSUE: 0 = one lane, 1 = a lane group per stage (default),
+  // 2 = one lane per stage, 3 = one group of lanes splitting every stage's boxes; measured on B200
+  // in profiles/r01_tma_issue_ab.txt: 1 is fastest; a warp-uniform variant of 1 (every lane waiting
+  // each stage's release in ring order) was slower still and is not kept)
+  static const int mode = [] {
+    const char* e = std::getenv("FASER_TMA_ISSUE");
+    return e ? std::atoi(e) : 1;
+  }();
+  const int boxes = MC + BN / kXBox;
+  const int issue = mode == 0 ? 101 : mode == 2 ? ST * 100 + 1 : mode == 3 ? 100 + (boxes < 32 ? boxes : 32)
+                                                                        : ST * 100 + 32 / ST;
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST, MC>, w.map, x.map, ea, w.rows, kb_total, kps, z, issue);
 }
 
 }  // namespace
