@@ -74,7 +74,11 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 
 // MT = 16-row M tiles per CTA in GROUP mode (128 threads per tile): the tiles of one (request,
 // kv head) share every K/V page load instead of re-reading it per tile.
-template <int HD, bool ROWS, int MT = 1>
+// PPS = pages per pipeline step. PPS = 2 (GROUP mode): each of a tile's 4 warps takes 32
+// consecutive keys of a 128-key step, two 16-key chunks under one online-softmax update. That
+// halves the rescale / max-reduce / barrier steps per key against PPS = 1 (one 16-key chunk per
+// warp per 64-key page).
+template <int HD, bool ROWS, int MT = 1, int PPS = 1>
 __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ CUtensorMap kvmap, int use_tma,
                                                         RowsDev rows, KvDev kv, int layer, int n_q, int n_kv,
                                                    const __nv_bfloat16* __restrict__ qbuf,
@@ -84,6 +88,8 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   constexpr int kStages = kAttnStages<HD>;
   constexpr int kChunks = HD / 8;          // 16-byte chunks per K/V row
   constexpr int kTileBytes = 64 * HD * 2;  // one K (or V) page
+  constexpr int kStageBytes = PPS * 2 * kTileBytes;
+  static_assert(PPS == 1 || (PPS == 2 && !ROWS), "two-page steps are a GROUP-mode layout");
   constexpr int kKS = HD / 16;             // k-steps over head_dim
   constexpr int kDT = HD / 8;              // 8-wide dim tiles of O
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -91,7 +97,7 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int s_last;
   __shared__ __align__(8) uint64_t full[kAttnStages<HD>];
-  const bool tma = HD == 64 && use_tma;
+  const bool tma = HD == 64 && use_tma && PPS == 1;
   // let the next (PDL-launched) GEMM start streaming its weights while attention runs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   }
   __syncthreads();
   const int64_t layer_rows = kv.layer_stride / HD;
-  auto load_tile = [&](int t, int buf) {
+  auto load_tile = [&](int t, int buf, int h) {
     const int page = t - t0 < kMaxPagesPerCta ? s_page[t - t0] : kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t];
     if (tma) {  // one thread, two 8 KB boxes (K, V) with the hardware swizzle
       if (threadIdx.x == 0) {
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
     }
     const uint8_t* gk = reinterpret_cast<const uint8_t*>(kvl + (static_cast<int64_t>(page) * n_kv + kvh) * 2 * 64 * HD);
     const uint8_t* gv = gk + kTileBytes;
-    uint8_t* sk = smem + buf * 2 * kTileBytes;
+    uint8_t* sk = smem + buf * kStageBytes + h * 2 * kTileBytes;
     uint8_t* sv = sk + kTileBytes;
 #pragma unroll
     for (int i = threadIdx.x; i < 64 * kChunks; i += NT) {
@@ -185,23 +191,119 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
     }
   };
 
+  const int nsteps = (t1 - t0 + PPS - 1) / PPS;
+  auto load_step = [&](int u) {
+#pragma unroll
+    for (int h = 0; h < PPS; ++h) {
+      const int t = t0 + u * PPS + h;
+      if (t < t1) load_tile(t, u % kStages, h);
+    }
+  };
 #pragma unroll
   for (int st = 0; st < kStages - 1; ++st) {
-    if (t0 + st < t1) load_tile(t0 + st, st);
+    if (st < nsteps) load_step(st);
     cp_async_commit();
   }
-  for (int t = t0; t < t1; ++t) {
+  for (int u = 0; u < nsteps; ++u) {
     if (tma)
-      sm100::mbar_wait(&full[(t - t0) % kStages], ((t - t0) / kStages) & 1);
+      sm100::mbar_wait(&full[u % kStages], (u / kStages) & 1);
     else
       cp_async_wait<kStages - 2>();
-    __syncthreads();  // tile t landed for everyone; tile t-1's buffer is free
+    __syncthreads();  // step u landed for everyone; step u-1's buffer is free
     {
-      const int nt = t + kStages - 1;
-      if (nt < t1) load_tile(nt, (nt - t0) % kStages);
+      const int nu = u + kStages - 1;
+      if (nu < nsteps) load_step(nu);
       cp_async_commit();
     }
-    const uint8_t* k_s = smem + ((t - t0) % kStages) * 2 * kTileBytes;
+    const uint8_t* stage = smem + (u % kStages) * kStageBytes;
+    if constexpr (PPS == 2) {
+      // this warp: page h of the step, keys [cb*16, cb*16 + 32) of that page
+      const int h = kg >> 1, cb = (kg & 1) * 2;
+      const int t = t0 + u * 2 + h;
+      const int kbase = t * 64 + cb * 16;
+      if (t < t1 && kbase <= warp_lim) {
+        const uint8_t* k_s = stage + h * 2 * kTileBytes;
+        const uint8_t* v_s = k_s + kTileBytes;
+        float s[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+        const int mi = lane >> 3;
+#pragma unroll
+        for (int kk = 0; kk < kKS; ++kk) {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            uint32_t b[4];
+            const int key = (cb + cc) * 16 + 8 * (mi >> 1) + (lane & 7);
+            ldsm_x4(b, k_s + swz<HD>(key, kk * 2 + (mi & 1)));
+            mma16816(s[2 * cc], qa[kk], b[0], b[1]);
+            mma16816(s[2 * cc + 1], qa[kk], b[2], b[3]);
+          }
+        }
+        float mx_lo = kNegBig, mx_hi = kNegBig;
+#pragma unroll
+        for (int nt2 = 0; nt2 < 4; ++nt2) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int key = kbase + nt2 * 8 + (lane & 3) * 2 + e;
+            s[nt2][e] = key <= lim_lo ? s[nt2][e] * scale_log2 : -INFINITY;
+            s[nt2][2 + e] = key <= lim_hi ? s[nt2][2 + e] * scale_log2 : -INFINITY;
+            mx_lo = fmaxf(mx_lo, s[nt2][e]);
+            mx_hi = fmaxf(mx_hi, s[nt2][2 + e]);
+          }
+        }
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+          mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, off));
+          mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, off));
+        }
+        const float nm_lo = fmaxf(m_lo, mx_lo), nm_hi = fmaxf(m_hi, mx_hi);
+        const float al_lo = exp2f(m_lo - nm_lo), al_hi = exp2f(m_hi - nm_hi);
+        m_lo = nm_lo;
+        m_hi = nm_hi;
+        uint32_t pa[2][4];
+        float sl = 0.f, sh = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float p[2][4];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            p[q][0] = exp2f(s[2 * cc + q][0] - nm_lo);
+            p[q][1] = exp2f(s[2 * cc + q][1] - nm_lo);
+            p[q][2] = exp2f(s[2 * cc + q][2] - nm_hi);
+            p[q][3] = exp2f(s[2 * cc + q][3] - nm_hi);
+            sl += p[q][0] + p[q][1];
+            sh += p[q][2] + p[q][3];
+          }
+          pa[cc][0] = pack_bf16(p[0][0], p[0][1]);
+          pa[cc][1] = pack_bf16(p[0][2], p[0][3]);
+          pa[cc][2] = pack_bf16(p[1][0], p[1][1]);
+          pa[cc][3] = pack_bf16(p[1][2], p[1][3]);
+        }
+        l_lo = l_lo * al_lo + sl;
+        l_hi = l_hi * al_hi + sh;
+#pragma unroll
+        for (int i = 0; i < kDT; ++i) {
+          o[i][0] *= al_lo;
+          o[i][1] *= al_lo;
+          o[i][2] *= al_hi;
+          o[i][3] *= al_hi;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+          for (int dt = 0; dt < kDT; dt += 2) {
+            uint32_t b[4];
+            const int key = (cb + cc) * 16 + 8 * (mi & 1) + (lane & 7);
+            ldsm_x4_t(b, v_s + swz<HD>(key, dt + (mi >> 1)));
+            mma16816(o[dt], pa[cc], b[0], b[1]);
+            mma16816(o[dt + 1], pa[cc], b[2], b[3]);
+          }
+        }
+      }
+      continue;
+    }
+    const int t = t0 + u;
+    const uint8_t* k_s = stage;
     const uint8_t* v_s = k_s + kTileBytes;
     for (int c = ROWS ? 0 : kg; c < 4; c += (ROWS ? 1 : nkg)) {  // 16-key chunks of the page
       const int kbase = t * 64 + c * 16;
@@ -389,25 +491,30 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   }
 }
 
-template <int HD, bool ROWS, int MT = 1>
+bool want_tma_env() {
+  static const bool v = getenv("FASER_ATTN_TMA") && getenv("FASER_ATTN_TMA")[0] == '1';
+  return v;
+}
+
+template <int HD, bool ROWS, int MT = 1, int PPS = 1>
 cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int n_split, KvDev kv,
                    int layer, const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, float* part_o,
                    float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s) {
   constexpr int kTile = 64 * HD * 2;
   constexpr int kMerge = (4 * MT * 16 * HD + 128 * MT) * 4;
-  constexpr int kSmem = (2 * kAttnStages<HD> * kTile > kMerge ? 2 * kAttnStages<HD> * kTile : kMerge) + 1024;
+  constexpr int kSmem = (PPS * 2 * kAttnStages<HD> * kTile > kMerge ? PPS * 2 * kAttnStages<HD> * kTile : kMerge) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_kernel<HD, ROWS, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(attn_kernel<HD, ROWS, MT, PPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
   dim3 grid(n_req, m.n_kv, blocks * n_split);
   static CUtensorMap dummy{};
   // TMA page loads (one thread, hardware swizzle) measured equal to the cp.async path on B200
   // (config 3, B = 1/32/128): opt-in FASER_ATTN_TMA=1
-  static const bool want_tma = getenv("FASER_ATTN_TMA") && getenv("FASER_ATTN_TMA")[0] == '1';
+  static const bool want_tma = want_tma_env();
   const bool use_tma = want_tma && kv.tma != nullptr && HD == 64;
-  attn_kernel<HD, ROWS, MT><<<grid, 128 * MT, kSmem, s>>>(use_tma ? *kv.tma : dummy, use_tma ? 1 : 0, rows, kv, layer,
+  attn_kernel<HD, ROWS, MT, PPS><<<grid, 128 * MT, kSmem, s>>>(use_tma ? *kv.tma : dummy, use_tma ? 1 : 0, rows, kv, layer,
                                                           m.n_q, m.n_kv, qbuf, obuf, part_o, part_ml, counters,
                                                           n_split, rows_cap, blocks, scale_log2);
   return cudaGetLastError();
@@ -451,6 +558,12 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(m.hd));
   if (m.hd == 64) {
     if (rows_mode) return launch<64, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+    // two-page steps (PPS = 2, FASER_ATTN_WIDE=1)
+    static const bool wide = getenv("FASER_ATTN_WIDE") && getenv("FASER_ATTN_WIDE")[0] == '1';
+    if (wide && !(want_tma_env() && kv.tma)) {
+      if (mt == 2) return launch<64, false, 2, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+      return launch<64, false, 1, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+    }
     if (mt == 2) return launch<64, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
     return launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
   }
