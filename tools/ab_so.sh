@@ -1,4 +1,5 @@
-# attention two-page steps (FASER_ATTN_WIDE) : parity under the env, then A/B
-FASER_ATTN_WIDE=1 timeout 900 python -m pytest tests -m gpu -q -x -k "attn or attention or llama or trace" 2>&1 | tail -2
-for r in 1 2; do for v in 0 1; do echo "== wide $v"; FASER_ATTN_WIDE=$v timeout 120 python tools/attn_bench.py 32,4,600 32,4,1200 32,4,64 128,4,600 32,1,600 1,4,600 8,4,2400; done; done
-for v in 0 1; do echo "== wide $v"; FASER_ATTN_WIDE=$v timeout 200 python tools/llama_perf.py cfg3 32 4 2>&1 | tail -1; FASER_ATTN_WIDE=$v timeout 200 python tools/llama_perf.py cfg3 128 4 2>&1 | tail -1; done
+# A/B of product-library builds (ab_old.so / ab_new.so at the repo root, untracked): PDL-launched attention
+L=paper_2604_20503_b200/libfaser_b200.so
+cp ab_new.so $L; timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for r in 1 2; do for v in old new; do cp ab_$v.so $L; echo "== $v"; timeout 200 python tools/llama_perf.py cfg3 32 4 2>&1 | tail -1; timeout 200 python tools/llama_perf.py cfg3 128 4 2>&1 | tail -1; timeout 300 python tools/llama_perf.py cfg4 32 4 2>&1 | tail -1; done; done
+cp ab_new.so $L
