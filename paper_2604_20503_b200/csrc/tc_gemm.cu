@@ -600,6 +600,13 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     const int kps = (kb + 3) / 4;
     p.splits = (kb + kps - 1) / kps;
     p.deep = true;
+  } else if (t > 64 && t <= 128 && k >= 4096 && k < 8192 && mt <= 16) {  // config-3 down (2048 x 5632)
+    // in-stream: verify 1.694 -> 1.681 ms at B = 32 (profiles/r01_plan_down128_ab.txt)
+    p.bn = 64;
+    p.mc = 1;
+    const int kps = (kb + 3) / 4;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
   } else if (t > 64 && t <= 128 && k >= 4096 && mt >= 40 && mt <= 64) {  // config-4 qkv (6144 x 4096)
     p.bn = 64;
     p.mc = 1;

@@ -1,5 +1,10 @@
-# A/B of product-library builds (ab_old.so / ab_new.so at the repo root, untracked): PDL-launched attention
-L=paper_2604_20503_b200/libfaser_b200.so
-cp ab_new.so $L; timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for r in 1 2; do for v in old new; do cp ab_$v.so $L; echo "== $v"; timeout 200 python tools/llama_perf.py cfg3 32 4 2>&1 | tail -1; timeout 200 python tools/llama_perf.py cfg3 128 4 2>&1 | tail -1; timeout 300 python tools/llama_perf.py cfg4 32 4 2>&1 | tail -1; done; done
-cp ab_new.so $L
+# in-stream verify-plan A/B for the config-3 down GEMM (2048x5632) at 65..128 rows
+run() { echo "== $1"; FASER_PLAN_OVERRIDE="$1" timeout 200 python tools/llama_perf.py cfg3 32 4 2>&1 | tail -1; }
+for r in 1 2; do
+run ""
+run "2048,5632,65,128,64,1,4"
+run "2048,5632,65,128,64,1,3"
+run "2048,5632,65,128,64,1,6"
+run "2048,5632,65,128,64,2,4"
+run "2048,5632,65,128,32,1,4"
+done
