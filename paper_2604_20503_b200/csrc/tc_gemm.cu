@@ -607,6 +607,20 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     const int kps = (kb + 3) / 4;
     p.splits = (kb + kps - 1) / kps;
     p.deep = true;
+  } else if (t > 160 && t <= 256 && k >= 4096 && k < 8192 && mt <= 16) {  // config-3 down at 161..256 rows
+    // one 128-row token tile, 4-way split (in-stream verify, profiles/r01_plan_256_ab.txt:
+    // B = 48 2.63 -> 2.35 ms, B = 56 2.34 -> 2.26 ms, B = 64 2.77 -> 2.59 ms; neutral at 160 rows)
+    p.bn = 128;
+    p.mc = 1;
+    const int kps = (kb + 3) / 4;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
+  } else if (t > 240 && t <= 256 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 241..256 rows
+    // 64-row token tiles, no split: B = 64 2.77 -> 2.67 ms alone (worse at 160..224 rows)
+    p.bn = 64;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = true;
   } else if (t > 64 && t <= 128 && k >= 4096 && mt >= 40 && mt <= 64) {  // config-4 qkv (6144 x 4096)
     p.bn = 64;
     p.mc = 1;
