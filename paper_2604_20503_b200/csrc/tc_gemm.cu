@@ -615,6 +615,20 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     const int kps = (kb + 3) / 4;
     p.splits = (kb + kps - 1) / kps;
     p.deep = true;
+  } else if (t > 300 && t <= 512 && k >= 4096 && k < 8192 && mt <= 16) {  // config-3 down at 301..512 rows
+    // 128-row token tiles, 2-way split (in-stream verify, profiles/r01_plan_512_ab.txt:
+    // B = 80 3.92 -> 3.43 ms, B = 96 4.13 -> 3.60 ms, B = 128 4.26 -> 4.20 ms; slower at 288 rows)
+    p.bn = 128;
+    p.mc = 1;
+    const int kps = (kb + 1) / 2;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
+  } else if (t > 448 && t <= 512 && k == 2048 && mt >= 64 && mt <= 100) {  // config-3 gate/up at 449..512 rows
+    // 256 x 256 per CTA (B = 128: 4.26 -> 4.09 ms alone; slower at 384 rows)
+    p.bn = 256;
+    p.mc = 2;
+    p.splits = 1;
+    p.deep = true;
   } else if (t > 240 && t <= 256 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 241..256 rows
     // 64-row token tiles, no split: B = 64 2.77 -> 2.67 ms alone (worse at 160..224 rows)
     p.bn = 64;
