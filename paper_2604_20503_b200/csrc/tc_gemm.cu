@@ -561,7 +561,13 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
   const int kb = k / kBK;
   int cover = 32;
   while (cover < t && cover < 256) cover <<= 1;
-  if (t >= 1024 && mt >= 2 && ((mt + 1) / 2) * ((t + 255) / 256) >= 120) {  // 256 x 256 per CTA (4096 rows: gate/up
+  if (t > 768 && t <= 1024 && k == 2048 && mt >= 64 && mt <= 100) {  // config-3 gate/up at 769..1024 rows
+    // 128 x 256 per CTA (with the qkv rule below, profiles/r01_plan_1024_ab.txt)
+    p.bn = 256;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t >= 1024 && mt >= 2 && ((mt + 1) / 2) * ((t + 255) / 256) >= 120) {  // 256 x 256 per CTA (4096 rows: gate/up
     p.bn = 256;                   // 233 -> 183 us = 1.03 PFLOP/s, o 48 -> 34 us, down 101 -> 73 us)
     p.mc = 2;
     p.splits = 1;
@@ -627,6 +633,13 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     // 256 x 256 per CTA (B = 128: 4.26 -> 4.09 ms alone; slower at 384 rows)
     p.bn = 256;
     p.mc = 2;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t > 768 && t <= 1024 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 769..1024 rows
+    // one 128-row token tile per CTA, no split (in-stream verify with the gate/up rule below,
+    // profiles/r01_plan_1024_ab.txt: B = 200 6.95 -> 6.20 ms, B = 224 7.78 -> 6.41, B = 256 7.07 -> 6.40)
+    p.bn = 128;
+    p.mc = 1;
     p.splits = 1;
     p.deep = true;
   } else if (t > 240 && t <= 256 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 241..256 rows
