@@ -642,6 +642,19 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 1;
     p.splits = 1;
     p.deep = true;
+  } else if (t > 96 && t <= 256 && k == 768 && mt >= 40 && mt <= 56) {  // config-3 draft gate/up (6144 x 768)
+    // in-stream draft time (profiles/r01_plan_draft_ab.txt): B = 128 0.930 -> 0.892 ms (64-row
+    // tiles), B = 256 1.413 -> 1.379 ms (128-row tiles)
+    p.bn = t <= 128 ? 64 : 128;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t > 96 && t <= 128 && k == 3072 && mt <= 8) {  // config-3 draft down (768 x 3072): B = 128 -> 0.910 ms
+    p.bn = 64;
+    p.mc = 1;
+    const int kps = (kb + 3) / 4;
+    p.splits = (kb + kps - 1) / kps;
+    p.deep = true;
   } else if (t > 240 && t <= 256 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 241..256 rows
     // 64-row token tiles, no split: B = 64 2.77 -> 2.67 ms alone (worse at 160..224 rows)
     p.bn = 64;

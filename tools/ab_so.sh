@@ -1,5 +1,12 @@
-# in-stream validation of combined qkv + gate/up plans at 769..1024 rows
+# in-stream draft-plan search (config-3 draft shapes) at 97..128 rows (B=128) and 193..256 rows (B=256)
 run() { echo "== B=$2 $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 $2 4 2>&1 | tail -1; }
-C="2560,2048,769,1024,128,1,1;11264,2048,769,1024,256,1,1"
-for B in 256 224 200; do run "" $B; run "$C" $B; run "2560,2048,769,1024,128,1,1" $B; done
-run "11264,2048,769,1024,256,1,1" 200
+run "" 128
+for c in 64,1,1 128,1,1 64,1,2; do run "2304,768,97,128,$c" 128; done
+for c in 64,1,1 128,1,1 128,2,1; do run "6144,768,97,128,$c" 128; done
+for c in 64,1,4 128,1,4 128,1,2; do run "768,3072,97,128,$c" 128; done
+for c in 64,1,1 128,1,3; do run "768,768,97,128,$c" 128; done
+run "" 256
+for c in 128,1,1 64,1,2 256,1,1; do run "2304,768,193,256,$c" 256; done
+for c in 128,1,1 128,2,1 256,1,1; do run "6144,768,193,256,$c" 256; done
+for c in 64,1,2 128,1,2 128,1,4; do run "768,3072,193,256,$c" 256; done
+for c in 64,1,2 128,1,2; do run "768,768,193,256,$c" 256; done
