@@ -688,10 +688,21 @@ GemmPlan gemm_plan_prefill(int n_out, int t, int k, int num_sms) {
   // single-prompt prefill (256..1023 rows), from the 576-row sweep (profiles/r01_gemm_sweep_576rows.jsonl)
   static const bool off = getenv("FASER_PREFILL_PLAN") && getenv("FASER_PREFILL_PLAN")[0] == '0';
   GemmPlan p = gemm_plan(n_out, t, k, num_sms);
-  if (off || t < 256 || t >= 1024) return p;
+  // in-stream single-prompt admissions (profiles/r01_prefill_len_ab.txt): the gate/up, qkv and
+  // draft-down rules win at 512..767 rows but lose at 300 / 400 / 1000 rows to the general plan
+  if (off || t < 512 || t >= 1024) return p;
   const int mt = n_out / kBM;
   const int kb = k / kBK;
-  if (mt >= 64 && ((mt + 1) / 2) * ((t + 255) / 256) >= 100) {  // gate/up: 43.9 -> 34.6 us
+  if (mt <= 16 && mt > 8 && t > 576) {  // o / down (2048 outputs) past 576 rows: 64-row tiles
+    // would need 16 x 10+ CTAs = a second wave; one 128-row tile each (600-token admission
+    // 5.62 -> 5.26 ms, 700: 6.07 -> 5.47 ms, 760: 6.24 -> 5.60 ms)
+    p.bn = 128;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t >= 768) {
+    // general plan
+  } else if (mt >= 64 && ((mt + 1) / 2) * ((t + 255) / 256) >= 100) {  // gate/up: 43.9 -> 34.6 us
     p.bn = 256;
     p.mc = 2;
     p.splits = 1;
