@@ -689,10 +689,21 @@ GemmPlan gemm_plan_prefill(int n_out, int t, int k, int num_sms) {
   static const bool off = getenv("FASER_PREFILL_PLAN") && getenv("FASER_PREFILL_PLAN")[0] == '0';
   GemmPlan p = gemm_plan(n_out, t, k, num_sms);
   // in-stream single-prompt admissions (profiles/r01_prefill_len_ab.txt): the gate/up, qkv and
-  // draft-down rules win at 512..767 rows but lose at 300 / 400 / 1000 rows to the general plan
-  if (off || t < 512 || t >= 1024) return p;
+  // draft-down rules below win at 512..767 rows but lose at 300 / 400 / 1000 rows to the general plan
+  if (off || t < 256 || t >= 1024) return p;
   const int mt = n_out / kBM;
   const int kb = k / kBK;
+  if (t < 512) {
+    // qkv / o / down (2048..2560 outputs) at 256..511 rows: 64-row token tiles keep the grid in one
+    // wave (32-row tiles need 16-20 x 10+ CTAs); 300-token admission 4.67 -> 4.01 ms, 400: 4.48 -> 4.36
+    if (mt > 8 && mt <= 20 && k >= 2048) {
+      p.bn = 64;
+      p.mc = 1;
+      p.splits = 1;
+      p.deep = true;
+    }
+    return p;
+  }
   if (mt <= 16 && mt > 8 && t > 576) {  // o / down (2048 outputs) past 576 rows: 64-row tiles
     // would need 16 x 10+ CTAs = a second wave; one 128-row tile each (600-token admission
     // 5.62 -> 5.26 ms, 700: 6.07 -> 5.47 ms, 760: 6.24 -> 5.60 ms)
