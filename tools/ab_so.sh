@@ -1,4 +1,3 @@
-# validation: prefill 256..511-row rule; admissions across lengths; default bench x2; GPU tests
-timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-for L in 200 260 300 400 500 576 700 800 1000; do timeout 200 python tools/prefill_perf.py cfg3 $L 4 2>&1 | tail -1; done
-for r in 1 2; do timeout 300 python bench.py > gpurun_out/bench_default_v9_$r.json 2>/dev/null; tail -1 gpurun_out/bench_default_v9_$r.json | cut -c1-160; done
+# prefill gate/up just above 256 rows (bn 256 leaves a nearly empty second token tile)
+run() { echo "== L=$2 $1"; FASER_PLAN_OVERRIDE="$1" timeout 200 python tools/prefill_perf.py cfg3 $2 4 2>&1 | tail -1; }
+for L in 260 300 350; do run "" $L; run "11264,2048,257,400,128,2,1" $L; run "11264,2048,257,400,256,2,1" $L; run "11264,2048,257,400,128,1,1" $L; done
