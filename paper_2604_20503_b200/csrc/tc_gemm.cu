@@ -635,6 +635,19 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 2;
     p.splits = 1;
     p.deep = true;
+  } else if (t > 512 && t <= 768 && k >= 2048 && k < 8192 && mt > 8 && mt <= 20 && (mt > 16 || t > 576)) {
+    // config-3 qkv / o / down at 513..768 rows: one 128-row token tile per CTA, no split (in-stream
+    // verify with the gate/up rule below, profiles/r01_plan_768_ab.txt; o / down keep 64-row tiles
+    // up to 576 rows, where 16 x 9 CTAs still fit one wave)
+    p.bn = 128;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = true;
+  } else if (t > 512 && t <= 768 && k == 2048 && mt >= 64 && mt <= 100) {  // config-3 gate/up at 513..768 rows
+    p.bn = 256;
+    p.mc = 2;
+    p.splits = 1;
+    p.deep = true;
   } else if (t > 768 && t <= 1024 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 769..1024 rows
     // one 128-row token tile per CTA, no split (in-stream verify with the gate/up rule below,
     // profiles/r01_plan_1024_ab.txt: B = 200 6.95 -> 6.20 ms, B = 224 7.78 -> 6.41, B = 256 7.07 -> 6.40)

@@ -1,3 +1,11 @@
-# prefill gate/up just above 256 rows (bn 256 leaves a nearly empty second token tile)
-run() { echo "== L=$2 $1"; FASER_PLAN_OVERRIDE="$1" timeout 200 python tools/prefill_perf.py cfg3 $2 4 2>&1 | tail -1; }
-for L in 260 300 350; do run "" $L; run "11264,2048,257,400,128,2,1" $L; run "11264,2048,257,400,256,2,1" $L; run "11264,2048,257,400,128,1,1" $L; done
+# in-stream verify-plan search for config-3 shapes at 513..768 rows (B=160 -> 640 rows, B=192 -> 768)
+run() { echo "== B=$2 $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 $2 4 2>&1 | tail -1; }
+for B in 160 192; do
+run "" $B
+run "2048,5632,513,768,128,1,1" $B
+run "2048,5632,513,768,128,1,2" $B
+run "2048,2048,513,768,128,1,1" $B
+run "2560,2048,513,768,128,1,1" $B
+run "11264,2048,513,768,256,1,1" $B
+run "11264,2048,513,768,256,2,1" $B
+done
