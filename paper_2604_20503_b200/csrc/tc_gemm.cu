@@ -526,24 +526,25 @@ GemmPlan gemm_plan_legacy(int n_out, int t, int k, int num_sms) {
 //    2.77 -> 3.57 ms, so they are not applied);
 //  * <= 32 rows and >= 40 tiles: no K split (6144x768 @32: 10.3 -> 5.7 us);
 //  * <= 8 tiles with K >= 3072: 8-way K split (768x3072 @32: 6.7 -> 5.4 us).
-// Per SM the TMA ingest saturates near 44 GB/s (tools/tma_probe.cu), which is why sharing one
-// rows tile across weight tiles pays once the rows tile is comparable to a weight block.
-// Experiment hook: FASER_PLAN_OVERRIDE="n_out,k,t_lo,t_hi,bn,mc,splits;..." forces a plan for
-// matching launches (in-stream A/B of plans without rebuilding).
+// Sharing one rows tile across weight tiles (MC) pays once the rows tile is comparable to a weight
+// block: the rows tile is re-read by every weight-tile CTA.
+// Experiment hook: FASER_PLAN_OVERRIDE="n_out,k,t_lo,t_hi,bn,mc,splits[,deep];..." forces a plan
+// for matching launches (in-stream A/B of plans without rebuilding; deep defaults to 1).
 static bool plan_override(int n_out, int t, int k, GemmPlan* p) {
   static const char* env = getenv("FASER_PLAN_OVERRIDE");
   if (!env) return false;
   const char* c = env;
   while (*c) {
-    int v[7] = {0, 0, 0, 0, 0, 0, 0}, used = 0;
+    int v[8] = {0, 0, 0, 0, 0, 0, 0, 1}, used = 0, used8 = 0;
     if (sscanf(c, "%d,%d,%d,%d,%d,%d,%d%n", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &used) != 7) return false;
+    if (c[used] == ',' && sscanf(c + used, ",%d%n", &v[7], &used8) == 1) used += used8;
     if (v[0] == n_out && v[1] == k && t >= v[2] && t <= v[3]) {
       const int kb = k / kBK, s1 = v[6] < 1 ? 1 : (v[6] > 8 ? 8 : v[6]);
       const int kps = (kb + s1 - 1) / s1;
       p->bn = v[4];
       p->mc = v[5];
       p->splits = (kb + kps - 1) / kps;
-      p->deep = true;
+      p->deep = v[7] != 0;
       return true;
     }
     c += used;
@@ -655,6 +656,14 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 1;
     p.splits = 1;
     p.deep = true;
+  } else if (t > 64 && t <= 128 && k == 2048 && mt >= 64 && mt <= 100) {  // config-3 gate/up at 65..128 rows
+    // 64-row token tiles with the shallow pipeline: 2 x 88 CTAs at 2 per SM fill the GPU where one
+    // 128-row tile per CTA leaves 60 SMs idle (in-stream verify B = 32 1.684 -> 1.651 ms,
+    // profiles/r01_plan_gu128_ab.txt)
+    p.bn = 64;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = false;
   } else if (t > 96 && t <= 256 && k == 768 && mt >= 40 && mt <= 56) {  // config-3 draft gate/up (6144 x 768)
     // in-stream draft time (profiles/r01_plan_draft_ab.txt): B = 128 0.930 -> 0.892 ms (64-row
     // tiles), B = 256 1.413 -> 1.379 ms (128-row tiles)
