@@ -678,11 +678,19 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.splits = (kb + kps - 1) / kps;
     p.deep = true;
   } else if (t > 240 && t <= 256 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 241..256 rows
-    // 64-row token tiles, no split: B = 64 2.77 -> 2.67 ms alone (worse at 160..224 rows)
-    p.bn = 64;
+    // 32-row token tiles, no split, shallow pipeline (2 CTAs/SM over 160 CTAs): B = 64 2.50 -> 2.41 ms
+    // (64-row deep tiles: 2.77 -> 2.67 ms; both worse at 160..224 rows)
+    p.bn = 32;
     p.mc = 1;
     p.splits = 1;
-    p.deep = true;
+    p.deep = false;
+  } else if (t > 224 && t <= 256 && k == 2048 && mt >= 64 && mt <= 100) {  // config-3 gate/up at 225..256 rows
+    // one 128-row token tile per CTA, shallow pipeline: 2 x 88 CTAs at 2 per SM (B = 64 2.40 -> 2.37 ms;
+    // neutral at 192 / 224 rows, worse at 160)
+    p.bn = 128;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = false;
   } else if (t > 64 && t <= 128 && k >= 4096 && mt >= 40 && mt <= 64) {  // config-4 qkv (6144 x 4096)
     p.bn = 64;
     p.mc = 1;

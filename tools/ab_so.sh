@@ -1,6 +1,8 @@
-# shallow (2 CTAs/SM) vs deep plans for the under-filled config-3 gate/up at 65..128 rows (B=32)
-run() { echo "== $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 32 4 2>&1 | tail -1; }
+# shallow (2 CTAs/SM) variants at 129..256 rows (B=64)
+run() { echo "== $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 64 4 2>&1 | tail -1; }
 run ""
-for c in 128,1,2,0 128,1,3,0 64,1,1,0 64,1,2,0 128,1,1,0; do run "11264,2048,65,128,$c"; done
-for c in 128,1,2,0 64,1,1,0; do run "32000,2048,65,128,$c"; done
-run "2048,5632,65,128,64,1,4,0"
+for c in 128,1,1,0 64,1,1,0 128,1,2,0; do run "11264,2048,129,256,$c"; done
+run "2560,2048,241,256,32,1,1,0"
+run "2048,2048,129,256,32,1,1,0"
+run "2048,2048,129,256,64,1,1,0"
+run ""
