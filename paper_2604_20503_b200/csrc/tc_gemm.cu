@@ -651,11 +651,19 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.deep = true;
   } else if (t > 768 && t <= 1024 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 769..1024 rows
     // one 128-row token tile per CTA, no split (in-stream verify with the gate/up rule below,
-    // profiles/r01_plan_1024_ab.txt: B = 200 6.95 -> 6.20 ms, B = 224 7.78 -> 6.41, B = 256 7.07 -> 6.40)
+    // profiles/r01_plan_1024_ab.txt: B = 200 6.95 -> 6.20 ms, B = 224 7.78 -> 6.41, B = 256 7.07 -> 6.40);
+    // shallow pipeline (2 CTAs/SM) above 960 rows: B = 256 6.40 -> 6.28 ms, but B = 200 (800 rows)
+    // 6.21 -> 6.33 ms (profiles/r01_plan_shallow256_ab.txt)
     p.bn = 128;
     p.mc = 1;
     p.splits = 1;
-    p.deep = true;
+    p.deep = t <= 960;
+  } else if (t > 448 && t <= 512 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 449..512 rows
+    // 64-row token tiles, shallow pipeline: 160 CTAs at 2 per SM (B = 128 4.04 -> 3.87 ms)
+    p.bn = 64;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = false;
   } else if (t > 64 && t <= 128 && k == 2048 && mt >= 64 && mt <= 100) {  // config-3 gate/up at 65..128 rows
     // 64-row token tiles with the shallow pipeline: 2 x 88 CTAs at 2 per SM fill the GPU where one
     // 128-row tile per CTA leaves 60 SMs idle (in-stream verify B = 32 1.684 -> 1.651 ms,

@@ -1,8 +1,10 @@
-# shallow (2 CTAs/SM) variants at 129..256 rows (B=64)
-run() { echo "== $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 64 4 2>&1 | tail -1; }
-run ""
-for c in 128,1,1,0 64,1,1,0 128,1,2,0; do run "11264,2048,129,256,$c"; done
-run "2560,2048,241,256,32,1,1,0"
-run "2048,2048,129,256,32,1,1,0"
-run "2048,2048,129,256,64,1,1,0"
-run ""
+# shallow (2 CTAs/SM) variants at 449..512 rows (B=128) and 769..1024 rows (B=256)
+run() { echo "== B=$2 $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 $2 4 2>&1 | tail -1; }
+run "" 128
+run "2560,2048,449,512,64,1,1,0" 128
+run "11264,2048,449,512,256,1,1,0" 128
+run "11264,2048,449,512,128,1,1,0" 128
+run "2048,2048,449,512,64,1,1,0" 128
+run "" 256
+run "11264,2048,769,1024,256,1,1,0" 256
+run "2560,2048,769,1024,128,1,1,0" 256
