@@ -658,6 +658,14 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 1;
     p.splits = 1;
     p.deep = t <= 960;
+  } else if (t > 256 && t <= 448 && k == 2048 && ((mt >= 9 && mt <= 20) || (mt >= 64 && mt <= 100))) {
+    // config-3 qkv / o / gate/up at 257..448 rows, shallow pipeline (2 CTAs/SM) so the grids that
+    // would spill into a second wave at 1 CTA/SM fit one (profiles/r01_plan_448_ab.txt):
+    // qkv 64-row tiles, o 32-row tiles, gate/up one 128-row tile (B = 96 3.62 -> ~3.1 ms)
+    p.bn = mt >= 64 ? 128 : (mt >= 18 ? 64 : 32);
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = false;
   } else if (t > 448 && t <= 512 && k == 2048 && mt >= 18 && mt <= 20) {  // config-3 qkv at 449..512 rows
     // 64-row token tiles, shallow pipeline: 160 CTAs at 2 per SM (B = 128 4.04 -> 3.87 ms)
     p.bn = 64;
