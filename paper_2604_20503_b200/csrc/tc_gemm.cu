@@ -658,6 +658,13 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 1;
     p.splits = 1;
     p.deep = t <= 960;
+  } else if (t > 176 && t <= 208 && k == 2048 && mt > 8 && mt <= 16) {  // config-3 o at 177..208 rows
+    // 32-row tiles, no split, shallow pipeline (B = 48 2.36 -> 2.24 ms; worse at 160 and 224 rows,
+    // profiles/r01_plan_192_ab.txt)
+    p.bn = 32;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = false;
   } else if (t > 256 && t <= 448 && k == 2048 && ((mt >= 9 && mt <= 20) || (mt >= 64 && mt <= 100))) {
     // config-3 qkv / o / gate/up at 257..448 rows, shallow pipeline (2 CTAs/SM) so the grids that
     // would spill into a second wave at 1 CTA/SM fit one (profiles/r01_plan_448_ab.txt):
