@@ -538,7 +538,8 @@ static bool plan_override(int n_out, int t, int k, GemmPlan* p) {
     int v[8] = {0, 0, 0, 0, 0, 0, 0, 1}, used = 0, used8 = 0;
     if (sscanf(c, "%d,%d,%d,%d,%d,%d,%d%n", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &used) != 7) return false;
     if (c[used] == ',' && sscanf(c + used, ",%d%n", &v[7], &used8) == 1) used += used8;
-    if (v[0] == n_out && v[1] == k && t >= v[2] && t <= v[3]) {
+    const bool valid = (v[4] == 32 || v[4] == 64 || v[4] == 128 || v[4] == 256) && (v[5] == 1 || v[5] == 2 || v[5] == 4);
+    if (valid && v[0] == n_out && v[1] == k && t >= v[2] && t <= v[3]) {  // invalid entries are ignored
       const int kb = k / kBK, s1 = v[6] < 1 ? 1 : (v[6] > 8 ? 8 : v[6]);
       const int kps = (kb + s1 - 1) / s1;
       p->bn = v[4];
