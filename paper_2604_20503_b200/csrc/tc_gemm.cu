@@ -688,6 +688,12 @@ GemmPlan gemm_plan(int n_out, int t, int k, int num_sms) {
     p.mc = 1;
     p.splits = 1;
     p.deep = false;
+  } else if (t > 32 && t <= 64 && k == 768 && mt >= 40 && mt <= 56) {  // config-3 draft gate/up at 33..64 rows
+    // 32-row tiles, no split, shallow pipeline (draft B = 64 0.681 -> 0.640 ms, profiles/r01_plan_draft_ab.txt)
+    p.bn = 32;
+    p.mc = 1;
+    p.splits = 1;
+    p.deep = false;
   } else if (t > 96 && t <= 256 && k == 768 && mt >= 40 && mt <= 56) {  // config-3 draft gate/up (6144 x 768)
     // in-stream draft time (profiles/r01_plan_draft_ab.txt): B = 128 0.930 -> 0.892 ms (64-row
     // tiles), B = 256 1.413 -> 1.379 ms (128-row tiles)

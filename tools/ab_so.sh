@@ -1,9 +1,7 @@
-# wave-aware shallow variants at 129..224 rows (B=40 -> 160, B=48 -> 192, B=56 -> 224)
-run() { echo "== B=$2 $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 $2 4 2>&1 | tail -1; }
-for B in 48 40 56; do
-run "" $B
-run "11264,2048,129,224,128,1,1,0" $B
-run "2560,2048,129,224,32,1,1,0" $B
-run "2560,2048,129,224,64,1,1,0" $B
-run "2048,2048,129,224,32,1,1,0" $B
-done
+# shallow draft-plan variants at 33..64 rows (B=64 draft steps)
+run() { echo "== $1"; FASER_PLAN_OVERRIDE="$1" timeout 250 python tools/llama_perf.py cfg3 64 4 2>&1 | tail -1; }
+run ""
+for c in 32,1,1,0 32,1,2,0 64,1,2,0; do run "6144,768,33,64,$c"; done
+for c in 32,1,2,0 32,1,4,0 64,1,4,0; do run "2304,768,33,64,$c"; done
+for c in 32,1,4,0 64,1,4,1; do run "768,3072,33,64,$c"; done
+run ""
