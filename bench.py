@@ -9,7 +9,15 @@ verification. A "step" is one serving iteration: [admission prefill] -> ragged d
 verify forward (+ early exit) -> fused accept/commit for every live request.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--batch B] [--k K]
-                  [--mode vsd|ee] [--workload cfg3|toy] [--sweep 1,8,32,...]
+                  [--mode vsd|ad|ee|vsd_ee|full] [--workload cfg3|cfg4|cfg5|toy] [--no-sweep]
+                  [--trace SECONDS] [--tp]
+
+Measurement window: before the W warm-up steps every point serves until at least B requests
+have finished (<= FILL_CAP untimed steps), so the K timed steps see the steady-state mix of
+admissions (prefill), decoding requests and completions instead of the first batch's
+admission burst; the number does not depend on K beyond sampling noise.
+batch_sweep: the same measurement at B in SWEEP (1, 8, 32, 128, 256), each with its own
+roofline under the right bound (tensor when B*k rows exceed the ridge, HBM below).
 
 value      : committed tokens / device time of the K steps (CUDA events on the engine stream,
              max over ranks), prompts submitted to the engine before the timed region.
@@ -17,8 +25,10 @@ e2e        : the same metric through the C ABI with HOST buffers: prompts submit
              memory inside the timed region, per-step H2D of the step plan + admissions and D2H
              of the round results, wall clock.
 reference  : `--impl reference` runs the reference semantics on the host CPU: for cfg3 the
-             fp32 oracle port (oracle/lmsd.py — the reference has no transformer path), for the
-             toy workload the reference's own compiled engine (oracle/_ref).
+             fp32 oracle port (oracle/lmsd.py — the reference has no transformer path) on the
+             SAME backlog (prompts from the reference's own compiled synth_prompt, whole request
+             lifetimes incl. prefill) and the same `config`; for the toy workload the reference's
+             own compiled engine (oracle/_ref). It never loads the product library.
 Multi-GPU  : requests are sharded across ranks (independent replicas, no collective on the
              data path); value = all ranks' tokens / max-over-ranks device time.
 """
@@ -224,11 +234,11 @@ def llama_desc(name):
     return llama.PRESETS[name]()
 
 
-def make_engine(desc, args, local_rank, **tp):
+def make_engine(desc, args, local_rank, batch=None, **tp):
     from paper_2604_20503_b200 import engine
     mode = {"vsd": abi.MODE_VSD, "ad": abi.MODE_VSD_AD, "ee": abi.MODE_VSD_AD_EE,
             "ov": abi.MODE_FULL, "full": abi.MODE_FULL, "vsd_ee": abi.MODE_VSD_AD_EE}[args.mode]
-    return engine.ServingEngine(desc=desc, max_batch=args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
+    return engine.ServingEngine(desc=desc, max_batch=batch or args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
                                 mode=mode, default_spec_length=args.k, max_spec_length=16,
                                 prefill_rows=8192, device=local_rank, **tp)
 
@@ -326,7 +336,9 @@ def step_plan_hook(desc, args, models):
 def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=None, chunk=0, hook=None):
     """n_steps serving iterations; per-request first/last commit times on `clock`. With a
     drafter (AdaptiveDrafter) the per-request k_i come from assign_lengths before each step and
-    the round is fed back with observe_round after it (the reference loop)."""
+    the round is fed back with observe_round after it (the reference loop).
+    Returns the committed tokens; state["steps"] counts the steps actually executed and
+    state["finished"] the requests that completed."""
     tokens = 0
     for _ in range(n_steps):
         if feeder is not None:
@@ -336,19 +348,22 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
             break
         ks = None
         if drafter is not None:
-            ks = drafter.assign_lengths(live, len(live), 1.0)
+            ks = drafter.assign_lengths(live, len(live), drafter_r(eng))
             eng.set_spec_lengths(live, ks)
         if gate is not None:
             eng.set_gate(gate)
         if hook is not None:
             hook(eng, live, ks or [eng.cfg.default_spec_length] * len(live))
         res = eng.step()
+        state["steps"] = state.get("steps", 0) + 1
         for r in res:
             state["acc"] = state.get("acc", 0) + r.outcome.accepted_count
             state["sub"] = state.get("sub", 0) + r.outcome.submitted
             state["flr"] = state.get("flr", 0.0) + r.outcome.full_layers_run
+            state["finished"] = state.get("finished", 0) + (1 if r.done else 0)
         if drafter is not None:
-            drafter.observe_results(res, len(live), 1.0, max(eng.last_step_timing()[2], 1e-3))
+            drafter.observe_results(res, len(live), drafter_r(eng),
+                                    max(eng.last_step_timing()[2], 1e-3))
         now = clock()
         for r in res:
             if r.committed:
@@ -357,6 +372,200 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
                 n0 = state["last"].get(r.req_id, (0, 0))[1]
                 state["last"][r.req_id] = (now, n0 + r.committed)
     return tokens
+
+
+def drafter_r(eng):
+    """SM share the AdaptiveDrafter sees (assign_lengths(b, r), drafter.hpp:105-107): the draft
+    lane's share of the overlap plan in force, 1.0 for serial execution (overlap.hpp:14)."""
+    ov = getattr(eng, "overlap_state", None)
+    if ov and ov[0]:
+        return float(ov[2])
+    return 1.0
+
+
+# ---------------------------------------------------------------- backlog + steady state
+REQS_PER_RANK = 1 << 20  # index space per rank: request-sharded replicas own disjoint blocks
+FILL_CAP = 400           # max untimed steps spent bringing the server to steady state
+SWEEP = (1, 8, 32, 128, 256)
+
+
+class Backlog:
+    """The workload's request stream for one rank: request i = (synth_prompt(1, base+i, len_i,
+    V), max_out_i) with lengths from synth_workload's `lens` substream (workload.cpp:77,89-122),
+    generated lazily. `synth` is the prompt generator (the product's C ABI for our arm, the
+    reference's own compiled workload.cpp for the reference arm)."""
+
+    def __init__(self, base, vocab, synth, n_lens=4096):
+        self.base, self.vocab, self.synth = base, vocab, synth
+        self.ins, self.outs = lens(1, base + n_lens, IN_RANGE, OUT_RANGE)
+        self.next = 0
+
+    def take(self):
+        i = self.base + self.next
+        if i >= len(self.ins):
+            self.ins, self.outs = lens(1, 2 * len(self.ins), IN_RANGE, OUT_RANGE)
+        self.next += 1
+        return i, self.synth(i, self.ins[i]), self.outs[i]
+
+
+def product_synth(vocab):
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2604_20503_b200 import engine
+    L = engine.lib()
+
+    def synth(i, n):
+        buf = np.zeros(n, np.int32)
+        assert L.faser_synth_prompt(C.c_uint64(1), i, n, vocab, buf.ctypes.data_as(C.c_void_p)) == 0
+        return buf.tolist()
+    return synth
+
+
+def reference_synth(vocab):
+    """synth_prompt from the reference's own workload.cpp compiled in place (oracle/_ref); the
+    restated C oracle when the reference build is absent. Never loads the product library."""
+    from oracle import pyoracle as po
+    o = po.ref() if os.path.exists(po.REF_SO) else po.restated()
+    return (lambda i, n: list(o.synth_prompt(1, i, n, vocab))), ("reference" if o is not po.restated() else "port")
+
+
+def llama_config(args, world, B):
+    """The `config` object both arms print (identical by construction)."""
+    return {"workload": f"{WORKLOAD_NAMES.get(args.workload, args.workload)}, continuous batching "
+                        f"B={B}/GPU, k={args.k}, mode={args.mode}, steady state (>= one request "
+                        f"lifetime served before warm-up)",
+            "global_batch": B * world, "seq_len": f"in U{list(IN_RANGE)} out U{list(OUT_RANGE)}",
+            "parallelism": f"replicas x{world} (request-sharded)",
+            "l2": "target weights per verify >> 126 MB L2 (inputs larger than L2)"}
+
+
+def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kstats):
+    """One batch size: [fill to steady state] -> W warm-up steps -> K timed steps (device
+    time, CUDA events on the engine stream) -> kernel-class timing steps; optionally the e2e
+    leg on a fresh engine (host prompts submitted inside the timed region, wall clock)."""
+    import torch
+    from paper_2604_20503_b200 import llama as _llama
+    V = desc.target.vocab
+    gate = gate_plan(desc, args)
+    models = _llama.fitted_latency_model()
+    hook = step_plan_hook(desc, args, models)
+    synth = product_synth(V)
+
+    def new_drafter():
+        if args.mode in ("vsd", "ov", "vsd_ee"):
+            return None
+        from paper_2604_20503_b200 import controller
+        return controller.AdaptiveDrafter(models=models)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def session(eng, counting=False):
+        bl = Backlog(shard_base(rank, REQS_PER_RANK), V, synth)
+        io = {"sub": 0, "h2d": 0, "d2h": 0, "counting": False}
+
+        def feeder():
+            if io["counting"]:
+                a, b = eng.last_step_bytes()
+                io["h2d"] += a
+                io["d2h"] += b
+            while eng.pending_work() < B + 2:
+                i, p, m = bl.take()
+                eng.submit(i, p, m)
+                if io["counting"]:
+                    io["sub"] += 4 * len(p)
+        return feeder, io
+
+    def fill(eng, feeder, drafter, clock):
+        st = {"first": {}, "last": {}}
+        n = 0
+        while n < FILL_CAP and st.get("finished", 0) < B:
+            run_llama_steps(eng, 1, clock, st, feeder, gate=gate, drafter=drafter, hook=hook)
+            n += 1
+        return n
+
+    # ------------------------------------------------------------ value (device-timed)
+    eng = make_engine(desc, args, local_rank, batch=B)
+    feeder, _ = session(eng)
+    dev_clock = [0.0]
+
+    def clock():
+        dev_clock[0] += eng.last_step_timing()[2] / 1e3
+        return dev_clock[0]
+
+    drafter = new_drafter()
+    fill_steps = fill(eng, feeder, drafter, clock)
+    run_llama_steps(eng, args.warmup, clock, {"first": {}, "last": {}}, feeder, gate=gate, drafter=drafter,
+                    hook=hook)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = {"first": {}, "last": {}}
+    dev_clock[0] = 0.0
+    launches0 = eng.kernel_launches()
+    acc_ms = {"draft": 0.0, "verify": 0.0}
+
+    def clock_acc():
+        d, v, _ = eng.last_step_timing()
+        acc_ms["draft"] += d
+        acc_ms["verify"] += v
+        return clock()
+
+    sync_all()
+    with Clocks(local_rank) as clk:
+        ev0.record(stream)
+        t0 = time.perf_counter()
+        tokens = run_llama_steps(eng, args.steps, clock_acc, st, feeder, gate=gate, drafter=drafter, hook=hook)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    launches = eng.kernel_launches() - launches0
+    dev_ms = ev0.elapsed_time(ev1)
+    nsteps = max(st.get("steps", 0), 1)
+    out = {"B": B, "dev_ms": dev_ms, "tokens": tokens, "steps_run": st.get("steps", 0), "fill_steps": fill_steps,
+           "p50_tpot_ms": p50_tpot_ms(st["first"], st["last"]), "launches": launches, "clocks": clk.summary(),
+           "wall_s": wall, "draft_ms": acc_ms["draft"] / nsteps, "verify_ms": acc_ms["verify"] / nsteps,
+           "acceptance": st.get("acc", 0) / max(st.get("sub", 1), 1),
+           "layer_work": st.get("flr", 0.0) / max(st.get("sub", 1), 1)}
+    if want_kstats:
+        # per-kernel-class CUDA-event timing over steps that immediately follow the timed region
+        # (event records between launches would perturb the PDL overlap being timed)
+        eng.set_kernel_timing(True)
+        run_llama_steps(eng, max(args.steps // 2, 3), clock, {"first": {}, "last": {}}, feeder, gate=gate,
+                        drafter=drafter, hook=hook)
+        out["kstats"] = eng.kernel_stats()
+        eng.set_kernel_timing(False)
+    eng.close()
+    if not want_e2e:
+        return out
+
+    # ------------------------------------------------------------ e2e (host buffers, wall clock)
+    eng = make_engine(desc, args, local_rank, batch=B)
+    feeder, io = session(eng)
+    drafter2 = new_drafter()
+    fill(eng, feeder, drafter2, time.perf_counter)
+    run_llama_steps(eng, args.warmup, time.perf_counter, {"first": {}, "last": {}}, feeder, gate=gate,
+                    drafter=drafter2, hook=hook)
+    sync_all()
+    io["counting"] = True
+    eng.last_step_bytes()
+    st2 = {"first": {}, "last": {}}
+    t0 = time.perf_counter()
+    tokens2 = run_llama_steps(eng, args.steps, time.perf_counter, st2, feeder, gate=gate, drafter=drafter2,
+                              hook=hook)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    a, b = eng.last_step_bytes()
+    io["h2d"] += a
+    io["d2h"] += b
+    eng.close()
+    n2 = max(st2.get("steps", 0), 1)
+    out["e2e"] = {"s": e2e_s, "tokens": tokens2, "p50_tpot_ms": p50_tpot_ms(st2["first"], st2["last"]),
+                  "h2d_bytes_per_step": int((io["h2d"] + io["sub"]) / n2), "d2h_bytes_per_step": int(io["d2h"] / n2)}
+    return out
 
 
 def llama_ours(args, rank, world, local_rank):
@@ -368,179 +577,110 @@ def llama_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl")
     desc = llama_desc(args.workload)
     B = args.batch
-    V = desc.target.vocab
-    n_req = B * (args.steps + args.warmup) // 40 + 2 * B
-    base = shard_base(rank, n_req)  # request-sharded replicas: each rank owns its own requests
-    prompts, outl = prompts_for(base, n_req, V, IN_RANGE, OUT_RANGE)
-    gate = gate_plan(desc, args)
-    from paper_2604_20503_b200 import llama as _llama
-    models = _llama.fitted_latency_model()  # B200 stage latencies (profiles/r01_latency_model.json)
-    hook = step_plan_hook(desc, args, models)
-
-    def new_drafter():
-        if args.mode in ("vsd", "ov", "vsd_ee"):  # fixed k (vsd_ee: early exit without the k controller)
-            return None
-        from paper_2604_20503_b200 import controller
-        return controller.AdaptiveDrafter(models=models)
-
-    def sync_all():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-
-    # ---------------------------------------------------------------- value (device-timed)
-    eng = make_engine(desc, args, local_rank)
-    for i, (p, m) in enumerate(zip(prompts, outl)):
-        eng.submit(base + i, p, m)
-    st = {"first": {}, "last": {}}
-    dev_clock = [0.0]
-
-    def clock():
-        dev_clock[0] += eng.last_step_timing()[2] / 1e3
-        return dev_clock[0]
-
-    drafter = new_drafter()
-    run_llama_steps(eng, args.warmup, clock, st, gate=gate, drafter=drafter, hook=hook)
-    stream = torch.cuda.ExternalStream(eng.stream_ptr())
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st = {"first": {}, "last": {}}
-    dev_clock[0] = 0.0
-    launches0 = eng.kernel_launches()
-    draft_ms = verify_ms = 0.0
-    nsteps = [0]
-    sync_all()
-
-    def clock_acc():
-        nonlocal draft_ms, verify_ms
-        d, v, _ = eng.last_step_timing()
-        draft_ms += d
-        verify_ms += v
-        nsteps[0] += 1
-        return clock()
-
-    with Clocks(local_rank) as clk:
-        ev0.record(stream)
-        t0 = time.perf_counter()
-        tokens = run_llama_steps(eng, args.steps, clock_acc, st, gate=gate, drafter=drafter, hook=hook)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    launches = eng.kernel_launches() - launches0
-    dev_ms = ev0.elapsed_time(ev1)
-    tpot = p50_tpot_ms(st["first"], st["last"])
-    # per-kernel-class CUDA-event timing over steps that immediately follow the timed region
-    # (same engine and workload state; kept out of the timed region so event records cannot
-    # perturb the programmatic-dependent-launch overlap being measured)
-    eng.set_kernel_timing(True)
-    run_llama_steps(eng, max(args.steps // 2, 3), clock, {"first": {}, "last": {}}, gate=gate,
-                    drafter=drafter, hook=hook)
-    kstats = eng.kernel_stats()
-    eng.set_kernel_timing(False)
-    eng.close()
-
-    # ---------------------------------------------------------------- e2e (host buffers)
-    eng = make_engine(desc, args, local_rank)
-    nxt = [0]
-    sub_bytes = [0]
-    h2d = [0]
-    d2h = [0]
-
-    def feeder():
-        while eng.pending_work() < B + 2 and nxt[0] < len(prompts):
-            i = nxt[0]
-            eng.submit(base + i, prompts[i], outl[i])
-            sub_bytes[0] += 4 * len(prompts[i])
-            nxt[0] += 1
-
-    st2 = {"first": {}, "last": {}}
-    drafter2 = new_drafter()
-    run_llama_steps(eng, args.warmup, time.perf_counter, st2, feeder, gate=gate, drafter=drafter2, hook=hook)
-
-    def feeder_counting():
-        a, b = eng.last_step_bytes()
-        h2d[0] += a
-        d2h[0] += b
-        feeder()
-
-    sub_bytes[0] = 0
-    sync_all()
-    st2 = {"first": {}, "last": {}}
-    t0 = time.perf_counter()
-    tokens2 = run_llama_steps(eng, args.steps, time.perf_counter, st2, feeder_counting, gate=gate,
-                              drafter=drafter2, hook=hook)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    e2e_tpot = p50_tpot_ms(st2["first"], st2["last"])
-    eng.close()
-
-    stats = torch.tensor([dev_ms, float(tokens), e2e_s, float(tokens2)], dtype=torch.float64, device="cuda")
-    dev_ms, tokens, e2e_s, tokens2 = aggregate(stats, dist)
+    head = serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e=True, want_kstats=True)
+    points = [head]
+    if not args.no_sweep:
+        for b in SWEEP:
+            if b != B:
+                points.append(serve_point(args, desc, b, rank, world, local_rank, dist, want_e2e=False,
+                                          want_kstats=True))
+    # whole-job reduction per point: device time / wall = max over ranks, tokens = sum
+    agg = []
+    for p in points:
+        e = p.get("e2e", {"s": 0.0, "tokens": 0})
+        stats = torch.tensor([p["dev_ms"], float(p["tokens"]), e["s"], float(e["tokens"])], dtype=torch.float64,
+                             device="cuda")
+        agg.append(aggregate(stats, dist))
     if rank != 0:
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
         return
-    k = max(nsteps[0], 1)
+    dev_ms, tokens, e2e_s, tokens2 = agg[0]
     line = {
         "metric": METRIC, "value": tokens / (dev_ms / 1e3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "steps_executed": head["steps_run"],
+        "ms_per_step": dev_ms / max(head["steps_run"], 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts (synth_prompt), random-init weights",
-        "p50_tpot_ms": tpot,
-        "config": {"workload": f"{WORKLOAD_NAMES.get(args.workload, args.workload)}, "
-                               f"continuous batching B={B}/GPU, k={args.k}, mode={args.mode}",
-                   "global_batch": B * world, "seq_len": f"in U{list(IN_RANGE)} out U{list(OUT_RANGE)}",
-                   "parallelism": f"replicas x{world} (request-sharded)",
-                   "l2": "target weights per verify >> 126 MB L2 (inputs larger than L2)"},
-        "e2e": {"value": tokens2 / e2e_s, "unit": UNIT, "p50_tpot_ms": e2e_tpot,
-                "h2d_bytes_per_step": int((h2d[0] + sub_bytes[0]) / max(args.steps, 1)),
-                "d2h_bytes_per_step": int(d2h[0] / max(args.steps, 1))},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-        "device_ms_per_step": {"draft": draft_ms / k, "verify_accept": verify_ms / k},
-        "acceptance": st.get("acc", 0) / max(st.get("sub", 1), 1),
-        "layer_work_per_drafted_token": st.get("flr", 0.0) / max(st.get("sub", 1), 1),
-        "wall_s_timed": wall,
+        "p50_tpot_ms": head["p50_tpot_ms"],
+        "config": llama_config(args, world, B),
+        "e2e": {"value": tokens2 / e2e_s, "unit": UNIT, "p50_tpot_ms": head["e2e"]["p50_tpot_ms"],
+                "h2d_bytes_per_step": head["e2e"]["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": head["e2e"]["d2h_bytes_per_step"]},
+        "gpu_launches": int(head["launches"]),
+        "clocks": head["clocks"],
+        "device_ms_per_step": {"draft": head["draft_ms"], "verify_accept": head["verify_ms"]},
+        "acceptance": head["acceptance"],
+        "layer_work_per_drafted_token": head["layer_work"],
+        "fill_steps": head["fill_steps"],
+        "wall_s_timed": head["wall_s"],
     }
-    line["roofline"], line["kernels"] = kernel_roofline(kstats)
-    line["verify_forward_roofline"] = llama_roofline(desc, B, args.k, verify_ms / k, draft_ms / k)
+    line["roofline"], line["kernels"] = kernel_roofline(head["kstats"], B * args.k)
+    line["verify_forward_roofline"] = llama_roofline(desc, B, args.k, head["verify_ms"])
+    sweep = []
+    for p, (d_ms, tok, _, _) in zip(points, agg):
+        roof, _ = kernel_roofline(p["kstats"], p["B"] * args.k)
+        sweep.append({"batch": p["B"], "global_batch": p["B"] * world, "value": tok / (d_ms / 1e3),
+                      "p50_tpot_ms": p["p50_tpot_ms"], "ms_per_step": d_ms / max(p["steps_run"], 1),
+                      "steps_executed": p["steps_run"], "fill_steps": p["fill_steps"],
+                      "acceptance": p["acceptance"], "clocks_sm_mhz": p["clocks"]["sm_mhz"],
+                      "roofline": roof})
+    line["batch_sweep"] = sorted(sweep, key=lambda x: x["batch"])
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = llama_cpu_baseline(desc, args, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = llama_cpu_sample(desc, args, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def kernel_roofline(kstats):
-    """roofline object for the dominant kernel class (largest device time), achieved =
-    algorithmic bytes per launch / average launch duration (CUDA events around each launch)."""
+def kernel_roofline(kstats, rows):
+    """roofline object for the dominant kernel class (largest device time). `rows` = verify rows
+    per step (B*k): below the ridge (peak flops / peak bytes, ~216 rows for bf16 on B200) the
+    GEMM classes are HBM-bound (achieved = algorithmic bytes per launch / average launch time vs
+    the measured copy bandwidth), above it tensor-bound (algorithmic flops per launch / time vs
+    the sustained bf16 matmul rate). Attention classes are always HBM-bound."""
     pk, src = peaks()
+    ridge = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12 / (pk["hbm_gbs"] * 1e9)
     table = {}
     for name, v in kstats.items():
         if v["launches"]:
             gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            tfs = v.get("flops", 0.0) / (v["ms"] * 1e-3) / 1e12
             table[name] = {"avg_us": 1e3 * v["ms"] / v["launches"], "launches": v["launches"],
                            "bytes_per_launch": v["bytes"] / v["launches"], "achieved_GBs": gbs,
-                           "frac_hbm": gbs / pk["hbm_gbs"], "total_ms": v["ms"]}
+                           "frac_hbm": gbs / pk["hbm_gbs"], "total_ms": v["ms"],
+                           "flops_per_launch": v.get("flops", 0.0) / v["launches"], "achieved_TFs": tfs}
     if not table:
         return None, table
     top = max(table, key=lambda n: table[n]["total_ms"])
     t = table[top]
+    tensor = "gemm" in top or "lm_head" in top
+    tensor = tensor and rows >= ridge and t["flops_per_launch"] > 0
     traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, committed ncu capture
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            traffic = json.load(f)["classes"][top]["traffic_bytes_per_launch"]
-    except Exception:
-        pass
-    roof = {"bound": "hbm", "achieved": t["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": t["achieved_GBs"] / pk["hbm_gbs"], "traffic": traffic, "peak_source": src,
-            "kernel": top, "avg_launch_us": t["avg_us"], "bytes_per_launch": t["bytes_per_launch"],
-            "share_of_timed_kernels": t["total_ms"] / sum(x["total_ms"] for x in table.values())}
+    for fn in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                traffic = json.load(f)["classes"][top]["traffic_bytes_per_launch"]
+            break
+        except Exception:
+            pass
+    share = t["total_ms"] / sum(x["total_ms"] for x in table.values())
+    if tensor:
+        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        roof = {"bound": "tensor", "achieved": t["achieved_TFs"], "peak": peak, "unit": "TFLOP/s",
+                "frac": t["achieved_TFs"] / peak, "traffic": traffic, "peak_source": src + " bf16_tflops_sustained"}
+    else:
+        roof = {"bound": "hbm", "achieved": t["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": t["achieved_GBs"] / pk["hbm_gbs"], "traffic": traffic, "peak_source": src + " hbm_gbs"}
+    roof.update({"kernel": top, "avg_launch_us": t["avg_us"], "bytes_per_launch": t["bytes_per_launch"],
+                 "flops_per_launch": t["flops_per_launch"], "rows": rows, "ridge_rows": ridge,
+                 "share_of_timed_kernels": share})
     return roof, table
 
 
-def llama_roofline(desc, B, k, verify_ms, draft_ms):
+def llama_roofline(desc, B, k, verify_ms):
     """Dominant path = the verify forward (target weights streamed once per step). Algorithmic
     bytes per verify = 2 * target params (bf16) + KV read (sum ctx * KV bytes/token), SURVEY 8(d)."""
     pk, src = peaks()
@@ -558,43 +698,56 @@ def llama_roofline(desc, B, k, verify_ms, draft_ms):
             "algorithmic_bytes": bytes_, "rows_per_verify": B * k}
 
 
-def llama_cpu_baseline(desc, args, budget_s=20.0):
-    """Bounded sample on the host cores: the reference's SD semantics over the fp32 oracle
-    models (oracle/lmsd.py) for 2 requests of the workload, prompts capped at 256 tokens,
-    timed over decode rounds only (prefill untimed)."""
+def llama_cpu_sample(desc, args, budget_s=20.0):
+    """The reference's speculative-decoding semantics on the host cores over the fp32 oracle
+    models (oracle/lmsd.py: draft_tokens / full_verify / commit of sdcore.cpp:45-197 with the
+    transformer pair in place of LayeredToyLM; the reference has no transformer). SAME workload
+    as the GPU arm: requests of the same backlog in order (prompts from the reference's own
+    compiled synth_prompt, lengths from the `lens` substream), k fixed. The reference engine's
+    API is per request (SpeculativeEngine methods take one Request, sdcore.hpp:81-116), so a
+    batch of B live requests costs the sum of their per-request rounds and throughput does not
+    depend on B: the bounded sample is whole request lifetimes (admission prefill + every round
+    to completion), run one after another until `budget_s` is spent. Never loads the product
+    library."""
     from oracle import lmsd
     threads = os.cpu_count() or 1
-    prompts, outl = prompts_for(0, 2, desc.target.vocab, IN_RANGE, OUT_RANGE)
+    V = desc.target.vocab
+    synth, kind = reference_synth(V)
+    bl = Backlog(0, V, synth, n_lens=64)
     sd = lmsd.OracleSD(desc, threads)
-    for i, p in enumerate(prompts):
-        sd.submit(i, p[:256], outl[i])
-    tok = 0
-    rounds = 0
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        live = [i for i in sd.reqs if not sd.reqs[i].done]
-        if not live:
-            break
-        for i in live:
+    tok = rounds = nreq = 0
+    spent = 0.0
+    prefill_tok = 0
+    while spent < budget_s and nreq < 64:
+        t0 = time.perf_counter()
+        i, p, m = bl.take()
+        sd.submit(i, p, m)
+        while not sd.reqs[i].done:
             tok += sd.round(i, args.k)[3]
-        rounds += 1
-    dt = time.perf_counter() - t0
+            rounds += 1
+        spent += time.perf_counter() - t0
+        sd.release(i)
+        nreq += 1
+        prefill_tok += len(p)
     sd.close()
-    return {"value": tok / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle/lmsd.py fp32 SD loop (reference semantics, builder oracle: the "
-                      f"reference has no transformer), 2 requests x {rounds} rounds, k={args.k}, "
-                      f"prompts capped at 256 tokens, {tok} tokens in {dt:.1f} s"}
+    return {"value": tok / spent, "unit": UNIT, "cores": threads, "kind": "port",
+            "prompts": kind, "seconds": spent, "rounds": rounds, "ms_per_round": 1e3 * spent / max(rounds, 1),
+            "sample": f"oracle/lmsd.py fp32 (reference SD control flow over the builder's fp32 Llama oracle; "
+                      f"the reference has no transformer), first {nreq} requests of the same backlog run to "
+                      f"completion one at a time (per-request engine API): {prefill_tok} prompt tokens "
+                      f"prefilled, {rounds} rounds, {tok} tokens committed in {spent:.1f} s, k={args.k}"}
 
 
 def llama_reference(args, rank, world):
     if rank != 0:
         return
     desc = llama_desc(args.workload)
-    cb = llama_cpu_baseline(desc, args, budget_s=max(5.0, min(60.0, 2.0 * (args.steps + args.warmup))))
-    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"config 3 (CPU, oracle port), k={args.k}", "global_batch": args.batch},
+    cb = llama_cpu_sample(desc, args, budget_s=args.cpu_budget)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_round"],
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic prompts (synth_prompt), random-init weights",
+            "config": llama_config(args, world, args.batch),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -686,7 +839,7 @@ def toy_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "tiny", "tp_tiny", "toy"])
@@ -698,6 +851,7 @@ def main():
     ap.add_argument("--gate-layer", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the embedded batch sweep")
     ap.add_argument("--trace", type=float, default=0.0,
                     help="replay a bursty arrival trace of this many seconds instead of a fixed backlog")
     ap.add_argument("--trace-rate", type=float, default=26.0, help="mean arrival rate (req/s) of --trace")

@@ -303,6 +303,9 @@ faser_status faser_debug_weights(faser_engine* e, int32_t model, int32_t which, 
 faser_status faser_set_kernel_timing(faser_engine* e, int32_t enabled);
 faser_status faser_kernel_stats(faser_engine* e, int32_t cls, double* ms, int64_t* launches,
                                 double* bytes);
+/* Algorithmic flops accumulated by the same timed launches (2 * N * K * rows for the GEMM
+ * classes, 0 for attention): the tensor-pipe roofline basis when verify is TC-bound. */
+faser_status faser_kernel_flops(faser_engine* e, int32_t cls, double* flops);
 
 /* ABI self-description: FASER_ABI_VERSION and sizeof() of every struct above, in
  * declaration order (toy_params, exit_policy, gate_plan, gate_entry, overlap_plan,

@@ -161,6 +161,15 @@ int lmo_weight(const lmo_model* m, int which, int layer, int64_t idx, uint16_t* 
   return 0;
 }
 
+/* Copies n bf16 elements [idx, idx + n) of one tensor (same `which` codes) — lets an
+ * independent forward (tests/test_llama_oracle_torch.py) run on exactly these weights. */
+int lmo_weight_block(const lmo_model* m, int which, int layer, int64_t idx, int64_t n, uint16_t* out) {
+  const uint16_t* p = which == 0 ? m->lm : which == 1 ? m->emb : which == 2 ? m->layers[layer].wqkv
+                    : which == 3 ? m->layers[layer].wo : which == 4 ? m->layers[layer].wgu : m->layers[layer].wd;
+  memcpy(out, p + idx, (size_t)n * 2);
+  return 0;
+}
+
 lmo_cache* lmo_cache_create(const lmo_model* m, int max_len) {
   lmo_cache* c = (lmo_cache*)calloc(1, sizeof(lmo_cache));
   c->max_len = max_len;
@@ -182,21 +191,48 @@ int lmo_cache_truncate(lmo_cache* c, int len) {
 }
 int lmo_cache_len(const lmo_cache* c) { return c->len; }
 
-/* y[t][n] = sum_k x[t][k] * w[n][k] (w bf16 [N][K]) */
+/* y[t][n] = sum_k x[t][k] * w[n][k] (w bf16 [N][K]). Weight rows are converted in blocks of NB
+ * so each activation row is read once per block (cache-resident) instead of once per weight row;
+ * every output element is still one k-ordered simd dot product. */
+#define NB 32
 static void matmul(const float* x, int T, int K, const uint16_t* w, int N, float* y) {
 #pragma omp parallel
   {
-    float* wr = (float*)malloc((size_t)K * 4);
+    float* wr = (float*)malloc((size_t)K * 4 * NB);
 #pragma omp for schedule(static)
-    for (int n = 0; n < N; ++n) {
-      const uint16_t* src = w + (int64_t)n * K;
-      for (int k = 0; k < K; ++k) wr[k] = bf2f(src[k]);
+    for (int n0 = 0; n0 < N; n0 += NB) {
+      const int nb = N - n0 < NB ? N - n0 : NB;
+      for (int i = 0; i < nb; ++i) {
+        const uint16_t* src = w + (int64_t)(n0 + i) * K;
+        for (int k = 0; k < K; ++k) wr[(size_t)i * K + k] = bf2f(src[k]);
+      }
       for (int t = 0; t < T; ++t) {
         const float* xr = x + (int64_t)t * K;
-        float acc = 0.f;
+        int i = 0;
+        for (; i + 4 <= nb; i += 4) {  // 4 weight rows per activation load (independent dots)
+          const float *w0 = wr + (size_t)i * K, *w1 = w0 + K, *w2 = w1 + K, *w3 = w2 + K;
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma omp simd reduction(+ : a0, a1, a2, a3)
+          for (int k = 0; k < K; ++k) {
+            const float xv = xr[k];
+            a0 += xv * w0[k];
+            a1 += xv * w1[k];
+            a2 += xv * w2[k];
+            a3 += xv * w3[k];
+          }
+          float* yo = y + (int64_t)t * N + n0 + i;
+          yo[0] = a0;
+          yo[1] = a1;
+          yo[2] = a2;
+          yo[3] = a3;
+        }
+        for (; i < nb; ++i) {
+          const float* wi = wr + (size_t)i * K;
+          float acc = 0.f;
 #pragma omp simd reduction(+ : acc)
-        for (int k = 0; k < K; ++k) acc += xr[k] * wr[k];
-        y[(int64_t)t * N + n] = acc;
+          for (int k = 0; k < K; ++k) acc += xr[k] * wi[k];
+          y[(int64_t)t * N + n0 + i] = acc;
+        }
       }
     }
     free(wr);

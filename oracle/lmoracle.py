@@ -29,6 +29,7 @@ def lib():
                                  C.c_void_p, C.c_void_p]
         L.lmo_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p]
         L.lmo_set_threads.argtypes = [C.c_int]
+        L.lmo_weight_block.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p]
         _L = L
     return _L
 
@@ -56,6 +57,18 @@ class Model:
         out = C.c_uint16()
         lib().lmo_weight(self.h, which, layer, idx, C.byref(out))
         return out.value
+
+    def tensor(self, which, layer=0):
+        """A whole bf16 tensor as uint16 [rows][cols] (which: 0 lm, 1 emb, 2 wqkv, 3 wo, 4 wgu
+        (interleaved 64-row gate/up groups), 5 wd)."""
+        s = self.shape
+        d, F, V = s.d_model, s.ffn, s.vocab
+        qkv = (s.n_heads + 2 * s.n_kv_heads) * s.head_dim
+        qd = s.n_heads * s.head_dim
+        rows, cols = {0: (V, d), 1: (V, d), 2: (qkv, d), 3: (d, qd), 4: (2 * F, d), 5: (d, F)}[which]
+        out = np.zeros((rows, cols), np.uint16)
+        assert lib().lmo_weight_block(self.h, which, layer, 0, rows * cols, _p(out)) == 0
+        return out
 
     def logits(self, tokens, rows_from, layers=None):
         """Logits of positions rows_from..len(tokens)-1 after each layer count in `layers`

@@ -124,6 +124,12 @@ class OracleSD:
         acc, rec = self.full_verify(rid, d)
         return d, acc, rec, self.commit(rid, d, acc, rec)
 
+    def release(self, rid):
+        """Frees a finished request's KV caches."""
+        L = lmoracle.lib()
+        for c in self.caches.pop(rid, ()):
+            L.lmo_cache_destroy(c)
+
     def close(self):
         L = lmoracle.lib()
         for cd, ct in self.caches.values():

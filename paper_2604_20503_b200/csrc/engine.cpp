@@ -528,6 +528,11 @@ faser_status faser_kernel_stats(faser_engine* e, int32_t cls, double* ms, int64_
   return faser::llama_kernel_stats(e->llama, cls, ms, launches, bytes);
 }
 
+faser_status faser_kernel_flops(faser_engine* e, int32_t cls, double* flops) {
+  if (!e || !e->llama) return FASER_EINVAL;
+  return faser::llama_kernel_flops(e->llama, cls, flops);
+}
+
 faser_status faser_debug_kv_pages(faser_engine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n) {
   if (!e || !n || !e->llama) return FASER_EINVAL;
   return faser::llama_debug_kv_pages(e->llama, req_id, pages, cap, n);

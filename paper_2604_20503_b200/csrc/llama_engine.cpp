@@ -628,11 +628,11 @@ class LlamaEngine {
   struct KPend {
     int cls;
     cudaEvent_t a, b;
-    double bytes;
+    double bytes, flops;
   };
   std::vector<KPend> kpend;
   std::vector<cudaEvent_t> kpool;
-  double k_ms[kClasses] = {}, k_bytes[kClasses] = {};
+  double k_ms[kClasses] = {}, k_bytes[kClasses] = {}, k_flops[kClasses] = {};
   int64_t k_n[kClasses] = {};
   cudaEvent_t kev() {
     if (kpool.empty()) {
@@ -645,12 +645,12 @@ class LlamaEngine {
     return e;
   }
   template <class F>
-  void timed(int cls, double bytes, F&& launch) {
+  void timed(int cls, double bytes, F&& launch, double flops = 0.0) {
     if (!ktiming || capturing || cls < 0) {
       launch();
       return;
     }
-    KPend p{cls, kev(), kev(), bytes};
+    KPend p{cls, kev(), kev(), bytes, flops};
     LCK(cudaEventRecord(p.a, fs));
     launch();
     LCK(cudaEventRecord(p.b, fs));
@@ -663,6 +663,7 @@ class LlamaEngine {
       LCK(cudaEventElapsedTime(&ms, p.a, p.b));
       k_ms[p.cls] += ms;
       k_bytes[p.cls] += p.bytes;
+      k_flops[p.cls] += p.flops;
       k_n[p.cls] += 1;
       kpool.push_back(p.a);
       kpool.push_back(p.b);
@@ -787,6 +788,7 @@ class LlamaEngine {
     auto gbytes = [&](int64_t n_out, int64_t k, int64_t out_cols) {
       return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * out_cols;
     };
+    auto gflops = [&](int64_t n_out, int64_t k) { return 2.0 * n_out * k * T; };
     // attention: the K/V bytes every request reads (its context incl. the new rows) + q/o
     const double abytes = static_cast<double>(f.kv_tokens) * 2 * s.n_kv * s.hd * 2 + 4.0 * T * s.n_q * s.hd;
     // timing experiments only (FASER_SKIP bitmask, target verify forward): 1 attention, 2 qkv,
@@ -798,7 +800,7 @@ class LlamaEngine {
       e_qkv.layer = l;
       if (!(skip & 2))
       timed(gcls, gbytes(s.qkv_out(), s.d, s.qkv_out()),
-            [&] { LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, fs)); });
+            [&] { LCK(gemm_fused(m.op_qkv[l], w.op_xb, T, p_qkv, e_qkv, fs)); }, gflops(s.qkv_out(), s.d));
       if (!(skip & 1))
       timed(acls, abytes, [&] {
         LCK(lm_attention(s, rows, f.n_req, f.max_rows, f.max_ctx, kv, l, w.q.as<__nv_bfloat16>(),
@@ -814,13 +816,16 @@ class LlamaEngine {
       if (tp_rows)
         row_parallel(m.op_o[l], w.op_ob, p_o);
       else if (!(skip & 4))
-        timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); });
+        timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); },
+              gflops(s.d, qd));
       if (!(skip & 8))
-      timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); });
+      timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); },
+            gflops(2 * s.ffn, s.d));
       if (tp_rows)
         row_parallel(m.op_d[l], w.op_h, p_d);
       else if (!(skip & 16))
-        timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); });
+        timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); },
+              gflops(s.d, s.ffn));
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
@@ -836,7 +841,7 @@ class LlamaEngine {
     }
     if (f.logits) {
       timed(is_target ? 4 : 2, gbytes(s.vocab, s.d, 2 * s.vocab),
-            [&] { LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs)); });
+            [&] { LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs)); }, gflops(s.vocab, s.d));
       if (is_tp_target) {  // vocab-parallel greedy argmax: all-gather (max, lowest global id) per row
         LCK(tp_local_argmax(s.vocab / 128, T, w.amax.as<float2>(), tp_loc.as<float2>(), fs));
         LCK(tpg->allgather_f2(tp_rank, tp_loc.as<float2>(), tp_all.as<float2>(), static_cast<size_t>(T), fs));
@@ -1575,7 +1580,7 @@ faser_status llama_set_kernel_timing(LlamaEngine* e, int32_t on) {
   return lguard(e, [&] {
     e->ktiming = on != 0;
     for (int c = 0; c < LlamaEngine::kClasses; ++c) {
-      e->k_ms[c] = e->k_bytes[c] = 0.0;
+      e->k_ms[c] = e->k_bytes[c] = e->k_flops[c] = 0.0;
       e->k_n[c] = 0;
     }
   });
@@ -1586,6 +1591,12 @@ faser_status llama_kernel_stats(LlamaEngine* e, int32_t cls, double* ms, int64_t
     if (ms) *ms = e->k_ms[cls];
     if (launches) *launches = e->k_n[cls];
     if (bytes) *bytes = e->k_bytes[cls];
+  });
+}
+faser_status llama_kernel_flops(LlamaEngine* e, int32_t cls, double* flops) {
+  return lguard(e, [&] {
+    if (cls < 0 || cls >= LlamaEngine::kClasses) throw LFail{FASER_EINVAL, "unknown kernel class"};
+    if (flops) *flops = e->k_flops[cls];
   });
 }
 }  // namespace faser

@@ -39,6 +39,7 @@ faser_status llama_debug_weights(LlamaEngine* e, int32_t model, int32_t which, i
                                  int32_t n, uint16_t* out);
 faser_status llama_set_kernel_timing(LlamaEngine* e, int32_t on);
 faser_status llama_kernel_stats(LlamaEngine* e, int32_t cls, double* ms, int64_t* launches, double* bytes);
+faser_status llama_kernel_flops(LlamaEngine* e, int32_t cls, double* flops);
 faser_status llama_debug_kv_pages(LlamaEngine* e, int64_t req_id, int32_t* pages, int32_t cap, int32_t* n);
 
 }  // namespace faser

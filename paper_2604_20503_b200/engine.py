@@ -289,6 +289,7 @@ class ServingEngine:
         """OverlapPlan (overlap.hpp:11-17): in MODE_FULL, frontier chunk q of the drafted tokens
         is verified on a second lane while chunk q+1 is drafted."""
         self.plan.overlap = abi.OverlapPlan(1 if enabled else 0, chunk, r, 0.0, 0.0)
+        self.overlap_state = (bool(enabled), chunk, r)
 
     def step(self):
         n = C.c_int32()
@@ -334,7 +335,9 @@ class ServingEngine:
         for i, name in enumerate(self.KERNEL_CLASSES):
             ms, n, b = C.c_double(), C.c_int64(), C.c_double()
             _check(lib().faser_kernel_stats(self.h, i, C.byref(ms), C.byref(n), C.byref(b)), self.h)
-            out[name] = {"ms": ms.value, "launches": n.value, "bytes": b.value}
+            f = C.c_double()
+            _check(lib().faser_kernel_flops(self.h, i, C.byref(f)), self.h)
+            out[name] = {"ms": ms.value, "launches": n.value, "bytes": b.value, "flops": f.value}
         return out
 
     # ---- Llama validation hooks (cfg.debug_capture = 1)
