@@ -314,15 +314,17 @@ def gate_plan(desc, args):
     return abi.GatePlan(args.gate_layer, args.gate_layer + 1, 1.0)
 
 
-def step_plan_hook(desc, args, models):
-    """Per-step controller decisions that need the batch: the early-exit gate (make_gate_plan,
-    r pinned at 0.5 as should_prune requires r in (0,1)) and the overlap plan (plan_overlap)."""
+def step_plan_hook(desc, args, models, book=None):
+    """Per-step controller decisions that need the batch: the early-exit gate (make_gate_plan
+    with GateEntry.accept_estimate from the AcceptanceBook `book` (drafter.cpp:151-161), r pinned
+    at 0.5 as should_prune requires r in (0,1)) and the overlap plan (plan_overlap)."""
     from paper_2604_20503_b200 import engine
     L = desc.target.layers
 
     def hook(eng, live, ks):
         if args.mode in ("ee", "vsd_ee") and not args.gate_layer:
-            eng.set_gate(engine.make_gate_plan(abi.ExitPolicy.default(), [(k, 0.6) for k in ks],
+            a_hat = book.estimate(live, ks, len(live), 1.0) if book is not None else [0.6] * len(ks)
+            eng.set_gate(engine.make_gate_plan(abi.ExitPolicy.default(), list(zip(ks, a_hat)),
                                                float(len(ks)), 0.5, L, models))
         if args.mode in ("ov", "full"):
             if args.chunk:
@@ -333,7 +335,8 @@ def step_plan_hook(desc, args, models):
     return hook
 
 
-def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=None, chunk=0, hook=None):
+def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=None, chunk=0, hook=None,
+                    book=None):
     """n_steps serving iterations; per-request first/last commit times on `clock`. With a
     drafter (AdaptiveDrafter) the per-request k_i come from assign_lengths before each step and
     the round is fed back with observe_round after it (the reference loop).
@@ -361,9 +364,8 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
             state["sub"] = state.get("sub", 0) + r.outcome.submitted
             state["flr"] = state.get("flr", 0.0) + r.outcome.full_layers_run
             state["finished"] = state.get("finished", 0) + (1 if r.done else 0)
-        if drafter is not None:
-            drafter.observe_results(res, len(live), drafter_r(eng),
-                                    max(eng.last_step_timing()[2], 1e-3))
+        for obs in {id(x): x for x in (drafter, book) if x is not None}.values():
+            obs.observe_results(res, len(live), drafter_r(eng), max(eng.last_step_timing()[2], 1e-3))
         now = clock()
         for r in res:
             if r.committed:
@@ -450,11 +452,17 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
     V = desc.target.vocab
     gate = gate_plan(desc, args)
     models = _llama.fitted_latency_model()
-    hook = step_plan_hook(desc, args, models)
     synth = product_synth(V)
 
     def new_drafter():
         if args.mode in ("vsd", "ov", "vsd_ee"):
+            return None
+        from paper_2604_20503_b200 import controller
+        return controller.AdaptiveDrafter(models=models)
+
+    def new_book():
+        """AcceptanceBook for the early-exit gate when k is fixed (no AdaptiveDrafter choosing k)."""
+        if args.mode not in ("vsd_ee",):
             return None
         from paper_2604_20503_b200 import controller
         return controller.AdaptiveDrafter(models=models)
@@ -484,7 +492,7 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
         st = {"first": {}, "last": {}}
         n = 0
         while n < FILL_CAP and st.get("finished", 0) < B:
-            run_llama_steps(eng, 1, clock, st, feeder, gate=gate, drafter=drafter, hook=hook)
+            run_llama_steps(eng, 1, clock, st, feeder, gate=gate, drafter=drafter, hook=hook, book=book)
             n += 1
         return n
 
@@ -498,9 +506,11 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
         return dev_clock[0]
 
     drafter = new_drafter()
+    book = drafter or new_book()
+    hook = step_plan_hook(desc, args, models, book)
     fill_steps = fill(eng, feeder, drafter, clock)
     run_llama_steps(eng, args.warmup, clock, {"first": {}, "last": {}}, feeder, gate=gate, drafter=drafter,
-                    hook=hook)
+                    hook=hook, book=book)
     stream = torch.cuda.ExternalStream(eng.stream_ptr())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st = {"first": {}, "last": {}}
@@ -518,7 +528,7 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
     with Clocks(local_rank) as clk:
         ev0.record(stream)
         t0 = time.perf_counter()
-        tokens = run_llama_steps(eng, args.steps, clock_acc, st, feeder, gate=gate, drafter=drafter, hook=hook)
+        tokens = run_llama_steps(eng, args.steps, clock_acc, st, feeder, gate=gate, drafter=drafter, hook=hook, book=book)
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -535,7 +545,7 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
         # (event records between launches would perturb the PDL overlap being timed)
         eng.set_kernel_timing(True)
         run_llama_steps(eng, max(args.steps // 2, 3), clock, {"first": {}, "last": {}}, feeder, gate=gate,
-                        drafter=drafter, hook=hook)
+                        drafter=drafter, hook=hook, book=book)
         out["kstats"] = eng.kernel_stats()
         eng.set_kernel_timing(False)
     eng.close()
@@ -546,9 +556,11 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
     eng = make_engine(desc, args, local_rank, batch=B)
     feeder, io = session(eng)
     drafter2 = new_drafter()
+    book = drafter2 or new_book()
+    hook = step_plan_hook(desc, args, models, book)
     fill(eng, feeder, drafter2, time.perf_counter)
     run_llama_steps(eng, args.warmup, time.perf_counter, {"first": {}, "last": {}}, feeder, gate=gate,
-                    drafter=drafter2, hook=hook)
+                    drafter=drafter2, hook=hook, book=book)
     sync_all()
     io["counting"] = True
     eng.last_step_bytes()

@@ -367,6 +367,16 @@ faser_status faser_drafter_observe(faser_drafter* d, int32_t b, double r, double
                                    const int32_t* submitted, const int32_t* accepted, int32_t n);
 /* Drops a finished request's acceptance window. */
 faser_status faser_drafter_release(faser_drafter* d, int64_t req_id);
+/* AcceptanceBook::estimate (drafter.cpp:151-161) for request req_ids[i] at length s[i] in the
+ * (b, r) serving context: request window rate_for(s), else context rate, else context overall,
+ * else request overall, else the cold-start default. Feeds the early-exit gate's GateEntry
+ * accept_estimate (exitctl.hpp GateEntry, exitctl.cpp:19-46). */
+faser_status faser_drafter_estimate(faser_drafter* d, const int64_t* req_ids, const int32_t* s, int32_t n,
+                                    int32_t b, double r, double* a_hat);
+/* The request's AcceptanceWindow (sdcore.cpp:8-35): out[j] = rate_for(qs[j]) for j < nq,
+ * out[nq] = overall(); -1 when empty / unknown. */
+faser_status faser_drafter_request_window(faser_drafter* d, int64_t req_id, const int32_t* qs, int32_t nq,
+                                          double* out);
 /* GpPosterior mu/sigma per candidate of context (b, r) and its round count (for tests). */
 faser_status faser_drafter_posterior(faser_drafter* d, int32_t b, double r, double* mu,
                                      double* sigma, int32_t* rounds);

@@ -30,6 +30,12 @@ faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, in
 /* The launch plan the engine uses for an [n_out x k] weight and t rows: out = {bn, splits, mc,
  * deep}. Host-only (no device needed). */
 faser_status faser_k_gemm_plan(int32_t n_out, int32_t t, int32_t k, int32_t* out4);
+/* faser_k_gemm_bf16_plan with a per-CTA timeline: trace[cta][8] globaltimer stamps (entry, after
+ * griddepcontrol.wait, first stage landed, accumulators complete, split-K reduced, exit); the
+ * grid is (weight tiles / mc, row tiles, splits), cta = (z * gy + y) * gx + x. */
+faser_status faser_k_gemm_bf16_trace(const void* w, const void* x, float* out, int32_t n_out, int32_t t,
+                                     int32_t k, int32_t bn, int32_t splits, void* stream,
+                                     unsigned long long* trace);
 
 /* K3: causal attention of n_req ragged query blocks over the paged KV cache (one layer).
  * q bf16 [rows][n_q][hd]; kv bf16 pool [pages][n_kv][2 (K,V)][64][hd]; ptab int32

@@ -417,6 +417,20 @@ int specref_sine_segments(double mean_rate, double ptv, double duration_ms, int3
 // Per-request speculative length schedule used for bit-exact dynamic-k runs (config 2):
 // k = S[h % |S|], h = hash_combine(hash_combine(mix64(seed), req_id + 1), round + 1),
 // S = DrafterConfig::candidates (drafter.hpp:16). bench.py / tests restate it in Python.
+/* The reference's own AcceptanceWindow (sdcore.cpp:8-35): pushes n rounds (s, submitted,
+ * accepted) with the given window and, after each push, evaluates rate_for(q) for the nq query
+ * lengths and overall(): out[i * (nq + 1) + j] (j = nq is overall). */
+int specref_acceptance_window_replay(const int32_t* s, const int32_t* submitted, const int32_t* accepted,
+                                     int32_t n, int32_t window, const int32_t* qs, int32_t nq, double* out) {
+  specsim::AcceptanceWindow w;
+  for (int i = 0; i < n; ++i) {
+    w.push({s[i], submitted[i], accepted[i]}, window);
+    for (int j = 0; j < nq; ++j) out[static_cast<size_t>(i) * (nq + 1) + j] = w.rate_for(qs[j]);
+    out[static_cast<size_t>(i) * (nq + 1) + nq] = w.overall();
+  }
+  return 0;
+}
+
 int32_t specref_sched_k(uint64_t seed, int64_t req_id, int32_t round) {
   static const int kS[8] = {1, 2, 3, 4, 5, 6, 8, 10};
   const uint64_t h = hash_combine(hash_combine(mix64(seed), static_cast<uint64_t>(req_id) + 1),

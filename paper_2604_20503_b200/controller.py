@@ -60,6 +60,20 @@ class AdaptiveDrafter:
             if x.done:
                 lib().faser_drafter_release(self.h, C.c_int64(x.req_id))
 
+    def estimate(self, req_ids, ks, b, r):
+        """AcceptanceBook::estimate per request at its assigned length (drafter.cpp:151-161)."""
+        ids = np.ascontiguousarray(req_ids, np.int64)
+        s = np.ascontiguousarray(ks, np.int32)
+        out = np.zeros(max(len(ids), 1))
+        _check(lib().faser_drafter_estimate(self.h, _ptr(ids), _ptr(s), len(ids), int(b), C.c_double(r), _ptr(out)))
+        return out[:len(ids)].tolist()
+
+    def request_window(self, req_id, qs):
+        q = np.ascontiguousarray(qs, np.int32)
+        out = np.zeros(len(q) + 1)
+        _check(lib().faser_drafter_request_window(self.h, C.c_int64(req_id), _ptr(q), len(q), _ptr(out)))
+        return out.tolist()
+
     def posterior(self, b, r):
         m = self.cfg.n_candidates
         mu = np.zeros(m)

@@ -346,6 +346,23 @@ faser_status faser_drafter_observe(faser_drafter* d, int32_t b, double r, double
   return FASER_OK;
 }
 
+faser_status faser_drafter_estimate(faser_drafter* d, const int64_t* req_ids, const int32_t* s, int32_t n,
+                                    int32_t b, double r, double* a_hat) {
+  if (!d || b < 1 || (n > 0 && (!req_ids || !s || !a_hat))) return FASER_EINVAL;
+  const Ctx& c = d->ctx[key_of(b, r)];
+  for (int i = 0; i < n; ++i) a_hat[i] = d->estimate(req_ids[i], c, s[i]);
+  return FASER_OK;
+}
+
+faser_status faser_drafter_request_window(faser_drafter* d, int64_t req_id, const int32_t* qs, int32_t nq,
+                                          double* out) {
+  if (!d || (nq > 0 && (!qs || !out))) return FASER_EINVAL;
+  auto it = d->req.find(req_id);
+  for (int j = 0; j < nq; ++j) out[j] = it != d->req.end() ? it->second.rate_for(qs[j]) : -1.0;
+  out[nq] = it != d->req.end() ? it->second.overall() : -1.0;
+  return FASER_OK;
+}
+
 faser_status faser_drafter_release(faser_drafter* d, int64_t req_id) {
   if (!d) return FASER_EINVAL;
   d->req.erase(req_id);

@@ -33,9 +33,19 @@ int num_sms() {
 
 using namespace faser;
 
+extern "C" faser_status faser_k_gemm_bf16_trace(const void* w, const void* x, float* out, int32_t n_out,
+                                                int32_t t, int32_t k, int32_t bn, int32_t splits, void* stream,
+                                                unsigned long long* trace);
+
 extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, int32_t n_out,
                                                int32_t t, int32_t k, int32_t bn, int32_t splits,
                                                void* stream) {
+  return faser_k_gemm_bf16_trace(w, x, out, n_out, t, k, bn, splits, stream, nullptr);
+}
+
+extern "C" faser_status faser_k_gemm_bf16_trace(const void* w, const void* x, float* out, int32_t n_out,
+                                                int32_t t, int32_t k, int32_t bn, int32_t splits, void* stream,
+                                                unsigned long long* trace) {
   // bn may carry a pipeline-depth request in its upper bits: 1000 + bn = shallow, 2000 + bn = deep
   // bn may carry requests in its upper digits: 10000 * mc + 1000 * depth + bn
   const int mc = bn / 10000;
@@ -69,6 +79,7 @@ extern "C" faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, flo
   ea.mode = kEpiStore;
   ea.t_stride = t;
   ea.out = out;
+  ea.trace = trace;
   cudaError_t e = gemm_fused(W, X, t, plan, ea, s);
   return e == cudaSuccess ? FASER_OK : FASER_ECUDA;
 }
@@ -104,9 +115,10 @@ extern "C" faser_status faser_k_attention(const void* q, const void* kv, const i
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FASER_ECUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // request i's slot (page-table row) is i; n_rows is unused by the kernel but kept valid
-  static int* d_slot = nullptr;
-  static int cap = 0;
+  // request i's slot (page-table row) is i; n_rows is unused by the kernel but kept valid.
+  // Per host thread (thread_local): concurrent callers never share or free each other's buffer.
+  thread_local int* d_slot = nullptr;
+  thread_local int cap = 0;
   if (n_req + 1 > cap) {
     if (d_slot) cudaFree(d_slot);
     cap = n_req + 1 > 4096 ? n_req + 1 : 4096;

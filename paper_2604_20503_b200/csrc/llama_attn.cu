@@ -16,6 +16,7 @@
 // Few CTAs + long contexts split over KV (flash-decoding); the LAST split CTA to finish a
 // (request, kv head, block) merges the partial softmax states in split order (deterministic),
 // so there is no separate combine launch.
+#include <mutex>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -503,13 +504,12 @@ cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int
   constexpr int kTile = 64 * HD * 2;
   constexpr int kMerge = (4 * MT * 16 * HD + 128 * MT) * 4;
   constexpr int kSmem = (PPS * 2 * kAttnStages<HD> * kTile > kMerge ? PPS * 2 * kAttnStages<HD> * kTile : kMerge) + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;  // thread-safe: TP ranks launch from several host threads
+  std::call_once(attr_once, [] {
     cudaFuncSetAttribute(attn_kernel<HD, ROWS, MT, PPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    attr = true;
-  }
+  });
   dim3 grid(n_req, m.n_kv, blocks * n_split);
-  static CUtensorMap dummy{};
+  static const CUtensorMap dummy{};  // read-only placeholder when TMA is off
   // TMA page loads (one thread, hardware swizzle) measured equal to the cp.async path on B200
   // (config 3, B = 1/32/128): opt-in FASER_ATTN_TMA=1
   static const bool want_tma = want_tma_env();

@@ -75,6 +75,17 @@ __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
   asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp(const EpiArgs& ea, int i) {
+  if (ea.trace) {
+    const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    ea.trace[cta * 8 + i] = gtimer();
+  }
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -108,6 +119,7 @@ __global__ void __launch_bounds__(128, 1)
   const int nkb = kb1 - kb0;
 
   if (threadIdx.x == 0) {
+    stamp(ea, 0);
     sm100::tma_prefetch(&tmW);
     sm100::tma_prefetch(&tmX);
     for (int s = 0; s < C::kStages; ++s) {
@@ -143,6 +155,7 @@ __global__ void __launch_bounds__(128, 1)
     }
   }
   pdl_wait();  // everything below may read the previous kernel's output
+  if (threadIdx.x == 0) stamp(ea, 1);
   const int T = ea.n_rows ? min(*ea.n_rows, ea.t_stride) : ea.t_stride;
   if (n0 >= T) {  // uniform per CTA: tile entirely past the live rows (early-exit compaction)
     if (producer && pg == 0) {  // drain the prefetched weight tiles before exiting
@@ -186,6 +199,7 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t ph = (i / C::kStages) & 1;
       sm100::mbar_wait(&full[s], ph);
       sm100::tc_fence_after();
+      if (i == 0) stamp(ea, 2);
       const uint64_t db = sm100::desc_sw128(sm100::smem_u32(sB + s * C::kBBytes));
       for (int j = 0; j < ntile; ++j) {  // every weight tile of the stage against the same rows tile
         const uint64_t da = sm100::desc_sw128(sm100::smem_u32(sA + s * C::kAStage + j * kABytes));
@@ -229,6 +243,7 @@ __global__ void __launch_bounds__(128, 1)
   // ------------------------------------------------------------------ epilogue
   sm100::mbar_wait(accum, 0);
   sm100::tc_fence_after();
+  if (threadIdx.x == 0) stamp(ea, 3);
   const int tn = min(BN, T - n0);          // live tokens of this tile
 #pragma unroll 1
   for (int j = 0; j < ntile; ++j) {        // weight tiles of this CTA, one staging pass each
@@ -279,6 +294,7 @@ __global__ void __launch_bounds__(128, 1)
       __syncthreads();
     }
     __syncthreads();  // (the per-token prologue was written by warps 2-3 during the mainloop)
+    if (threadIdx.x == 0 && j == 0) stamp(ea, 4);
 
     // Token-per-warp passes: lane owns 4 consecutive tile rows (float4), a warp covers the 128
     // rows of one token, 4 tokens per pass.
@@ -372,6 +388,7 @@ __global__ void __launch_bounds__(128, 1)
   if (splits > 1) cluster_sync();  // peers may still be reading this CTA's partial
   __syncthreads();                 // the staging tile is reused by the next weight tile
   }
+  if (threadIdx.x == 0) stamp(ea, 5);
 }
 
 // ------------------------------------------------------------------ host side
@@ -538,7 +555,10 @@ static bool plan_override(int n_out, int t, int k, GemmPlan* p) {
     int v[8] = {0, 0, 0, 0, 0, 0, 0, 1}, used = 0, used8 = 0;
     if (sscanf(c, "%d,%d,%d,%d,%d,%d,%d%n", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &used) != 7) return false;
     if (c[used] == ',' && sscanf(c + used, ",%d%n", &v[7], &used8) == 1) used += used8;
-    const bool valid = (v[4] == 32 || v[4] == 64 || v[4] == 128 || v[4] == 256) && (v[5] == 1 || v[5] == 2 || v[5] == 4);
+    // only combinations gemm_fused instantiates (and that fit TMEM): otherwise the entry is
+    // ignored instead of silently launching a different plan than the one requested
+    const bool valid = (v[4] == 32 || v[4] == 64 || v[4] == 128 || v[4] == 256) && (v[5] == 1 || v[5] == 2 || v[5] == 4) &&
+                       !(v[4] > 128 && v[5] > 2) && v[4] * v[5] <= 512;
     if (valid && v[0] == n_out && v[1] == k && t >= v[2] && t <= v[3]) {  // invalid entries are ignored
       const int kb = k / kBK, s1 = v[6] < 1 ? 1 : (v[6] > 8 ? 8 : v[6]);
       const int kps = (kb + s1 - 1) / s1;

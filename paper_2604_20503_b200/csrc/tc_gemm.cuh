@@ -51,6 +51,9 @@ struct EpiArgs {
   float* logits = nullptr;               // kEpiLogits [t][n_out]
   float2* amax = nullptr;                // kEpiLogits [n_out/128][t_stride] (value, idx bits)
   int id_off = 0;                        // kEpiLogits: id of output row 0 (vocab-parallel shard)
+  // optional timeline (tools/layer_chain.py): per CTA 8 globaltimer stamps [cta][8] = entry, after
+  // griddepcontrol.wait, first stage landed, accumulators complete, split-K reduced, exit
+  unsigned long long* trace = nullptr;
 };
 
 // Launch plan: token-tile width and K split (the splits of a tile form one thread-block cluster

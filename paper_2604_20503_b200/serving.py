@@ -104,16 +104,23 @@ class ModeController:
         self.engine = engine
         self.drafter = controller.AdaptiveDrafter(models=models) if mode >= abi.MODE_VSD_AD else None
         self.overlap_on = False
+        self.r = 1.0  # draft-lane SM share of the plan in force (1.0 = serial, overlap.hpp:14)
 
     def plan(self, eng, live):
-        ks = self.drafter.assign_lengths(live, len(live), 1.0) if self.drafter else [self.k] * len(live)
+        b = len(live)
+        ks = self.drafter.assign_lengths(live, b, self.r) if self.drafter else [self.k] * b
         eng.set_spec_lengths(live, ks)
         if self.mode >= abi.MODE_VSD_AD_EE:
             if self.gate_layer:
                 eng.set_gate(abi.GatePlan(self.gate_layer, self.gate_layer + 1, 1.0))
             else:
-                eng.set_gate(self.engine.make_gate_plan(abi.ExitPolicy.default(), [(k, 0.6) for k in ks],
-                                                        float(len(ks)), 0.5, self.L, self.models))
+                # GateEntry.accept_estimate from the AcceptanceBook (drafter.cpp:151-161); the
+                # gate's r is the draft share of the overlap plan, 0.5 when serial because
+                # should_prune needs r in (0,1) (latmodel.cpp:45)
+                a_hat = self.drafter.estimate(live, ks, b, self.r)
+                r_gate = self.r if 0.0 < self.r < 1.0 else 0.5
+                eng.set_gate(self.engine.make_gate_plan(abi.ExitPolicy.default(), list(zip(ks, a_hat)),
+                                                        float(b), r_gate, self.L, self.models))
         self.overlap_on = False
         if self.mode == abi.MODE_FULL:
             if self.chunk:
@@ -123,11 +130,13 @@ class ModeController:
                 p = self.engine.plan_overlap(max(ks), len(ks), models=self.models)
                 eng.set_overlap(bool(p.enabled), max(p.chunk, 1), p.r)
                 self.overlap_on = bool(p.enabled) and p.chunk < max(ks)
+        self.r_used = self.r
+        self.r = float(eng.plan.overlap.r) if self.overlap_on else 1.0
         return ks
 
     def observe(self, res, b, step_ms):
         if self.drafter:
-            self.drafter.observe_results(res, b, 1.0, max(step_ms, 1e-3))
+            self.drafter.observe_results(res, b, getattr(self, "r_used", 1.0), max(step_ms, 1e-3))
 
     def close(self):
         if self.drafter:

@@ -103,3 +103,52 @@ def test_rejects_unknown_length():
         assert e.status == abi.EINVAL
     else:
         raise AssertionError("7 is not in the candidate set")
+
+
+def test_request_window_pinned_to_reference_acceptance_window():
+    """The drafter's per-request window (drafter.cpp ReqWindow) against the reference's OWN
+    AcceptanceWindow (sdcore.cpp:8-35, compiled in place in oracle/_ref): the same rounds pushed
+    through both, rate_for(s) for every s in S and overall() compared bit-for-bit after every
+    push, across the W = 16 eviction boundary and with submitted = 0 rounds."""
+    import ctypes as C
+    import os
+
+    import pytest
+
+    from oracle import pyoracle as po
+    if not os.path.exists(po.REF_SO):
+        pytest.skip("oracle/_ref not built")
+    R = po.ref().lib
+    rng = np.random.default_rng(12)
+    n = 40
+    s = rng.choice(S, size=n).astype(np.int32)
+    sub = np.minimum(s, rng.integers(0, 11, size=n)).astype(np.int32)
+    sub[[3, 17]] = 0
+    acc = np.array([rng.integers(0, x + 1) for x in sub], np.int32)
+    qs = np.array(S, np.int32)
+    cfg = controller.DrafterCfg.default()
+    ref = np.zeros((n, len(S) + 1))
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    assert R.specref_acceptance_window_replay(p(s), p(sub), p(acc), n, cfg.window_request, p(qs), len(S),
+                                              p(ref)) == 0
+    d = controller.AdaptiveDrafter()
+    for i in range(n):
+        d.observe_round(1, 1.0, 1.0, [7], [int(s[i])], [int(sub[i])], [int(acc[i])])
+        got = d.request_window(7, S)
+        assert got == ref[i].tolist(), i
+    d.close()
+
+
+def test_estimate_fallback_chain():
+    """AcceptanceBook::estimate (drafter.cpp:151-161): request window rate for s, then the
+    context's rate for s, then the context overall, then the request overall, then cold start."""
+    cfg = controller.DrafterCfg.default()
+    d = controller.AdaptiveDrafter()
+    assert d.estimate([1], [4], 8, 1.0) == [cfg.cold_start_accept]
+    d.observe_round(8, 1.0, 1.0, [1, 2], [4, 2], [4, 2], [3, 1])
+    a = d.estimate([1, 2, 1, 3], [4, 4, 2, 5], 8, 1.0)
+    assert a[0] == 0.75          # request 1's own window at s = 4
+    assert a[1] == 0.75          # request 2 has no s = 4 round: the context's rate for s = 4
+    assert a[2] == 0.5           # request 1 has no s = 2 round: the context's rate for s = 2
+    assert a[3] == (0.75 + 0.5) / 2  # nobody ran s = 5: the context overall
+    d.close()

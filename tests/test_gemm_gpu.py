@@ -71,3 +71,35 @@ def test_gemm_prefill_shapes_match_fp32(L, n_out, T, K, code, splits):
     torch.cuda.synchronize()
     ref = x.float() @ w.float().t()
     assert (out - ref).abs().max().item() <= 1e-4 * max(ref.abs().max().item(), 1.0) + 1e-3
+
+
+def _check_plan(L, n_out, T, K, code, splits):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(n_out * 5 + T + K + code)
+    w = (torch.randn(n_out, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn(T, K, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.full((T, n_out), float("nan"), device="cuda", dtype=torch.float32)
+    assert L.faser_k_gemm_bf16_plan(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                                    n_out, T, K, code, splits, None) == 0
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().t()
+    assert not torch.isnan(out).any()
+    assert (out - ref).abs().max().item() <= 1e-4 * max(ref.abs().max().item(), 1.0) + 1e-3
+
+
+# pipeline-depth variants the plan rules select (1000 + bn = shallow: 4 stages at 64-wide tiles,
+# 3 at 128-wide; 2000 + bn = deep), with and without a K split, at production row counts
+@pytest.mark.parametrize("code", [1032, 1064, 1128, 1256, 2064, 2128, 2256, 21064, 21128])
+@pytest.mark.parametrize("n_out,T,K,splits", [(11264, 96, 2048, 1), (2048, 160, 5632, 4), (2560, 1000, 2048, 0),
+                                              (6144, 48, 768, 1), (2048, 192, 2048, 3)])
+def test_gemm_pipeline_variants_match_fp32(L, code, n_out, T, K, splits):
+    _check_plan(L, n_out, T, K, code, splits)
+
+
+# planner-driven launches at the exact shapes of the config-3 plan rules (tc_gemm.cu gemm_plan)
+@pytest.mark.parametrize("n_out,T,K", [(2048, 192, 2048), (11264, 96, 2048), (2560, 320, 2048), (6144, 48, 768),
+                                       (2560, 1000, 2048), (11264, 128, 2048), (2048, 128, 5632), (2560, 128, 2048),
+                                       (32000, 128, 2048), (11264, 576, 2048), (2048, 1024, 5632), (11264, 1024, 2048),
+                                       (2560, 768, 2048), (2048, 512, 5632), (11264, 512, 2048)])
+def test_gemm_planner_rule_shapes_match_fp32(L, n_out, T, K):
+    _check_plan(L, n_out, T, K, 0, 0)
