@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define FASER_ABI_VERSION 2
+#define FASER_ABI_VERSION 3
 /* Largest speculative length a request may be assigned in one round (S = {1..10} in the
  * reference, drafter.hpp:16). Bounds per-request outcome arrays. */
 #define FASER_MAX_SPEC 32
@@ -213,7 +213,15 @@ typedef struct faser_step_plan {
   faser_gate_plan gate;         /* used in EE modes; inactive gate == full verify semantics */
   int32_t use_k_table;          /* 1: k_table[layer] replaces exit_policy.k_at */
   int32_t k_table[FASER_MAX_LAYERS + 1];
-  faser_overlap_plan overlap;   /* FULL mode: chunked draft/verify co-execution */
+  faser_overlap_plan overlap;   /* FULL mode: chunked draft/verify co-execution. With
+                                   overlap.r in (0,1) the draft lane runs on a green-context
+                                   partition of round8(r * SMs) SMs and the verify lane on the
+                                   rest; chunk == k runs the two stages back to back on their
+                                   partitions (per-share stage profiling). */
+  int32_t lane_mode;            /* 0: lanes overlap (verify chunk q || draft chunk q+1);
+                                   1: isolated - the same partitions and chunks, serialised (draft
+                                   chunk q+1 waits for verify chunk q), the interference baseline */
+  int32_t reserved_lane;
 } faser_step_plan;
 
 typedef struct faser_round_result {
@@ -270,6 +278,37 @@ faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, floa
 /* Bytes the last faser_step copied host->device (step plan + admissions) and
  * device->host (round results). */
 faser_status faser_last_step_bytes(const faser_engine* e, int64_t* h2d, int64_t* d2h);
+/* PipelineTimeline (overlap.hpp:19-56) of the last overlapped (FULL) step, measured: CUDA events
+ * on the two lanes, times in ms from the step's start. Kinds follow TimelineEvent::Kind. */
+enum { FASER_EV_DRAFT_CHUNK = 0, FASER_EV_VERIFY_CHUNK = 1, FASER_EV_RESET = 2, FASER_EV_COMMIT = 3 };
+typedef struct faser_timeline_event {
+  int32_t kind;
+  int32_t chunk;
+  double start_ms;
+  double end_ms;
+} faser_timeline_event;
+typedef struct faser_timeline_info {
+  int32_t n_events;
+  int32_t n_chunks;
+  int32_t draft_sms;          /* SMs of the draft partition (green context) */
+  int32_t verify_sms;         /* SMs of the verify partition */
+  int32_t green;              /* 1: green-context partitions, 0: plain concurrent streams */
+  int32_t cancelled_draft_steps; /* draft steps cancelled after every frontier was reset */
+  int32_t lane_mode;
+  int32_t survivors;          /* requests whose every drafted token was verified and accepted */
+  /* per chunk q: requests on the frontier with rows in q, its verify rows, and the requests
+   * whose frontier was reset by q's verification (rejection or prune: later chunks cancelled) */
+  int32_t chunk_alive[FASER_MAX_SPEC + 1];
+  int32_t chunk_rows[FASER_MAX_SPEC + 1];
+  int32_t chunk_resets[FASER_MAX_SPEC + 1];
+  int32_t reserved0;
+  double makespan_ms, draft_busy_ms, verify_busy_ms;
+  double wasted_draft_ms;     /* draft chunks no request was left to verify */
+} faser_timeline_info;
+/* Events of the last step into ev[0 .. min(n_events, cap)); FASER_EINVAL if the last step was not
+ * an overlapped Llama step. */
+faser_status faser_last_timeline(const faser_engine* e, faser_timeline_event* ev, int32_t cap,
+                                 faser_timeline_info* info);
 /* The engine's CUDA stream (cudaStream_t) so a caller can record events around steps. */
 void* faser_engine_stream(const faser_engine* e);
 /* Kernel launches issued by this engine since creation (evidence counter). */
@@ -310,7 +349,7 @@ faser_status faser_kernel_flops(faser_engine* e, int32_t cls, double* flops);
 /* ABI self-description: FASER_ABI_VERSION and sizeof() of every struct above, in
  * declaration order (toy_params, exit_policy, gate_plan, gate_entry, overlap_plan,
  * latency_params, latency_model, verify_outcome, model_desc, engine_cfg, step_plan,
- * round_result, llama_shape). Writes min(n, 13) entries. */
+ * round_result, llama_shape, timeline_event, timeline_info). Writes min(n, 15) entries. */
 int32_t faser_abi_version(void);
 faser_status faser_abi_struct_sizes(int64_t* out, int32_t n);
 

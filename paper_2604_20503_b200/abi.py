@@ -110,7 +110,28 @@ class EngineCfg(C.Structure):
 
 class StepPlan(C.Structure):
     _fields_ = [("gate", GatePlan), ("use_k_table", C.c_int32),
-                ("k_table", C.c_int32 * (MAX_LAYERS + 1)), ("overlap", OverlapPlan)]
+                ("k_table", C.c_int32 * (MAX_LAYERS + 1)), ("overlap", OverlapPlan),
+                ("lane_mode", C.c_int32), ("reserved_lane", C.c_int32)]
+
+
+LANES_OVERLAP, LANES_ISOLATED = 0, 1
+EV_DRAFT_CHUNK, EV_VERIFY_CHUNK, EV_RESET, EV_COMMIT = 0, 1, 2, 3
+
+
+class TimelineEvent(C.Structure):
+    """TimelineEvent (overlap.hpp:29-34), measured on the lanes."""
+    _fields_ = [("kind", C.c_int32), ("chunk", C.c_int32), ("start_ms", C.c_double), ("end_ms", C.c_double)]
+
+
+class TimelineInfo(C.Structure):
+    """PipelineTimeline totals (overlap.hpp:49-56) + the partitions and the frontier per chunk."""
+    _fields_ = [("n_events", C.c_int32), ("n_chunks", C.c_int32), ("draft_sms", C.c_int32),
+                ("verify_sms", C.c_int32), ("green", C.c_int32), ("cancelled_draft_steps", C.c_int32),
+                ("lane_mode", C.c_int32), ("survivors", C.c_int32),
+                ("chunk_alive", C.c_int32 * (MAX_SPEC + 1)), ("chunk_rows", C.c_int32 * (MAX_SPEC + 1)),
+                ("chunk_resets", C.c_int32 * (MAX_SPEC + 1)), ("reserved0", C.c_int32),
+                ("makespan_ms", C.c_double), ("draft_busy_ms", C.c_double), ("verify_busy_ms", C.c_double),
+                ("wasted_draft_ms", C.c_double)]
 
 
 class RoundResult(C.Structure):

@@ -79,13 +79,13 @@ int32_t faser_abi_version(void) { return FASER_ABI_VERSION; }
 
 faser_status faser_abi_struct_sizes(int64_t* out, int32_t n) {
   if (!out) return FASER_EINVAL;
-  const int64_t sizes[13] = {
+  const int64_t sizes[15] = {
       sizeof(faser_toy_params),    sizeof(faser_exit_policy),   sizeof(faser_gate_plan),
       sizeof(faser_gate_entry),    sizeof(faser_overlap_plan),  sizeof(faser_latency_params),
       sizeof(faser_latency_model), sizeof(faser_verify_outcome), sizeof(faser_model_desc),
       sizeof(faser_engine_cfg),    sizeof(faser_step_plan),     sizeof(faser_round_result),
-      sizeof(faser_llama_shape)};
-  for (int i = 0; i < n && i < 13; ++i) out[i] = sizes[i];
+      sizeof(faser_llama_shape),   sizeof(faser_timeline_event), sizeof(faser_timeline_info)};
+  for (int i = 0; i < n && i < 15; ++i) out[i] = sizes[i];
   return FASER_OK;
 }
 

@@ -495,6 +495,13 @@ faser_status faser_last_step_bytes(const faser_engine* e, int64_t* h2d, int64_t*
   return FASER_OK;
 }
 
+faser_status faser_last_timeline(const faser_engine* e, faser_timeline_event* ev, int32_t cap,
+                                 faser_timeline_info* info) {
+  if (!e || !info || cap < 0 || (cap > 0 && !ev)) return FASER_EINVAL;
+  if (!e->llama) return FASER_EINVAL;  // the toy engine runs its rounds serially
+  return faser::llama_last_timeline(e->llama, ev, cap, info);
+}
+
 void* faser_engine_stream(const faser_engine* e) {
   if (e && e->llama) return faser::llama_stream(e->llama);
   return e ? static_cast<void*>(e->stream) : nullptr;

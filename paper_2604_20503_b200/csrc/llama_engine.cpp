@@ -30,6 +30,7 @@
 #include "faser/engine.h"
 #include "llama.cuh"
 #include "llama_engine.cuh"
+#include "lanes.cuh"
 #include "llama_step.cuh"
 #include "mega.cuh"
 #include "tp.cuh"
@@ -406,6 +407,21 @@ class LlamaEngine {
   cudaStream_t fs = nullptr;       // stream the current forward() launches on
   cudaEvent_t ev[4] = {};
   cudaEvent_t ev_chunk[FASER_MAX_SPEC + 1] = {};
+  // overlapped mode: SM-partitioned lanes and the measured pipeline timeline of the last step
+  std::unique_ptr<SmLanes> lanes;
+  int fwd_sms = 148;  // SM count the current forward's GEMM plans size their grids for
+  static constexpr int kLaneRec = 2 * (FASER_MAX_SPEC + 2), kLaneDec = FASER_MAX_SPEC + 2;
+  static constexpr int kLaneRes = FASER_MAX_SPEC + 2;
+  static constexpr int kLaneInts = kLaneRec + kLaneDec + kLaneRes + 2;
+  cudaEvent_t ev_fork = nullptr, ev_dend = nullptr;
+  cudaEvent_t ev_d0[FASER_MAX_SPEC + 1] = {}, ev_d1[FASER_MAX_SPEC + 1] = {};
+  cudaEvent_t ev_v0[FASER_MAX_SPEC + 1] = {}, ev_v1[FASER_MAX_SPEC + 1] = {};
+  int32_t* h_lane = nullptr;
+  bool tl_valid = false;
+  int tl_nch = 0, tl_lane_mode = 0;
+  LanePair tl_lp;
+  std::vector<faser_timeline_event> tl_events;
+  faser_timeline_info tl_info{};
   int nsm = 148;
   bool graph_mode = false;  // FASER_CUDA_GRAPH=1: each step is captured and replayed as one graph
   int max_spec = 16;
@@ -421,7 +437,7 @@ class LlamaEngine {
   Mem s_tok, s_len, s_ncomm, s_maxout, s_done, s_exempt, ptab;
   LmSlots sl{};
   // per-request step state (sorted order), persistent
-  Mem r_drafted, r_count, r_active, r_gl, r_npl, r_pl, r_prl, r_pr, r_fail, r_truth, r_truth_rj;
+  Mem r_drafted, r_count, r_active, r_gl, r_npl, r_pl, r_prl, r_pr, r_fail, r_truth, r_truth_rj, r_span;
   LmReqState rq{};
   LmReqState cur_q{};  // rq + this step's per-request arrays (slot, k, ...) in the blob
   // step blob
@@ -463,6 +479,13 @@ class LlamaEngine {
       if (e) cudaEventDestroy(e);
     for (auto e : ev_chunk)
       if (e) cudaEventDestroy(e);
+    for (auto* arr : {ev_d0, ev_d1, ev_v0, ev_v1})
+      for (int i = 0; i <= FASER_MAX_SPEC; ++i)
+        if (arr[i]) cudaEventDestroy(arr[i]);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_dend) cudaEventDestroy(ev_dend);
+    if (h_lane) cudaFreeHost(h_lane);
+    lanes.reset();
     if (vstream) cudaStreamDestroy(vstream);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -510,6 +533,12 @@ class LlamaEngine {
     fs = stream;
     for (auto& e : ev) LCK(cudaEventCreate(&e));
     for (auto& e : ev_chunk) LCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto* arr : {ev_d0, ev_d1, ev_v0, ev_v1})
+      for (int i = 0; i <= FASER_MAX_SPEC; ++i) LCK(cudaEventCreate(&arr[i]));
+    LCK(cudaEventCreate(&ev_fork));
+    LCK(cudaEventCreateWithFlags(&ev_dend, cudaEventDisableTiming));
+    LCK(cudaMallocHost(reinterpret_cast<void**>(&h_lane), sizeof(int32_t) * kLaneInts));
+    fwd_sms = nsm;
     max_seq = cfg.max_seq_len + max_spec + 2;
     max_pages = (max_seq + kPage - 1) / kPage;
     n_pages = cfg.max_batch * max_pages;
@@ -575,6 +604,7 @@ class LlamaEngine {
     r_fail.alloc(B * 4);
     r_truth.alloc(static_cast<size_t>(cap) * 4);
     r_truth_rj.alloc(static_cast<size_t>(B) * FASER_MAX_SPEC * 4);
+    r_span.alloc(B * 4);
     rq.drafted = r_drafted.as<int32_t>();
     rq.count = r_count.as<int32_t>();
     rq.active = r_active.as<int32_t>();
@@ -586,12 +616,14 @@ class LlamaEngine {
     rq.failmask = r_fail.as<uint32_t>();
     rq.truth = r_truth.as<int32_t>();
     rq.truth_rj = r_truth_rj.as<int32_t>();
+    rq.span = r_span.as<int32_t>();
     // blob: request arrays (5n) + verify rows (4T + 4n + 16) + ptab triples + admits + prefill rows
     blob_cap = static_cast<size_t>(B) * 64 + static_cast<size_t>(verify_rows) * 16 +
                static_cast<size_t>(B) * max_pages * 12 + static_cast<size_t>(B) * sizeof(LmAdmit) +
                static_cast<size_t>(cap) * 16 + static_cast<size_t>(B) * 16 * 2 + 4096 +
                static_cast<size_t>(B) * cfg.max_seq_len * (4 + 16) +   // prompts + prefill rows
-               static_cast<size_t>(B) * (9 * 4 + 64);                   // per-chunk arrays
+               static_cast<size_t>(B) * (9 * 4 + 64) +                  // per-chunk arrays
+               sizeof(int32_t) * kLaneInts + 64;                        // lane state
     LCK(cudaMallocHost(reinterpret_cast<void**>(&h_blob), blob_cap));
     d_blob.alloc(blob_cap);
     LCK(cudaMallocHost(reinterpret_cast<void**>(&h_res), sizeof(faser_round_result) * B));
@@ -619,9 +651,10 @@ class LlamaEngine {
     int64_t kv_tokens = 0;  // sum over requests of the context each attention call reads
     bool pre_embedded = false;  // rows' embeddings already written (fused draft control kernel)
     bool skip_argmax = false;   // leave the LM head's per-tile (max, id) partials for the caller
+    int q0 = 0;                 // first drafted position of the rows (overlapped chunk start)
   };
 
-  GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, nsm); }
+  GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, fwd_sms); }
   // ---- per-kernel-class timing (opt-in): event pairs around launches, resolved after the step
   static constexpr int kClasses = 7;  // + 5: target mega forward, 6: draft mega forward
   bool ktiming = false;
@@ -705,7 +738,7 @@ class LlamaEngine {
     const KvDev kv = m.kvdev(ptab.as<int>(), max_pages);
     const int qd = s.n_q * s.hd;
     // prefill forwards (no logits) take the prefill plan
-    auto pl = [&](int n_out, int k) { return f.logits ? plan(n_out, T, k) : gemm_plan_prefill(n_out, T, k, nsm); };
+    auto pl = [&](int n_out, int k) { return f.logits ? plan(n_out, T, k) : gemm_plan_prefill(n_out, T, k, fwd_sms); };
     const GemmPlan p_qkv = pl(s.qkv_out(), s.d), p_o = pl(s.d, qd);
     const GemmPlan p_gu = pl(2 * s.ffn, s.d), p_d = pl(s.d, s.ffn), p_lm = plan(s.vocab, T, s.d);
     RowsDev rows = f.rows;
@@ -832,7 +865,7 @@ class LlamaEngine {
         LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs));
         if (f.capture) capture_stage(layer, m, w, f);
         LCK(lm_exit_test(sl, cur_q, rows, w.logits.as<float>(), 1, 0, s.vocab, f.k_table[layer], T, fs));
-        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), fs));
+        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), fs, f.q0));
         LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(),
                            w.ss.as<float>(), w.xs.as<float>(), w.xbs.as<__nv_bfloat16>(), w.sss.as<float>(),
                            fs));
@@ -900,6 +933,55 @@ class LlamaEngine {
   template <class T>
   T* dev_of(const T* host) const {
     return reinterpret_cast<T*>(d_blob.as<char>() + (reinterpret_cast<const char*>(host) - h_blob));
+  }
+
+  // PipelineTimeline of the last overlapped step (overlap.cpp:44-91 semantics, measured): event
+  // times relative to the lanes' fork; a chunk with no request left on its frontier has no
+  // VerifyChunk, its (not cancelled) draft counts as waste; Reset where the frontier shrank.
+  void build_timeline() {
+    const int nch = tl_nch;
+    const int32_t* rec = h_lane;
+    const int32_t* dec = h_lane + kLaneRec;
+    const int32_t* res = dec + kLaneDec;
+    auto at = [&](cudaEvent_t e) {
+      float ms = 0.f;
+      LCK(cudaEventElapsedTime(&ms, ev_fork, e));
+      return static_cast<double>(ms);
+    };
+    faser_timeline_info& I = tl_info;
+    I = faser_timeline_info{};
+    tl_events.clear();
+    I.n_chunks = nch;
+    I.draft_sms = tl_lp.draft_sms;
+    I.verify_sms = tl_lp.verify_sms;
+    I.green = tl_lp.green ? 1 : 0;
+    I.lane_mode = tl_lane_mode;
+    for (int t = 0; t < kLaneDec; ++t) I.cancelled_draft_steps += dec[t] == 2;
+    for (int qq = 0; qq < nch && qq <= FASER_MAX_SPEC; ++qq) {
+      I.chunk_alive[qq] = rec[2 * qq];
+      I.chunk_rows[qq] = rec[2 * qq + 1];
+      I.chunk_resets[qq] = res[qq];
+    }
+    I.survivors = rec[2 * nch];
+    for (int qq = 0; qq < nch; ++qq) {
+      const double d0 = at(ev_d0[qq]), d1 = at(ev_d1[qq]);
+      const double v0 = at(ev_v0[qq]), v1 = at(ev_v1[qq]);
+      const int alive = rec[2 * qq];
+      if (d1 - d0 > 1e-3) {  // a chunk whose steps were all cancelled ran no kernels worth timing
+        tl_events.push_back({FASER_EV_DRAFT_CHUNK, qq, d0, d1});
+        I.draft_busy_ms += d1 - d0;
+        if (alive == 0) I.wasted_draft_ms += d1 - d0;
+      }
+      if (alive > 0) {
+        tl_events.push_back({FASER_EV_VERIFY_CHUNK, qq, v0, v1});
+        I.verify_busy_ms += v1 - v0;
+        if (res[qq] > 0) tl_events.push_back({FASER_EV_RESET, qq, v1, v1});
+      }
+    }
+    const double end = at(ev[2]);
+    tl_events.push_back({FASER_EV_COMMIT, nch - 1, end, end});
+    for (const auto& e : tl_events) I.makespan_ms = std::max(I.makespan_ms, e.end_ms);
+    I.n_events = static_cast<int32_t>(tl_events.size());
   }
 
   void step(const faser_step_plan* plan, faser_round_result* out, int cap, int* n_out) {
@@ -998,10 +1080,13 @@ class LlamaEngine {
       int T, max_rows;
     };
     std::vector<VChunkH> chunks_h;
+    // chunk < k: frontier-chunked overlap; chunk >= k with a share r in (0,1): one chunk, the two
+    // stages back to back on their partitions (per-share stage profiling)
+    const bool part_r = plan && plan->overlap.r > 0.0 && plan->overlap.r < 1.0;
     const bool overlap = cfg.mode == FASER_MODE_FULL && plan && plan->overlap.enabled &&
-                         plan->overlap.chunk >= 1 && plan->overlap.chunk < kmax && !use_graph_mode();
+                         plan->overlap.chunk >= 1 && (plan->overlap.chunk < kmax || part_r) && !use_graph_mode();
     if (overlap) {
-      const int c = plan->overlap.chunk;
+      const int c = std::min(plan->overlap.chunk, kmax);
       for (int q0 = 0; q0 < kmax; q0 += c) {
         int T = 0;
         for (int i = 0; i < n; ++i) T += std::max(0, std::min(ents[i].k, q0 + c) - q0);
@@ -1036,6 +1121,13 @@ class LlamaEngine {
         chunks_h.push_back(h);
       }
     }
+    // lane state of the overlapped mode (LaneState): rec | step_dec | alive, zero except alive = n
+    int32_t* b_rec = carve<int32_t>(off, kLaneInts);
+    std::memset(b_rec, 0, sizeof(int32_t) * kLaneInts);
+    int32_t* b_dec = b_rec + kLaneRec;
+    int32_t* b_res = b_dec + kLaneDec;
+    int32_t* b_alive = b_res + kLaneRes;
+    *b_alive = n;
     // admissions: slot row copy + page reservation for the prompt prefix
     for (int64_t id : newly) {
       Req& r = reqs.at(id);
@@ -1222,12 +1314,29 @@ class LlamaEngine {
       while (c < n && ents[c].k > t) ++c;
       return c;
     };
-    auto draft_step = [&](int t) {
+    // lanes: the draft lane drafts, the verify lane verifies; serial mode runs both on `stream`.
+    // Overlapped (FULL) mode with overlap.r in (0,1) puts them on disjoint green-context SM
+    // partitions (lanes.cuh) and the GEMM plans size their grids for the lane's SM count.
+    LanePair lp;
+    lp.draft = lp.verify = stream;
+    lp.draft_sms = lp.verify_sms = nsm;
+    if (overlap) {
+      if (plan->overlap.r > 0.0 && plan->overlap.r < 1.0) {
+        if (!lanes) lanes = std::make_unique<SmLanes>(cfg.device, nsm);
+        std::string lerr;
+        if (!lanes->get(plan->overlap.r, &lp, &lerr)) throw LFail{FASER_ECUDA, lerr};
+      } else {
+        lp.verify = vstream;
+      }
+    }
+    const cudaStream_t ds = lp.draft;
+    auto draft_step = [&](int t, const LaneState* ln) {
       const int nt = rows_at(t);
+      fwd_sms = lp.draft_sms;
       if (fuse_draft) {
         if (t == 0) {
           LCK(lm_draft_begin(sl, q, wd.rows, nt, draft.emb, dsh.d, wd.x.as<float>(), wd.xb.as<__nv_bfloat16>(),
-                             wd.ss.as<float>(), stream));
+                             wd.ss.as<float>(), ds));
           ++launches;
         }
         Fwd f;
@@ -1241,15 +1350,15 @@ class LlamaEngine {
         f.kv_tokens = ctx_sum + static_cast<int64_t>(nt) * (t + 1);
         f.pre_embedded = true;
         f.skip_argmax = true;
-        fs = stream;
+        fs = ds;
         forward(draft, wd, f);
         const int n_next = t + 1 < kmax ? rows_at(t + 1) : 0;
         LCK(lm_draft_advance(sl, q, wd.rows, wd.amax.as<float2>(), dsh.vocab / 128, nt, t, n_next, draft.emb, dsh.d,
-                             wd.x.as<float>(), wd.xb.as<__nv_bfloat16>(), wd.ss.as<float>(), stream));
+                             wd.x.as<float>(), wd.xb.as<__nv_bfloat16>(), wd.ss.as<float>(), ds, ln));
         ++launches;
         return;
       }
-      LCK(lm_draft_prep(sl, q, wd.rows, nt, t, stream));
+      LCK(lm_draft_prep(sl, q, wd.rows, nt, t, ds));
       Fwd f;
       f.rows = wd.rows;
       f.T = nt;
@@ -1259,24 +1368,39 @@ class LlamaEngine {
       f.logits = true;
       f.argmax_out = wd.argmax.as<int>();
       f.kv_tokens = ctx_sum + static_cast<int64_t>(nt) * (t + 1);
-      fs = stream;
+      fs = ds;
       forward(draft, wd, f);
-      LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, stream));
+      LCK(lm_draft_post(q, wd.argmax.as<int>(), nt, t, ds));
       launches += 2;
     };
     cudaStream_t vs = stream;  // stream of the verify lane
+    tl_valid = false;
     if (!chunks_v.empty()) {
       // ---- overlapped (FULL) mode: frontier chunk q is verified on the verify lane while the
-      // draft lane drafts chunk q+1 (overlap.cpp:44-91 made real); truth is scattered per
-      // (request, position) so the accept sees exactly what one full verify would produce.
-      vs = vstream;
-      const int c = plan->overlap.chunk;
-      for (size_t qi = 0; qi < chunks_v.size(); ++qi) {
-        for (int t = static_cast<int>(qi) * c; t < std::min(kmax, static_cast<int>(qi + 1) * c); ++t) draft_step(t);
-        if (qi + 1 == chunks_v.size()) LCK(record_event(ev[1]));
-        LCK(cudaEventRecord(ev_chunk[qi], stream));
+      // draft lane drafts chunk q+1 (overlap.cpp:44-91 made real). Before each chunk the verify
+      // lane drops the requests whose frontier was reset by an earlier chunk (rejection, prune
+      // or EOS): their rows are cancelled, and once no request is left the draft lane cancels
+      // the steps it has not started. Early exit runs inside every chunk (FULL = AD + EE +
+      // overlap); truth is scattered per (request, position) for the accept.
+      vs = lp.verify;
+      const int c = std::min(plan->overlap.chunk, kmax);
+      const int nch = static_cast<int>(chunks_v.size());
+      const bool isolate = plan->lane_mode == 1;
+      LaneState ln{dev_of(b_alive), dev_of(b_rec), dev_of(b_dec), dev_of(b_res)};
+      LCK(cudaEventRecord(ev_fork, stream));
+      LCK(cudaStreamWaitEvent(ds, ev_fork, 0));
+      if (vs != ds) LCK(cudaStreamWaitEvent(vs, ev_fork, 0));
+      for (int qi = 0; qi < nch; ++qi) {
+        if (isolate && qi > 0 && vs != ds) LCK(cudaStreamWaitEvent(ds, ev_v1[qi - 1], 0));
+        LCK(cudaEventRecord(ev_d0[qi], ds));
+        for (int t = qi * c; t < std::min(kmax, (qi + 1) * c); ++t) draft_step(t, fuse_draft ? &ln : nullptr);
+        LCK(cudaEventRecord(ev_d1[qi], ds));
+        if (qi + 1 == nch) LCK(cudaEventRecord(ev[1], ds));
+        LCK(cudaEventRecord(ev_chunk[qi], ds));
         LCK(cudaStreamWaitEvent(vs, ev_chunk[qi], 0));
+        LCK(cudaEventRecord(ev_v0[qi], vs));
         const VChunk& vc = chunks_v[qi];
+        LCK(lm_chunk_frontier(q, vc.rows, n, qi, qi * c, qi == 0 ? 1 : 0, L, eos, ln, vs));
         Fwd f;
         if (fuse_verify) {
           LCK(lm_verify_begin(sl, q, vc.rows, vc.T, target.emb, tsh.d, wt.x.as<float>(), wt.xb.as<__nv_bfloat16>(),
@@ -1293,18 +1417,29 @@ class LlamaEngine {
         f.logits = true;
         f.argmax_out = rq.truth;
         f.kv_tokens = ctx_sum + vc.T;
+        f.ee = ee;
+        f.gate_lo = glo;
+        f.gate_hi = ghi;
+        f.k_table = k_table;
+        f.q0 = qi * c;
         fs = vs;
+        fwd_sms = lp.verify_sms;
         forward(target, wt, f);
         if (fuse_verify)
           LCK(lm_verify_argmax(vc.rows, target.sh.vocab / 128, vc.T, wt.amax.as<float2>(), rq.truth, rq.truth_rj, vs));
         else
           LCK(lm_truth_scatter(vc.rows, rq.truth, rq.truth_rj, vc.T, vs));
-        launches += 2;
+        LCK(cudaEventRecord(ev_v1[qi], vs));
+        launches += 3;
       }
-      LCK(lm_verify_init(q, n, L, eos, vs));
+      LCK(lm_chunk_finalize(q, n, eos, nch, c, ln, vs));
       ++launches;
+      tl_nch = nch;
+      tl_lane_mode = isolate ? 1 : 0;
+      tl_lp = lp;
+      tl_valid = true;
     } else {
-      for (int t = 0; t < kmax; ++t) draft_step(t);
+      for (int t = 0; t < kmax; ++t) draft_step(t, nullptr);
       LCK(record_event(ev[1]));
       // ---- verify (+ early exit)
       LCK(lm_verify_init(q, n, L, eos, stream));
@@ -1337,14 +1472,18 @@ class LlamaEngine {
         LCK(lm_truth_scatter(vrows, rq.truth, rq.truth_rj, total, stream));
       launches += 3;
     }
-    StepCtl ctl{n, L, eos, (ee && chunks_v.empty()) ? 1 : 0, cfg.exempt_rule};
+    fwd_sms = nsm;
+    StepCtl ctl{n, L, eos, ee ? 1 : 0, cfg.exempt_rule};
     LCK(lm_accept_commit(sl, q, vrows, ctl, d_res.as<faser_round_result>(), vs));
     ++launches;
-    {
-      const cudaStream_t keep = stream;
-      stream = vs;  // record_event targets the lane that finishes the step
+    if (vs == stream)
       LCK(record_event(ev[2]));
-      stream = keep;
+    else
+      LCK(cudaEventRecord(ev[2], vs));
+    if (vs != stream) LCK(cudaStreamWaitEvent(stream, ev[2], 0));
+    if (ds != stream) {  // join the draft lane too: the next step's blob upload must not race it
+      LCK(cudaEventRecord(ev_dend, ds));
+      LCK(cudaStreamWaitEvent(stream, ev_dend, 0));
     }
     if (use_graph) {
       capturing = false;
@@ -1357,8 +1496,9 @@ class LlamaEngine {
       cudaGraphExecDestroy(ge);
       cudaGraphDestroy(g);
     }
-    LCK(cudaMemcpyAsync(h_res, d_res.p, sizeof(faser_round_result) * n, cudaMemcpyDeviceToHost, vs));
-    if (vs != stream) LCK(cudaStreamSynchronize(vs));
+    LCK(cudaMemcpyAsync(h_res, d_res.p, sizeof(faser_round_result) * n, cudaMemcpyDeviceToHost, stream));
+    if (tl_valid)
+      LCK(cudaMemcpyAsync(h_lane, dev_of(b_rec), sizeof(int32_t) * kLaneInts, cudaMemcpyDeviceToHost, stream));
     if (capture) {
       std::vector<int32_t> dr(static_cast<size_t>(n) * FASER_MAX_SPEC);
       LCK(cudaMemcpyAsync(dr.data(), rq.drafted, dr.size() * 4, cudaMemcpyDeviceToHost, stream));
@@ -1373,6 +1513,7 @@ class LlamaEngine {
     cudaEventElapsedTime(&t_draft, ev[0], ev[1]);
     cudaEventElapsedTime(&t_verify, ev[1], ev[2]);
     cudaEventElapsedTime(&t_step, ev[0], ev[2]);
+    if (tl_valid) build_timeline();
 
     // ---- host bookkeeping: commit mirror, page rollback, retire finished requests
     for (int64_t id : newly) reqs.at(id).admitted = true;
@@ -1504,6 +1645,14 @@ faser_status llama_release(LlamaEngine* e, int64_t req_id) {
 }
 
 int32_t llama_pending_work(const LlamaEngine* e) { return static_cast<int32_t>(e->live.size() + e->pending.size()); }
+faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev, int32_t cap, faser_timeline_info* info) {
+  if (!e->tl_valid) return FASER_EINVAL;
+  *info = e->tl_info;
+  const int n = std::min<int>(cap, static_cast<int>(e->tl_events.size()));
+  for (int i = 0; i < n; ++i) ev[i] = e->tl_events[i];
+  return FASER_OK;
+}
+
 void llama_last_step_timing(const LlamaEngine* e, float* d, float* v, float* s) {
   if (d) *d = e->t_draft;
   if (v) *v = e->t_verify;

@@ -31,6 +31,7 @@ int32_t llama_pending_work(const LlamaEngine* e);
 void llama_last_step_timing(const LlamaEngine* e, float* d, float* v, float* s);
 void llama_last_step_bytes(const LlamaEngine* e, int64_t* h2d, int64_t* d2h);
 void* llama_stream(const LlamaEngine* e);
+faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev, int32_t cap, faser_timeline_info* info);
 int64_t llama_launches(const LlamaEngine* e);
 faser_status llama_debug_verify_logits(LlamaEngine* e, int32_t stage, float* logits, int64_t* row_ids,
                                        int32_t cap_rows, int32_t* rows);

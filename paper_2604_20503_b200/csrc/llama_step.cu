@@ -94,12 +94,35 @@ __global__ void draft_begin_kernel(LmSlots sl, LmReqState rq, RowsDev rows, int 
 // After draft step t (one warp per row): argmax_lowest over the LM head's per-tile partials ->
 // drafted[r][t]; rows that draft again get step t+1's row and embedding (argmax_reduce +
 // draft_post + draft_prep + embed fused into one launch).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __global__ void draft_advance_kernel(LmSlots sl, LmReqState rq, RowsDev rows, const float2* __restrict__ amax,
                                      int n_tiles, int n_t, int t, int n_next, const __nv_bfloat16* emb, int d,
-                                     float* x, __nv_bfloat16* xb, float* ss) {
+                                     float* x, __nv_bfloat16* xb, float* ss, LaneState ln) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  // overlapped mode: a cancelled step t also cancels t+1 (its rows stay empty)
+  if (ln.step_dec && ln.step_dec[t] == 2) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && n_next > 0) ln.step_dec[t + 1] = 2;
+    return;
+  }
+  // decision for step t+1, taken once for the whole grid (first block to get here): cancel it
+  // if no request is left on the frontier the verify lane has published so far
+  __shared__ int s_dec;
+  if (ln.step_dec && n_next > 0) {
+    if (threadIdx.x == 0) {
+      const int mine = ld_acquire_gpu(ln.alive) == 0 ? 2 : 1;
+      const int prev = atomicCAS(&ln.step_dec[t + 1], 0, mine);
+      s_dec = prev == 0 ? mine : prev;
+    }
+    __syncthreads();
+  }
+  const bool cancel_next = ln.step_dec && n_next > 0 && s_dec == 2;
   if (r >= n_t) return;
   float bv = -3.402823466e38f;
   int bi = 0x7fffffff;
@@ -124,10 +147,14 @@ __global__ void draft_advance_kernel(LmSlots sl, LmReqState rq, RowsDev rows, co
                bi, n_t);
   if (lane == 0) rq.drafted[r * kMS + t] = bi;
   if (r < n_next) {  // rows are sorted by k' descending: the first n_next rows draft again
-    if (lane == 0) set_draft_row(sl, rq, rows, r, t + 1, bi);
-    embed_row_warp(emb, bi, r, d, n_next, x, xb, ss, lane);
+    if (cancel_next) {
+      if (lane == 0) rows.req_n[r] = 0;  // attention skips the request
+    } else {
+      if (lane == 0) set_draft_row(sl, rq, rows, r, t + 1, bi);
+      embed_row_warp(emb, bi, r, d, n_next, x, xb, ss, lane);
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n_next > 0) *rows.n_rows = n_next;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n_next > 0) *rows.n_rows = cancel_next ? 0 : n_next;
 }
 
 // Verify rows' input tokens + their embeddings, one warp per row (verify_tokens + embed fused).
@@ -264,7 +291,9 @@ __global__ void __launch_bounds__(kExitThreads) exit_test_kernel(LmSlots sl, LmR
 }
 
 // One thread per request (n <= 1024), single CTA.
-__global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, int* src_of) {
+// q0: first drafted position of these rows (0, or the chunk start in the overlapped mode, where
+// row (i, q0 + jl) sits at local index jl of request i).
+__global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, int* src_of, int q0) {
   __shared__ int scan[1024];
   const int i = threadIdx.x;
   int keep = 0, old_first = 0, pos0 = 0;
@@ -273,7 +302,7 @@ __global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, i
     old_first = rows.req_first[i];
     pos0 = rows.req_pos0[i];
     const int old_n = rows.req_n[i];
-    if (act > 0) {
+    if (act > q0 && old_n > 0) {
       rq.gate_layers[i] += 1;
       const uint32_t live = act >= 32 ? 0xffffffffu : ((1u << act) - 1u);
       const uint32_t f = rq.failmask[i] & live;
@@ -289,8 +318,9 @@ __global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, i
       }
     }
     rq.failmask[i] = 0u;
-    keep = act > 1 ? act : 1;  // row 0 survives (force-verify, sdcore.cpp:150-166)
-    keep = keep < old_n ? keep : old_n;
+    keep = act - q0;
+    if (q0 == 0 && keep < 1) keep = 1;  // row 0 survives (force-verify, sdcore.cpp:150-166)
+    keep = keep < 0 ? 0 : (keep < old_n ? keep : old_n);
   }
   scan[i] = keep;
   __syncthreads();
@@ -308,10 +338,113 @@ __global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, i
       src_of[nf + j] = old_first + j;
       rows.row_req[nf + j] = i;
       rows.row_pos[nf + j] = pos0 + j;
-      rows.row_j[nf + j] = j;
+      rows.row_j[nf + j] = q0 + j;
     }
   }
   if (i == blockDim.x - 1) *rows.n_rows = scan[i];
+}
+
+// Overlapped verify, before chunk q: which requests are still on the frontier, and the chunk's
+// rows compacted to theirs (one thread per request, single CTA). Compaction is in place: request
+// i's new range starts at or before its old one and no thread reads another request's rows.
+__global__ void chunk_frontier_kernel(LmReqState rq, RowsDev rows, int n, int q, int q0, int first, int layers,
+                                      int eos, LaneState ln) {
+  __shared__ int scan[1024];
+  const int i = threadIdx.x;
+  int keep = 0, on = 0, pos0 = 0;
+  if (i < n) {
+    if (first) {  // per-request verify state (the verify_init of the serial path, active = k)
+      for (int j = 0; j < kMS; ++j) rq.prune_layer[i * kMS + j] = layers;
+      rq.active[i] = rq.k[i];
+      rq.gate_layers[i] = 0;
+      rq.n_pl[i] = 0;
+      rq.pr[2 * i] = -1;
+      rq.pr[2 * i + 1] = -1;
+      rq.failmask[i] = 0u;
+      rq.span[i] = 0;
+    }
+    const int old_n = rows.req_n[i];
+    pos0 = rows.req_pos0[i];
+    const int32_t* d = rq.drafted + i * kMS;
+    const int32_t* tr = rq.truth_rj + i * kMS;
+    bool ok = old_n > 0 && rq.active[i] > q0;
+    for (int j = 0; ok && j < q0; ++j) ok = d[j] != eos && d[j] == tr[j];
+    if (ok) {
+      on = 1;
+      keep = old_n;
+      for (int j = 0; j < old_n; ++j)
+        if (d[q0 + j] == eos) {  // draft_tokens stops at EOS (sdcore.cpp:56): no rows past it
+          keep = j + 1;
+          break;
+        }
+      rq.span[i] = q0 + keep;
+    }
+  }
+  const int n_on = __syncthreads_count(on);
+  scan[i] = keep;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    const int v = i >= off ? scan[i - off] : 0;
+    __syncthreads();
+    scan[i] += v;
+    __syncthreads();
+  }
+  const int nf = scan[i] - keep;
+  if (i < n) {
+    rows.req_first[i] = nf;
+    rows.req_n[i] = keep;
+    for (int j = 0; j < keep; ++j) {
+      rows.row_req[nf + j] = i;
+      rows.row_pos[nf + j] = pos0 + j;
+      rows.row_j[nf + j] = q0 + j;
+    }
+  }
+  if (i == blockDim.x - 1) {
+    *rows.n_rows = scan[i];
+    ln.rec[2 * q] = n_on;
+    ln.rec[2 * q + 1] = scan[i];
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ln.alive), "r"(n_on) : "memory");
+  }
+}
+
+__global__ void chunk_finalize_kernel(LmReqState rq, int n, int eos, int nchunks, int chunk, LaneState ln) {
+  __shared__ int s_res[kMS + 1];
+  const int i = threadIdx.x;
+  for (int q = i; q <= kMS; q += blockDim.x) s_res[q] = 0;
+  __syncthreads();
+  int surv = 0;
+  if (i < n) {
+    // every draft step has finished when this runs (the last chunk waited for the draft lane):
+    // the EOS stop scans all drafted tokens up to the first cancelled step, as the serial path
+    const int k = rq.k[i];
+    int t_c = k;
+    for (int t = 1; t < k; ++t)
+      if (ln.step_dec[t] == 2) {
+        t_c = t;
+        break;
+      }
+    const int32_t* d = rq.drafted + i * kMS;
+    const int32_t* tr = rq.truth_rj + i * kMS;
+    const int span = rq.span[i];
+    int count = k;
+    for (int j = 0; j < t_c; ++j)
+      if (d[j] == eos) {
+        count = j + 1;
+        break;
+      }
+    const int act = rq.active[i] < count ? rq.active[i] : count;
+    rq.count[i] = count;
+    rq.active[i] = act;
+    bool ok = act >= count && span >= count;
+    for (int j = 0; ok && j < count; ++j) ok = d[j] == tr[j];
+    surv = ok ? 1 : 0;
+    // the frontier ended in the last chunk the request had rows in; unless everything it
+    // drafted was accepted, that chunk's verification reset it
+    if (!ok && span > 0) atomicAdd(&s_res[(span - 1) / chunk], 1);
+  }
+  const int ns = __syncthreads_count(surv);
+  if (i == 0) ln.rec[2 * nchunks] = ns;
+  for (int q = i; q < nchunks; q += blockDim.x) ln.resets[q] = s_res[q];
 }
 
 // Compaction, pass 1: copy the surviving rows' residual (fp32 + bf16 operand copy + per-chunk
@@ -510,10 +643,11 @@ cudaError_t lm_draft_begin(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, con
 }
 cudaError_t lm_draft_advance(LmSlots sl, LmReqState rq, RowsDev rows, const float2* amax, int n_tiles, int n_t,
                              int t, int n_next, const __nv_bfloat16* emb, int d, float* x, __nv_bfloat16* xb,
-                             float* ss, cudaStream_t s) {
+                             float* ss, cudaStream_t s, const LaneState* lane) {
   if (n_t <= 0) return cudaSuccess;
+  const LaneState ln = lane ? *lane : LaneState{nullptr, nullptr, nullptr, nullptr};
   return launch_pdl(draft_advance_kernel, cdiv(n_t * 32, 256), 256, s, sl, rq, rows, amax, n_tiles, n_t, t,
-                    n_next, emb, d, x, xb, ss);
+                    n_next, emb, d, x, xb, ss, ln);
 }
 cudaError_t lm_verify_begin(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, const __nv_bfloat16* emb, int d,
                             float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s) {
@@ -553,11 +687,24 @@ cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* l
   return cudaGetLastError();
 }
 cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
-                                int* src_of, cudaStream_t s) {
+                                int* src_of, cudaStream_t s, int q0) {
   (void)sl;
   if (n <= 0) return cudaSuccess;
   if (n > 1024) return cudaErrorInvalidValue;
-  frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, layer, src_of);
+  frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, layer, src_of, q0);
+  return cudaGetLastError();
+}
+cudaError_t lm_chunk_frontier(LmReqState rq, RowsDev rows, int n, int q, int q0, int first, int layers, int eos,
+                              LaneState lane, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 1024) return cudaErrorInvalidValue;
+  chunk_frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, q, q0, first, layers, eos, lane);
+  return cudaGetLastError();
+}
+cudaError_t lm_chunk_finalize(LmReqState rq, int n, int eos, int nchunks, int chunk, LaneState lane, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 1024 || chunk < 1 || nchunks > kMS) return cudaErrorInvalidValue;
+  chunk_finalize_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, n, eos, nchunks, chunk, lane);
   return cudaGetLastError();
 }
 cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, int t_stride, float* x,

@@ -40,6 +40,22 @@ struct LmReqState {
   uint32_t* failmask;   // [n] exit-test failures at the current gated layer
   int32_t* truth;       // [rows] final argmax per verify row (compacted order)
   int32_t* truth_rj;    // [n][FASER_MAX_SPEC] final argmax by (request, drafted position)
+  int32_t* span;        // [n] chunked verify: drafted positions covered by the chunks the request
+                        // was verified in (its frontier's reach)
+};
+
+// Frontier-chunked (FULL) verify state shared by the two lanes of one step (device ints):
+//   alive        requests still on the frontier after the latest verified chunk (verify lane
+//                writes, the draft lane reads it to cancel chunks nobody will verify)
+//   rec[2q]      requests on the frontier with rows in chunk q, rec[2q+1] its rows;
+//                rec[2*nchunks] requests whose every drafted token was verified and accepted
+//   resets[q]    requests whose frontier chunk q's verification reset (rejection or prune)
+//   step_dec[t]  draft step t: 0 undecided, 1 run, 2 cancelled (reset observed before it started)
+struct LaneState {
+  int32_t* alive;
+  int32_t* rec;
+  int32_t* step_dec;
+  int32_t* resets;
 };
 
 struct StepCtl {
@@ -58,9 +74,12 @@ cudaError_t lm_draft_prep(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, int 
 // rows + embeddings for the first n_next rows (argmax_reduce + draft_post + draft_prep + embed).
 cudaError_t lm_draft_begin(LmSlots sl, LmReqState rq, RowsDev rows, int n_t, const __nv_bfloat16* emb, int d,
                            float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s);
+// With `lane` (overlapped mode), step t+1 is cancelled when no request is left on the frontier
+// (lane.alive == 0) at the time step t finishes: its rows are emptied so the forward's kernels exit
+// at once (the reference's draft cancellation after a reset, overlap.cpp:58-62).
 cudaError_t lm_draft_advance(LmSlots sl, LmReqState rq, RowsDev rows, const float2* amax, int n_tiles, int n_t,
                              int t, int n_next, const __nv_bfloat16* emb, int d, float* x, __nv_bfloat16* xb,
-                             float* ss, cudaStream_t s);
+                             float* ss, cudaStream_t s, const LaneState* lane = nullptr);
 // verify rows' tokens + embeddings (verify_tokens + embed fused; one warp per row)
 cudaError_t lm_verify_begin(LmSlots sl, LmReqState rq, RowsDev rows, int rows_cap, const __nv_bfloat16* emb, int d,
                             float* x, __nv_bfloat16* xb, float* ss, cudaStream_t s);
@@ -81,8 +100,19 @@ cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* l
 // K4 frontier: per request earliest failing row prunes the suffix; compacts the row set.
 // src_of[new_row] = old row; the residual (x fp32, xb bf16, ss per-chunk sums of squares) is
 // gathered through scratch buffers of the same shapes.
+// q0 = first drafted position of the rows (0, or the chunk start in the overlapped mode).
 cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
-                                int* src_of, cudaStream_t s);
+                                int* src_of, cudaStream_t s, int q0 = 0);
+// Overlapped (FULL) verify, before chunk q (drafted positions [q0, q0 + rows)): a request stays on
+// the frontier iff no earlier row was pruned (active > q0), rejected (drafted != truth) or EOS;
+// otherwise its rows of the chunk are cancelled (reset, overlap.cpp:44-91). The chunk's rows are
+// compacted in place; lane.alive / lane.rec[2q..2q+1] record the frontier. first = 1 for chunk 0
+// also initialises the per-request early-exit state (active = k).
+cudaError_t lm_chunk_frontier(LmReqState rq, RowsDev rows, int n, int q, int q0, int first, int layers, int eos,
+                              LaneState lane, cudaStream_t s);
+// After the last chunk: drafted length (EOS stop over the drafted tokens, as the serial path),
+// active = min(active, count), survivors and per-chunk resets (chunk = frontier chunk size).
+cudaError_t lm_chunk_finalize(LmReqState rq, int n, int eos, int nchunks, int chunk, LaneState lane, cudaStream_t s);
 cudaError_t lm_gather_rows(RowsDev rows, const int* src_of, int d, int t_stride, float* x,
                            __nv_bfloat16* xb, float* ss, float* xs, __nv_bfloat16* xbs, float* sss,
                            cudaStream_t s);

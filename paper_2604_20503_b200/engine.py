@@ -235,6 +235,12 @@ def plan_overlap(s, b, r_grid=(0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9), mod
     return out
 
 
+def num_sms(device=0):
+    """SM count of `device` (the lanes partition it in multiples of 8)."""
+    import torch
+    return torch.cuda.get_device_properties(device).multi_processor_count
+
+
 class ServingEngine:
     """Stateful GPU engine: submit() requests, step() one draft->verify->commit round."""
 
@@ -290,6 +296,18 @@ class ServingEngine:
         is verified on a second lane while chunk q+1 is drafted."""
         self.plan.overlap = abi.OverlapPlan(1 if enabled else 0, chunk, r, 0.0, 0.0)
         self.overlap_state = (bool(enabled), chunk, r)
+
+    def set_lane_mode(self, mode):
+        """abi.LANES_OVERLAP (default) or abi.LANES_ISOLATED: the same partitions and chunks with the
+        lanes serialised (draft chunk q+1 after verify chunk q), the interference baseline."""
+        self.plan.lane_mode = int(mode)
+
+    def last_timeline(self, cap=4 * (abi.MAX_SPEC + 2)):
+        """Measured PipelineTimeline of the last overlapped step: (TimelineInfo, [TimelineEvent])."""
+        evs = (abi.TimelineEvent * cap)()
+        info = abi.TimelineInfo()
+        _check(lib().faser_last_timeline(self.h, evs, cap, C.byref(info)), self.h)
+        return info, [evs[i] for i in range(min(cap, info.n_events))]
 
     def step(self):
         n = C.c_int32()

@@ -31,13 +31,13 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_sizes_match_header():
     L = engine.lib()
-    out = (C.c_int64 * 13)()
-    assert L.faser_abi_struct_sizes(out, 13) == 0
+    out = (C.c_int64 * 15)()
+    assert L.faser_abi_struct_sizes(out, 15) == 0
     py = [abi.ToyParams, abi.ExitPolicy, abi.GatePlan, abi.GateEntry, abi.OverlapPlan,
           abi.LatencyParams, abi.LatencyModel, abi.VerifyOutcome, abi.ModelDesc, abi.EngineCfg,
-          abi.StepPlan, abi.RoundResult, abi.LlamaShape]
+          abi.StepPlan, abi.RoundResult, abi.LlamaShape, abi.TimelineEvent, abi.TimelineInfo]
     assert [C.sizeof(t) for t in py] == list(out)
-    assert L.faser_abi_version() == 2
+    assert L.faser_abi_version() == 3
 
 
 def test_library_is_sm100a_cubin():
