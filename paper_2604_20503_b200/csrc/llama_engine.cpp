@@ -873,8 +873,12 @@ class LlamaEngine {
       }
     }
     if (f.logits) {
-      timed(is_target ? 4 : 2, gbytes(s.vocab, s.d, 2 * s.vocab),
-            [&] { LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs)); }, gflops(s.vocab, s.d));
+      // the final head needs only the per-tile (max, id) partials; the T x V logits are written
+      // for validation (debug capture) only
+      EpiArgs e_fin = e_lm;
+      if (!f.capture) e_fin.logits = nullptr;
+      timed(is_target ? 4 : 2, gbytes(s.vocab, s.d, f.capture ? 2 * s.vocab : 0),
+            [&] { LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_fin, fs)); }, gflops(s.vocab, s.d));
       if (is_tp_target) {  // vocab-parallel greedy argmax: all-gather (max, lowest global id) per row
         LCK(tp_local_argmax(s.vocab / 128, T, w.amax.as<float2>(), tp_loc.as<float2>(), fs));
         LCK(tpg->allgather_f2(tp_rank, tp_loc.as<float2>(), tp_all.as<float2>(), static_cast<size_t>(T), fs));

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(128, 1)
           if (lane == 0) ea.ss_out[static_cast<size_t>(m0 / kBM) * ea.t_stride + n0 + t] = q;
         } else {  // kEpiLogits
           a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
-          *reinterpret_cast<float4*>(ea.logits + idx) = a;
+          if (ea.logits) *reinterpret_cast<float4*>(ea.logits + idx) = a;  // validation / exit test only
           float bv = a.x;
           const int id0 = ea.id_off + m0 + c4;
           int bi = id0;

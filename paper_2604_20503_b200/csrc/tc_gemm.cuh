@@ -48,7 +48,7 @@ struct EpiArgs {
   __nv_bfloat16* q = nullptr;            // kEpiQkv [t][n_q*hd]
   __nv_bfloat16* h = nullptr;            // kEpiSwiglu [t][ffn]
   int ffn = 0;
-  float* logits = nullptr;               // kEpiLogits [t][n_out]
+  float* logits = nullptr;               // kEpiLogits [t][n_out]; nullptr: argmax partials only
   float2* amax = nullptr;                // kEpiLogits [n_out/128][t_stride] (value, idx bits)
   int id_off = 0;                        // kEpiLogits: id of output row 0 (vocab-parallel shard)
   // optional timeline (tools/layer_chain.py): per CTA 8 globaltimer stamps [cta][8] = entry, after

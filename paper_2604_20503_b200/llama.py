@@ -92,16 +92,21 @@ def tiny128(target_bigram=None, draft_bigram=None, hard=None):
 PRESETS = {"tiny": tiny, "cfg3": config3, "cfg4": config4, "cfg5": config5, "tp_tiny": tp_tiny, "tiny128": tiny128}
 
 
-def fitted_latency_model(path=None):
-    """abi.LatencyModel from the B200 stage-latency fit (tools/profile_latency.py ->
-    profiles/r01_latency_model.json); None when the file is absent."""
+def fitted_latency_model(path=None, share_path=None):
+    """abi.LatencyModel from the B200 stage-latency fits: ee_check / prune from
+    tools/profile_latency.py (profiles/r01_latency_model.json), draft / target with their measured
+    SM-share factor from tools/lane_profile.py (profiles/r02_lane_profile.json: green-context
+    partitions at r in {0.25, 0.5, 0.75} + whole-GPU samples) when present. None when absent."""
     import json
     import os
-    path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                "profiles", "r01_latency_model.json")
+    prof = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+    path = path or os.path.join(prof, "r01_latency_model.json")
+    share_path = share_path or os.path.join(prof, "r02_lane_profile.json")
     if not os.path.exists(path):
         return None
-    m = json.load(open(path))["model"]
+    m = dict(json.load(open(path))["model"])
+    if os.path.exists(share_path):
+        m.update(json.load(open(share_path))["model"])
     out = abi.LatencyModel()
     for name in ("draft", "target", "ee_check", "prune"):
         p = getattr(out, name)

@@ -124,8 +124,8 @@ class ModeController:
         self.overlap_on = False
         if self.mode == abi.MODE_FULL:
             if self.chunk:
-                eng.set_overlap(True, self.chunk)
                 self.overlap_on = self.chunk < max(ks)
+                eng.set_overlap(self.overlap_on, self.chunk)
             else:
                 p = self.engine.plan_overlap(max(ks), len(ks), models=self.models)
                 eng.set_overlap(bool(p.enabled), max(p.chunk, 1), p.r)
