@@ -32,12 +32,28 @@ def build_product(force=False, verbose=False):
         os.path.join(ROOT, "include", "faser", "*.h"))
     if not force and not _stale(LIB, deps):
         return LIB
-    cmd = ["nvcc", *ARCH, "-lineinfo", "-O3", "-std=c++17", "-shared", "-cudart", "static",
-           "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *srcs]
+    # one object per translation unit, compiled in parallel and rebuilt only when the unit or
+    # any header changed (same flags as a single nvcc invocation; no device linking is needed)
+    flags = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+             "-I", os.path.join(ROOT, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+        flags.insert(0, "-Xptxas=-v")
+    odir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(odir, exist_ok=True)
+    headers = [d for d in deps if d not in srcs]
+    objs, jobs = [], []
+    for src in srcs:
+        obj = os.path.join(odir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + headers):
+            jobs.append(["nvcc", *flags, "-c", src, "-o", obj])
+    procs = []
+    for cmd in jobs:
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
+    subprocess.run(["nvcc", *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *objs], check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(128, 1)
     int ts = 0, te = tn;
     if (splits > 1) {
       cluster_sync();
+      if (threadIdx.x == 0 && j == 0) stamp(ea, 6);
       const int per = (tn + splits - 1) / splits;
       ts = min(tn, static_cast<int>(blockIdx.z) * per);
       te = min(tn, ts + per);

@@ -136,13 +136,14 @@ def main():
         rows = []
         for (l, n, t) in traces:
             v = t.view(-1, 8).cpu().double()
-            ent, wt, first, acc, red, ex = (v[:, i] for i in range(6))
+            ent, wt, first, acc, red, ex, syn = (v[:, i] for i in range(7))
+            syn = torch.where(syn > 0, syn, acc)
             ok = ex > 0
             med = lambda x: float(x[ok].median()) / 1e3  # noqa: E731
             r = {"layer": l, "gemm": n, "ctas": int(v.shape[0]),
                  "gap_us": None if prev_end is None else round((float(ent[ok].min()) - prev_end) / 1e3, 2),
                  "pre_us": round(med(wt - ent), 2), "fill_us": round(med(first - wt), 2),
-                 "main_us": round(med(acc - first), 2), "red_us": round(med(red - acc), 2),
+                 "main_us": round(med(acc - first), 2), "sync_us": round(med(syn - acc), 2), "red_us": round(med(red - syn), 2),
                  "epi_us": round(med(ex - red), 2),
                  "span_us": round((float(ex[ok].max()) - float(ent[ok].min())) / 1e3, 2),
                  "entry_spread_us": round((float(ent[ok].max()) - float(ent[ok].min())) / 1e3, 2)}
