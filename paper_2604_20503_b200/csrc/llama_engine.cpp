@@ -32,7 +32,6 @@
 #include "llama_engine.cuh"
 #include "lanes.cuh"
 #include "llama_step.cuh"
-#include "mega.cuh"
 #include "tp.cuh"
 #include "tc_gemm.cuh"
 
@@ -277,62 +276,6 @@ struct LmWork {
   }
 };
 
-// ------------------------------------------------------------------ persistent forward state
-struct MegaCtx {
-  Mem maps, sync, ws;
-  MegaModelDev dev{};
-  int grid = 0;
-  void build(const LmModel& m, const LmWork& w, int nsm, cudaStream_t st) {
-    const LlamaShape& s = m.sh;
-    const int L = s.layers;
-    std::vector<CUtensorMap> h(static_cast<size_t>(4) * L + 25);
-    for (int l = 0; l < L; ++l) {
-      h[4 * l] = m.op_qkv[l].map;
-      h[4 * l + 1] = m.op_o[l].map;
-      h[4 * l + 2] = m.op_gu[l].map;
-      h[4 * l + 3] = m.op_d[l].map;
-    }
-    h[4 * L] = m.op_lm.map;
-    const GemmOperand* acts[3] = {&w.op_xb, &w.op_ob, &w.op_h};
-    for (int a = 0; a < 3; ++a)
-      for (int j = 0; j < 8; ++j) {
-        GemmOperand op;
-        LCK(make_operand(&op, acts[a]->base, acts[a]->rows, acts[a]->k, 32 * (j + 1)));
-        h[4 * L + 1 + 8 * a + j] = op.map;
-      }
-    maps.alloc(h.size() * sizeof(CUtensorMap));
-    LCK(cudaMemcpyAsync(maps.p, h.data(), maps.bytes, cudaMemcpyHostToDevice, st));
-    grid = nsm;
-    const int max_mt = std::max({s.qkv_out(), s.d, 2 * s.ffn, s.vocab}) / 128;
-    dev.tile_stride = max_mt;
-    sync.alloc(mega_sync_words(L, dev.tile_stride) * 4);
-    LCK(cudaMemsetAsync(sync.p, 0, sync.bytes, st));
-    ws.alloc(mega_ws_floats(grid, max_mt) * 4);
-    dev.maps = maps.as<CUtensorMap>();
-    dev.emb = m.emb;
-    dev.rope = m.rope.as<float2>();
-    dev.d = s.d;
-    dev.layers = L;
-    dev.n_q = s.n_q;
-    dev.n_kv = s.n_kv;
-    dev.hd = s.hd;
-    dev.ffn = s.ffn;
-    dev.vocab = s.vocab;
-    dev.eps = s.eps;
-    dev.x = w.x.as<float>();
-    dev.xb = w.xb.as<__nv_bfloat16>();
-    dev.ss = w.ss.as<float>();
-    dev.q = w.q.as<__nv_bfloat16>();
-    dev.ob = w.ob.as<__nv_bfloat16>();
-    dev.h = w.h.as<__nv_bfloat16>();
-    dev.amax = w.amax.as<float2>();
-    dev.ws = ws.as<float>();
-    dev.ws_slots = mega_ws_slots(grid, max_mt);
-    dev.sync = sync.as<unsigned>();
-    LCK(cudaStreamSynchronize(st));  // h is a host temporary
-  }
-};
-
 int num_sms_dev() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -350,58 +293,9 @@ class LlamaEngine {
   LlamaShape dsh{}, tsh{};
   LmModel draft, target;
   LmWork wd, wt;
-  MegaCtx md, mtg;          // persistent single-launch forwards (draft step / verify), opt-in
-  Mem mega_trace;
   int tp = 1, tp_rank = 0;  // tensor-parallel verification of the target (tp.cuh)
   TpGroup* tpg = nullptr;
   Mem tp_part, tp_loc, tp_all;  // row-parallel partial [rows][d] fp32; argmax partials (float2)
-  void dump_mega_trace(int layers, int G) {
-    LCK(cudaStreamSynchronize(fs));
-    const int P = mega_phases(layers);
-    std::vector<unsigned long long> t(static_cast<size_t>(2 * P + 4) * G + 4096);
-    LCK(cudaMemcpy(t.data(), mega_trace.p, t.size() * 8, cudaMemcpyDeviceToHost));
-    unsigned long long t0 = ~0ull;
-    for (int c = 0; c < G; ++c) t0 = std::min(t0, t[c]);
-    unsigned long long prev_end = t0;
-    fprintf(stderr, "mega trace (us rel. to first phase-0 arrival): phase end / dur / min-first-X - prev end\n");
-    for (int p = 0; p < P; ++p) {
-      unsigned long long e = 0, xs = ~0ull;
-      for (int c = 0; c < G; ++c) {
-        e = std::max(e, t[static_cast<size_t>(p) * G + c]);
-        const unsigned long long x = t[static_cast<size_t>(P + p) * G + c];
-        if (x) xs = std::min(xs, x);
-      }
-      fprintf(stderr, "  p%3d end %9.2f dur %7.2f xlag %7.2f\n", p, (e - t0) / 1e3, (e - prev_end) / 1e3,
-              xs == ~0ull ? -1.0 : ((double)xs - (double)prev_end) / 1e3);
-      prev_end = e;
-    }
-    // phase 4 per-CTA detail (relative to the end of phase 3)
-    unsigned long long e3 = 0;
-    for (int c = 0; c < G; ++c) e3 = std::max(e3, t[static_cast<size_t>(3) * G + c]);
-    fprintf(stderr, "phase4 CTA0 jobs: W issue, X issue, MMA start\n");
-    for (int j = 0; j < 32; ++j) {
-      const unsigned long long* q = &t[static_cast<size_t>(2 * P + 4) * G + j * 4];
-      if (!q[0] && !q[1] && !q[2]) continue;
-      auto rel = [&](unsigned long long v) { return v ? ((double)v - (double)e3) / 1e3 : -99.0; };
-      fprintf(stderr, "  job%2d %8.2f %8.2f %8.2f\n", j, rel(q[0]), rel(q[1]), rel(q[2]));
-    }
-    for (int w = 0; w < 2; ++w) {
-      fprintf(stderr, "phase4 worker events cta %d:", w ? 77 : 0);
-      for (int k = 0; k < 32; ++k) {
-        const unsigned long long v = t[static_cast<size_t>(2 * P + 4) * G + 256 + 32 * w + k];
-        if (v) fprintf(stderr, " [%d]%.2f", k, ((double)v - (double)e3) / 1e3);
-      }
-      fprintf(stderr, "\n");
-    }
-    fprintf(stderr, "phase4 per CTA: xfirst xlast mmalast pass1 arrive\n");
-    for (int c = 0; c < G; c += 4) {
-      auto rel = [&](unsigned long long v) { return v ? ((double)v - (double)e3) / 1e3 : -1.0; };
-      fprintf(stderr, "  cta%3d %7.2f %7.2f %7.2f %7.2f %7.2f\n", c, rel(t[static_cast<size_t>(P + 4) * G + c]),
-              rel(t[static_cast<size_t>(2 * P) * G + c]), rel(t[static_cast<size_t>(2 * P + 1) * G + c]),
-              rel(t[static_cast<size_t>(2 * P + 2) * G + c]), rel(t[static_cast<size_t>(4) * G + c]));
-    }
-  }       // persistent single-launch forwards (draft step / verify)
-  bool mega_on = true;   // FASER_MEGA=0 falls back to one launch per projection / attention
   cudaStream_t stream = nullptr;   // draft lane (and everything in serial mode)
   cudaStream_t vstream = nullptr;  // verify lane of the overlapped (FULL) mode
   cudaStream_t fs = nullptr;       // stream the current forward() launches on
@@ -570,14 +464,6 @@ class LlamaEngine {
       tp_all.alloc(static_cast<size_t>(cap) * 8 * tp);
     }
     LCK(cudaDeviceSynchronize());
-    // persistent single-launch forward: opt-in (FASER_MEGA=1) until it beats the per-layer
-    // launches (its split-K partial exchange is latency-bound at T ~ 128)
-    mega_on = getenv("FASER_MEGA") && getenv("FASER_MEGA")[0] == '1';
-    if (tp > 1) mega_on = false;
-    if (mega_on) {
-      md.build(draft, wd, nsm, stream);
-      mtg.build(target, wt, nsm, stream);
-    }
     s_tok.alloc(static_cast<size_t>(B) * max_seq * 4);
     s_len.alloc(B * 4);
     s_ncomm.alloc(B * 4);
@@ -656,7 +542,7 @@ class LlamaEngine {
 
   GemmPlan plan(int n_out, int T, int k) const { return gemm_plan(n_out, T, k, fwd_sms); }
   // ---- per-kernel-class timing (opt-in): event pairs around launches, resolved after the step
-  static constexpr int kClasses = 7;  // + 5: target mega forward, 6: draft mega forward
+  static constexpr int kClasses = 5;
   bool ktiming = false;
   struct KPend {
     int cls;
@@ -779,36 +665,6 @@ class LlamaEngine {
     e_lm.logits = w.logits.as<float>();
     e_lm.amax = w.amax.as<float2>();
 
-    const bool is_target_m = &m == &target;
-    if (mega_on && f.logits && !f.ee && !f.capture && T <= kMegaMaxT) {
-      // one persistent launch for the whole forward (mega.cu)
-      MegaCtx& mc = is_target_m ? mtg : md;
-      MegaStep st{};
-      st.rows = rows;
-      st.T = T;
-      st.n_req = f.n_req;
-      st.max_rows = f.max_rows;
-      st.max_ctx = f.max_ctx;
-      st.argmax_out = f.argmax_out;
-      LCK(mega_attn_plan(s, f.n_req, f.max_rows, f.max_ctx, w.attn.as<float>(), w.attn_bytes, &st));
-      const double wbytes = 2.0 * ((static_cast<double>(s.qkv_out()) * s.d + static_cast<double>(s.d) * qd +
-                                    3.0 * s.ffn * s.d) * s.layers + static_cast<double>(s.vocab) * s.d);
-      const double kvb = static_cast<double>(f.kv_tokens) * 2 * s.n_kv * s.hd * 2 * s.layers;
-      MegaModelDev dv = mc.dev;
-      static const int mega_minb = getenv("FASER_MEGA_MINB") ? atoi(getenv("FASER_MEGA_MINB")) : 4;
-      dv.min_blocks = mega_minb;
-      dv.kv = kv;
-      static const bool trace_on = getenv("FASER_MEGA_TRACE") != nullptr;
-      if (trace_on && is_target_m) {
-        if (!mega_trace.p) mega_trace.alloc(sizeof(unsigned long long) * ((2 * mega_phases(s.layers) + 4) * mc.grid + 4096));
-        LCK(cudaMemsetAsync(mega_trace.p, 0, mega_trace.bytes, fs));
-        st.trace = mega_trace.as<unsigned long long>();
-      }
-      timed(is_target_m ? 5 : 6, wbytes + kvb, [&] { LCK(mega_forward(dv, st, mc.grid, fs)); });
-      ++launches;
-      if (st.trace) dump_mega_trace(s.layers, mc.grid);
-      return;
-    }
     if (!f.pre_embedded) {
       LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), fs));
       ++launches;
@@ -1307,9 +1163,8 @@ class LlamaEngine {
         throw LFail{FASER_EINVAL, "invalid exit policy"};
       }
     }
-    // fused draft control (one launch between draft forwards) unless the persistent forward,
-    // which embeds and reduces the argmax itself, is on
-    const bool fuse_draft = !mega_on && !(getenv("FASER_UNFUSED_DRAFT") && getenv("FASER_UNFUSED_DRAFT")[0] == '1');
+    // fused draft control (one launch between draft forwards)
+    const bool fuse_draft = !(getenv("FASER_UNFUSED_DRAFT") && getenv("FASER_UNFUSED_DRAFT")[0] == '1');
     // verify: tokens + embedding in one launch, argmax + truth scatter in one launch (not under
     // TP, whose argmax is the all-gathered merge, nor with the persistent forward)
     const bool fuse_verify = fuse_draft && tp == 1;

@@ -342,8 +342,7 @@ class ServingEngine:
         return lib().faser_kernel_launches(self.h)
 
     # ---- per-kernel-class device timing (CUDA events around launches)
-    KERNEL_CLASSES = ("verify_gemm", "verify_attention", "draft_gemm", "draft_attention", "verify_lm_head",
-                      "verify_forward", "draft_forward")
+    KERNEL_CLASSES = ("verify_gemm", "verify_attention", "draft_gemm", "draft_attention", "verify_lm_head")
 
     def set_kernel_timing(self, enabled):
         _check(lib().faser_set_kernel_timing(self.h, 1 if enabled else 0), self.h)
