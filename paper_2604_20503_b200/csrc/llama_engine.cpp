@@ -225,13 +225,17 @@ struct LmWork {
   // residual stream: fp32 x, its bf16 copy xb (GEMM operand), per-128-column sums of squares
   Mem x, xb, ss, xs, xbs, sss;  // (+ scratch copies for early-exit compaction)
   Mem ob, q, h, logits, amax, attn, argmax, src_of;
+  // fused exit-test estimator (target only): gathered W_lm[d] rows, z_d blocks [rows][128],
+  // drafted id per row, per-(vocab tile, row) rank counts
+  Mem wg, zd, row_d, rank_cnt;
+  std::vector<GemmOperand> op_wg;  // one 128-row block of wg each
   size_t attn_bytes = 0;
   GemmOperand op_xb, op_ob, op_h;
   // persistent row metadata (draft steps)
   Mem meta;
   RowsDev rows{};
 
-  void build(const LlamaShape& s, int cap, int lm_cap) {
+  void build(const LlamaShape& s, int cap, int lm_cap, bool rank = false) {
     rows_cap = cap;
     lm_rows_cap = lm_cap;
     const int64_t d = s.d, qd = static_cast<int64_t>(s.n_q) * s.hd;
@@ -254,6 +258,16 @@ struct LmWork {
     LCK(make_act_operand(&op_xb, xb.p, cap, s.d));
     LCK(make_act_operand(&op_ob, ob.p, cap, static_cast<int>(qd)));
     LCK(make_act_operand(&op_h, h.p, cap, s.ffn));
+    if (rank) {
+      const int blocks = (lm_cap + 127) / 128;
+      wg.alloc(static_cast<size_t>(blocks) * 128 * d * 2);
+      zd.alloc(static_cast<size_t>(blocks) * 128 * 128 * 4);
+      row_d.alloc(static_cast<size_t>(blocks) * 128 * 4);
+      rank_cnt.alloc(static_cast<size_t>(s.vocab / 128) * lm_cap * 4);
+      op_wg.resize(blocks);
+      for (int b = 0; b < blocks; ++b)
+        LCK(make_weight_operand(&op_wg[b], wg.as<__nv_bfloat16>() + static_cast<size_t>(b) * 128 * d, 128, s.d));
+    }
     meta.alloc(static_cast<size_t>(cap) * 9 * 4 + 64);
     int* m = meta.as<int>();
     rows.n_rows = m;
@@ -457,7 +471,7 @@ class LlamaEngine {
     draft.build(dsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream);
     target.build(tsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream, tp, tp_rank);
     wd.build(dsh, cap, B);
-    wt.build(target.sh, cap, verify_rows);
+    wt.build(target.sh, cap, verify_rows, cfg.mode >= FASER_MODE_VSD_AD_EE);
     if (tp > 1) {
       tp_part.alloc(static_cast<size_t>(cap) * tsh.d * 4);
       tp_loc.alloc(static_cast<size_t>(cap) * 8);
@@ -718,14 +732,41 @@ class LlamaEngine {
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {
-        LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_lm, fs));
+        // fused exit-test estimator (no top-K, no T x V logits): z_d of every
+        // row through the LM head's own accumulation order (W_lm[d] gathered, one 128 x 128
+        // block-diagonal launch per 128 rows), then the LM head counts the outranking ids per
+        // tile in its epilogue and exit_rank sums them
+        LCK(lm_rank_prep(cur_q, rows, m.lm, s.d, w.wg.as<__nv_bfloat16>(), w.row_d.as<int>(), T, fs));
+        GemmPlan pz;
+        pz.bn = 128;
+        pz.mc = 1;
+        pz.splits = 1;  // K order of the LM head (splits = 1)
+        pz.deep = true;
+        for (int b = 0; b * 128 < T; ++b) {
+          EpiArgs ez = base;
+          ez.mode = kEpiStore;
+          ez.ss_in = w.ss.as<float>();
+          ez.out = w.zd.as<float>();
+          ez.t_begin = b * 128;
+          ez.w_after_wait = 1;  // wg was written by rank_prep: no weight prefetch before the PDL wait
+          LCK(gemm_fused(w.op_wg[b], w.op_xb, 128, pz, ez, fs));
+        }
+        EpiArgs e_rank = e_lm;
+        e_rank.mode = kEpiRank;
+        e_rank.logits = f.capture ? w.logits.as<float>() : nullptr;
+        e_rank.amax = nullptr;
+        e_rank.zd_src = w.zd.as<float>();
+        e_rank.row_d = w.row_d.as<int>();
+        e_rank.rank_cnt = w.rank_cnt.as<int>();
+        LCK(gemm_fused(m.op_lm, w.op_xb, T, p_lm, e_rank, fs));
         if (f.capture) capture_stage(layer, m, w, f);
-        LCK(lm_exit_test(sl, cur_q, rows, w.logits.as<float>(), 1, 0, s.vocab, f.k_table[layer], T, fs));
+        LCK(lm_exit_rank(sl, cur_q, rows, w.rank_cnt.as<int>(), s.vocab / 128, T, f.k_table[layer], T, fs));
+        launches += 3 + (T + 127) / 128;
         LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), fs, f.q0));
         LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(),
                            w.ss.as<float>(), w.xs.as<float>(), w.xbs.as<__nv_bfloat16>(), w.sss.as<float>(),
                            fs));
-        launches += 5;
+        launches += 2;
       }
     }
     if (f.logits) {

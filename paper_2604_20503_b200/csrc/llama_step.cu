@@ -4,9 +4,12 @@
 //                          step t runs the requests whose budget min(k_i, remaining) > t.
 //   verify prep          : verify row i,j has input token ctx.back() (j = 0) or drafted[j-1]
 //                          and predicts drafted[j] (full_verify, sdcore.cpp:61-81).
-//   exit test (K4)       : token_exit_test (exitctl.cpp:56-68) on LM-head logits of the
+//   exit test (K4)       : token_exit_test (exitctl.cpp:56-68) on the LM head of the
 //                          intermediate residual: prune iff >= K(layer) ids outrank drafted[j]
-//                          (ties: lower id outranks), no Top-K materialisation.
+//                          (ties: lower id outranks). No Top-K and no T x V logits: rank_prep
+//                          gathers W_lm[d], a block-diagonal GEMM gives z_d in the LM head's own
+//                          accumulation order, the LM head's epilogue counts outranking ids per
+//                          128-id tile (tc_gemm.cu kEpiRank) and exit_rank sums the tiles.
 //   frontier (K4)        : verify_with_early_exit's per-layer scan (sdcore.cpp:111-132):
 //                          earliest failing j prunes rows j.. of that request; surviving rows are
 //                          compacted so the remaining layers' GEMM/attention tiles shrink.
@@ -257,37 +260,39 @@ __global__ void truth_scatter_kernel(RowsDev rows, const int* __restrict__ argma
   truth_rj[rows.row_req[i] * kMS + rows.row_j[i]] = argmax[i];
 }
 
-constexpr int kExitThreads = 256;
-
-__global__ void __launch_bounds__(kExitThreads) exit_test_kernel(LmSlots sl, LmReqState rq, RowsDev rows,
-                                                                 const float* __restrict__ logits, int splits,
-                                                                 int64_t split_stride, int vocab, int k_thr) {
-  __shared__ int red[kExitThreads / 32];
+// K4 fused-estimator prep: each verify row's drafted id d (-1 when the row is off the frontier)
+// and W_lm[d] gathered into wg[row] (row 0 of W_lm for rows without a test), so a [128-row block
+// x 128] tcgen05 GEMM per block computes z_d in the LM head's own accumulation order.
+__global__ void rank_prep_kernel(LmReqState rq, RowsDev rows, const __nv_bfloat16* __restrict__ wlm, int d,
+                                 __nv_bfloat16* __restrict__ wg, int* __restrict__ row_d) {
   const int r = blockIdx.x;
-  if (r >= *rows.n_rows) return;
+  int tok = -1;
+  if (r < *rows.n_rows) {
+    const int req = rows.row_req[r], j = rows.row_j[r];
+    if (j < rq.active[req]) tok = rq.drafted[req * kMS + j];
+  }
+  FASER_DCHECK(tok < static_cast<int>(kTokLimit), "FASER check: rank prep token %d\n", tok);
+  if (threadIdx.x == 0) row_d[r] = tok;
+  const uint4* src = reinterpret_cast<const uint4*>(wlm + static_cast<int64_t>(tok < 0 ? 0 : tok) * d);
+  uint4* dst = reinterpret_cast<uint4*>(wg + static_cast<int64_t>(r) * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// K4 fused-estimator decision: sum of the per-tile rank counts of the LM head's kEpiRank epilogue
+// (one warp per row) >= k_thr -> the row fails the exit test (exitctl.cpp:56-68).
+__global__ void exit_rank_kernel(LmSlots sl, LmReqState rq, RowsDev rows, const int* __restrict__ cnt, int n_tiles,
+                                 int t_stride, int k_thr, int rows_cap) {
+  const int r = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows_cap || r >= *rows.n_rows) return;
   const int req = rows.row_req[r], j = rows.row_j[r];
   if (j >= rq.active[req]) return;
   const int slot = rq.slot[req];
   if (sl.ncomm[slot] + j == sl.exempt[slot]) return;  // re-entry exemption (sdcore.cpp:118-119)
-  const int d = rq.drafted[req * kMS + j];
-  const float* z = logits + static_cast<int64_t>(r) * vocab;
-  float zd = z[d];
-  for (int s = 1; s < splits; ++s) zd += z[s * split_stride + d];
-  int cnt = 0;
-  for (int v = threadIdx.x; v < vocab; v += kExitThreads) {
-    float zv = z[v];
-    for (int s = 1; s < splits; ++s) zv += z[s * split_stride + v];
-    cnt += (zv > zd) || (zv == zd && v < d);
-  }
+  int c = 0;
+  for (int t = lane; t < n_tiles; t += 32) c += cnt[static_cast<int64_t>(t) * t_stride + r];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int i = 0; i < kExitThreads / 32; ++i) tot += red[i];
-    if (tot >= k_thr) atomicOr(&rq.failmask[req], 1u << j);
-  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0 && c >= k_thr) atomicOr(&rq.failmask[req], 1u << j);
 }
 
 // One thread per request (n <= 1024), single CTA.
@@ -680,10 +685,17 @@ cudaError_t lm_truth_scatter(RowsDev rows, const int* argmax, int* truth_rj, int
   truth_scatter_kernel<<<cdiv(rows_cap, 128), 128, 0, s>>>(rows, argmax, truth_rj, rows_cap);
   return cudaGetLastError();
 }
-cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,
-                         int64_t split_stride, int vocab, int k_thr, int rows_cap, cudaStream_t s) {
+cudaError_t lm_rank_prep(LmReqState rq, RowsDev rows, const __nv_bfloat16* wlm, int d, __nv_bfloat16* wg,
+                         int* row_d, int rows_cap, cudaStream_t s) {
   if (rows_cap <= 0) return cudaSuccess;
-  exit_test_kernel<<<rows_cap, kExitThreads, 0, s>>>(sl, rq, rows, logits, splits, split_stride, vocab, k_thr);
+  if (d % 8) return cudaErrorInvalidValue;
+  rank_prep_kernel<<<rows_cap, 128, 0, s>>>(rq, rows, wlm, d, wg, row_d);
+  return cudaGetLastError();
+}
+cudaError_t lm_exit_rank(LmSlots sl, LmReqState rq, RowsDev rows, const int* cnt, int n_tiles, int t_stride,
+                         int k_thr, int rows_cap, cudaStream_t s) {
+  if (rows_cap <= 0) return cudaSuccess;
+  exit_rank_kernel<<<cdiv(rows_cap, 4), 128, 0, s>>>(sl, rq, rows, cnt, n_tiles, t_stride, k_thr, rows_cap);
   return cudaGetLastError();
 }
 cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,

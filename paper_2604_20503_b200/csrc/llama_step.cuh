@@ -94,9 +94,14 @@ cudaError_t lm_verify_tokens(LmSlots sl, LmReqState rq, RowsDev rows, int rows_c
 cudaError_t lm_verify_init(LmReqState rq, int n, int layers, int eos, cudaStream_t s);
 // final argmax rows -> truth_rj[request][j].
 cudaError_t lm_truth_scatter(RowsDev rows, const int* argmax, int* truth_rj, int rows_cap, cudaStream_t s);
-// K4: rank-count exit test of every live row against its drafted token at gated `layer`.
-cudaError_t lm_exit_test(LmSlots sl, LmReqState rq, RowsDev rows, const float* logits, int splits,
-                         int64_t split_stride, int vocab, int k_thr, int rows_cap, cudaStream_t s);
+// K4 fused estimator (no T x V logits): rank_prep writes each live row's drafted id (row_d, -1
+// off the frontier) and gathers W_lm[d] into wg [rows][d]; a block-diagonal GEMM over wg gives z_d;
+// the LM head's kEpiRank epilogue counts, per 128-id tile, the ids outranking d; exit_rank sums
+// the tiles and sets the failmask bit when the count reaches k_thr.
+cudaError_t lm_rank_prep(LmReqState rq, RowsDev rows, const __nv_bfloat16* wlm, int d, __nv_bfloat16* wg,
+                         int* row_d, int rows_cap, cudaStream_t s);
+cudaError_t lm_exit_rank(LmSlots sl, LmReqState rq, RowsDev rows, const int* cnt, int n_tiles, int t_stride,
+                         int k_thr, int rows_cap, cudaStream_t s);
 // K4 frontier: per request earliest failing row prunes the suffix; compacts the row set.
 // src_of[new_row] = old row; the residual (x fp32, xb bf16, ss per-chunk sums of squares) is
 // gathered through scratch buffers of the same shapes.

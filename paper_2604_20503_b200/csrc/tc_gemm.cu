@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = blockIdx.x * MC * kBM;                       // first weight row of this CTA
   const int ntile = min(MC, n_out / kBM - static_cast<int>(blockIdx.x) * MC);  // weight tiles here
-  const int n0 = blockIdx.y * BN;
+  const int n0 = ea.t_begin + blockIdx.y * BN;
   const int kb0 = blockIdx.z * kb_per_split;
   const int kb1 = min(kb_total, kb0 + kb_per_split);
   const int nkb = kb1 - kb0;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128, 1)
   const int ngrp = issue / 100, gsz = issue % 100;
   const int pst = lane / gsz, pg = lane % gsz;  // lane group (first stage) and box slot of this lane
   const bool producer = warp == 0 && pst < ngrp;
-  const int npre = nkb < C::kStages ? nkb : C::kStages;
+  const int npre = ea.w_after_wait ? 0 : (nkb < C::kStages ? nkb : C::kStages);
   const uint64_t pol_w = sm100::policy_evict_first();
   if (producer) {
     for (int i = pst; i < npre; i += ngrp) {
@@ -227,6 +227,11 @@ __global__ void __launch_bounds__(128, 1)
         rs = rsqrtf(((part[0] + part[1]) + (part[2] + part[3])) / ea.d_norm + ea.eps);
       }
       s_rs[t] = rs;
+      if (ea.mode == kEpiRank) {  // the row's drafted id and its z_d (s_pos / s_page reused)
+        const int row = n0 + t;
+        s_pos[t] = ea.row_d[row];
+        s_page[t] = __float_as_int(ea.zd_src[static_cast<size_t>(row) * kBM + (row & (kBM - 1))]);
+      }
       if (ea.mode == kEpiQkv) {
         const int row = n0 + t;
         const int pos = ea.rows.row_pos[row];
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(128, 1)
     // rows of one token, 4 tokens per pass.
     const int mode = ea.mode;
     const int c4 = lane * 4;
-    if (mode == kEpiStore || mode == kEpiResid || mode == kEpiLogits) {
+    if (mode == kEpiStore || mode == kEpiResid || mode == kEpiLogits || mode == kEpiRank) {
       for (int t = ts + warp; t < te; t += 4) {
         const float rs = s_rs[t];
         float4 a = *reinterpret_cast<const float4*>(S + t * kBM + c4);
@@ -321,6 +326,22 @@ __global__ void __launch_bounds__(128, 1)
   #pragma unroll
           for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
           if (lane == 0) ea.ss_out[static_cast<size_t>(m0 / kBM) * ea.t_stride + n0 + t] = q;
+        } else if (mode == kEpiRank) {
+          // token_exit_test's rank count (exitctl.cpp:56-68) on this tile's 128 ids: the same
+          // fp32 products acc * rs as the materialised logits, compared against z_d
+          a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+          if (ea.logits) *reinterpret_cast<float4*>(ea.logits + idx) = a;  // debug capture only
+          const float zd = __int_as_float(s_page[t]);
+          const int dd = s_pos[t];
+          const int id0 = ea.id_off + m0 + c4;
+          int c = 0;
+          c += (id0 != dd) & ((a.x > zd) | ((a.x == zd) & (id0 < dd)));
+          c += (id0 + 1 != dd) & ((a.y > zd) | ((a.y == zd) & (id0 + 1 < dd)));
+          c += (id0 + 2 != dd) & ((a.z > zd) | ((a.z == zd) & (id0 + 2 < dd)));
+          c += (id0 + 3 != dd) & ((a.w > zd) | ((a.w == zd) & (id0 + 3 < dd)));
+  #pragma unroll
+          for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+          if (lane == 0) ea.rank_cnt[static_cast<size_t>(m0 / kBM) * ea.t_stride + n0 + t] = c;
         } else {  // kEpiLogits
           a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
           if (ea.logits) *reinterpret_cast<float4*>(ea.logits + idx) = a;  // validation / exit test only

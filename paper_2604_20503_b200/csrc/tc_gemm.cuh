@@ -26,6 +26,8 @@ enum EpiMode : int {
   kEpiQkv = 2,     // RoPE(q,k) at row_pos; q -> bf16 [t][n_q*hd]; k,v -> paged KV cache
   kEpiSwiglu = 3,  // h[t][j] = bf16(silu(gate*rs) * up*rs), gate/up interleaved in 64-row groups
   kEpiLogits = 4,  // logits[t][v] = acc*rs (fp32) + per-tile (max, lowest idx) per token
+  kEpiRank = 5,    // fused exit-test estimator: per (vocab tile, token) count of ids outranking the
+                   // token's drafted id d (z_v > z_d, or = and v < d), z_d from zd_src; no logits
 };
 
 // Everything the fused epilogue may need (unused fields ignored per mode).
@@ -51,6 +53,15 @@ struct EpiArgs {
   float* logits = nullptr;               // kEpiLogits [t][n_out]; nullptr: argmax partials only
   float2* amax = nullptr;                // kEpiLogits [n_out/128][t_stride] (value, idx bits)
   int id_off = 0;                        // kEpiLogits: id of output row 0 (vocab-parallel shard)
+  // kEpiRank: z_d of token t = zd_src[t * 128 + t % 128] (a [t][128] block-diagonal GEMM over the
+  // gathered rows W[d_t], same accumulation order as this LM head), d_t = row_d[t] (-1: no test);
+  // counts -> rank_cnt[n_out/128][t_stride]. logits (optional) are written as in kEpiLogits.
+  const float* zd_src = nullptr;
+  const int* row_d = nullptr;
+  int* rank_cnt = nullptr;
+  int t_begin = 0;                       // first token of this launch (token tiles start here)
+  int w_after_wait = 0;                  // 1: the weights are written by the previous kernel (no
+                                         // weight prefetch before griddepcontrol.wait)
   // optional timeline (tools/layer_chain.py): per CTA 8 globaltimer stamps [cta][8] = entry, after
   // griddepcontrol.wait, first stage landed, accumulators complete, split-K reduced, exit
   unsigned long long* trace = nullptr;
