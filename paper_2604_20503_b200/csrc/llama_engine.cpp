@@ -34,6 +34,7 @@
 #include "llama_step.cuh"
 #include "tp.cuh"
 #include "tc_gemm.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 namespace faser {
 namespace {
@@ -290,6 +291,15 @@ struct LmWork {
   }
 };
 
+// NVTX ranges of the step phases (host enqueue side; nsys / ncu --nvtx project them onto the
+// GPU timeline). Header-only NVTX3: no cost unless a tool is attached.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+
 int num_sms_dev() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -309,7 +319,7 @@ class LlamaEngine {
   LmWork wd, wt;
   int tp = 1, tp_rank = 0;  // tensor-parallel verification of the target (tp.cuh)
   TpGroup* tpg = nullptr;
-  Mem tp_part, tp_loc, tp_all;  // row-parallel partial [rows][d] fp32; argmax partials (float2)
+  Mem tp_part, tp_loc, tp_all;  // row-parallel partial [rows][d] bf16; argmax partials (float2)
   cudaStream_t stream = nullptr;   // draft lane (and everything in serial mode)
   cudaStream_t vstream = nullptr;  // verify lane of the overlapped (FULL) mode
   cudaStream_t fs = nullptr;       // stream the current forward() launches on
@@ -473,7 +483,7 @@ class LlamaEngine {
     wd.build(dsh, cap, B);
     wt.build(target.sh, cap, verify_rows, cfg.mode >= FASER_MODE_VSD_AD_EE);
     if (tp > 1) {
-      tp_part.alloc(static_cast<size_t>(cap) * tsh.d * 4);
+      tp_part.alloc(static_cast<size_t>(cap) * tsh.d * 2);
       tp_loc.alloc(static_cast<size_t>(cap) * 8);
       tp_all.alloc(static_cast<size_t>(cap) * 8 * tp);
     }
@@ -669,9 +679,9 @@ class LlamaEngine {
     e_glu.h = w.h.as<__nv_bfloat16>();
     e_glu.ffn = s.ffn;
     const bool is_tp_target = tp > 1 && &m == &target;
-    EpiArgs e_part = base;  // row-parallel TP partial (fp32 [T][d], summed over ranks afterwards)
+    EpiArgs e_part = base;  // row-parallel TP partial (bf16 [T][d], summed over ranks afterwards)
     e_part.mode = kEpiStore;
-    e_part.out = tp_part.as<float>();
+    e_part.out_bf16 = tp_part.as<__nv_bfloat16>();
     EpiArgs e_lm = base;
     if (is_tp_target) e_lm.id_off = tp_rank * s.vocab;  // global token ids of this vocab shard
     e_lm.mode = kEpiLogits;
@@ -712,8 +722,8 @@ class LlamaEngine {
       const bool tp_rows = is_tp_target;  // row-parallel: partial sums -> all-reduce -> residual add
       auto row_parallel = [&](const GemmOperand& wop, const GemmOperand& xop, const GemmPlan& pl) {
         LCK(gemm_fused(wop, xop, T, pl, e_part, fs));
-        LCK(tpg->allreduce_sum(tp_rank, tp_part.as<float>(), static_cast<size_t>(T) * s.d, fs));
-        LCK(tp_resid_add(tp_part.as<float>(), w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), T, s.d, fs));
+        LCK(tpg->allreduce_sum(tp_rank, tp_part.as<__nv_bfloat16>(), static_cast<size_t>(T) * s.d, fs));
+        LCK(tp_resid_add(tp_part.as<__nv_bfloat16>(), w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), T, s.d, fs));
         launches += 2;
       };
       if (tp_rows)
@@ -886,6 +896,7 @@ class LlamaEngine {
   }
 
   void step(const faser_step_plan* plan, faser_round_result* out, int cap, int* n_out) {
+    Nvtx nv_step("faser.step");
     LCK(cudaSetDevice(cfg.device));
     admit_pending();
     const int n = static_cast<int>(live.size());
@@ -1158,6 +1169,7 @@ class LlamaEngine {
       capturing = true;
     }
     LCK(record_event(ev[0]));
+    nvtxRangePushA("faser.admit_prefill");
     LCK(lm_ptab_scatter(ptab.as<int>(), max_pages, dev_of(b_tr), n_tr, stream));
     LCK(lm_admit(sl, dev_of(b_adm), static_cast<int>(newly.size()), stream));
     launches += (n_tr > 0) + (!newly.empty());
@@ -1184,6 +1196,7 @@ class LlamaEngine {
       forward(draft, wd, f);
       forward(target, wt, f);
     }
+    nvtxRangePop();  // faser.admit_prefill
     // ---- early-exit configuration
     const bool capture = cfg.debug_capture != 0;
     const bool ee = cfg.mode >= FASER_MODE_VSD_AD_EE;
@@ -1339,9 +1352,12 @@ class LlamaEngine {
       tl_lp = lp;
       tl_valid = true;
     } else {
+      nvtxRangePushA("faser.draft");
       for (int t = 0; t < kmax; ++t) draft_step(t, nullptr);
+      nvtxRangePop();
       LCK(record_event(ev[1]));
       // ---- verify (+ early exit)
+      Nvtx nv_verify("faser.verify");
       LCK(lm_verify_init(q, n, L, eos, stream));
       Fwd f;
       if (fuse_verify) {

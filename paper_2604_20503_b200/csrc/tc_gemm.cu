@@ -312,7 +312,15 @@ __global__ void __launch_bounds__(128, 1)
         float4 a = *reinterpret_cast<const float4*>(S + t * kBM + c4);
         const size_t idx = static_cast<size_t>(n0 + t) * n_out + m0 + c4;
         if (mode == kEpiStore) {
-          *reinterpret_cast<float4*>(ea.out + idx) = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+          if (ea.out_bf16) {
+            __nv_bfloat162 b0 = __floats2bfloat162_rn(a.x * rs, a.y * rs), b1 = __floats2bfloat162_rn(a.z * rs, a.w * rs);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&b0);
+            pk.y = *reinterpret_cast<uint32_t*>(&b1);
+            *reinterpret_cast<uint2*>(ea.out_bf16 + idx) = pk;
+          } else {
+            *reinterpret_cast<float4*>(ea.out + idx) = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
+          }
         } else if (mode == kEpiResid) {
           const float4 xv = *reinterpret_cast<const float4*>(ea.x + idx);
           a = make_float4(xv.x + a.x, xv.y + a.y, xv.z + a.z, xv.w + a.w);

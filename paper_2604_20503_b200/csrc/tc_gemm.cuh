@@ -40,6 +40,7 @@ struct EpiArgs {
   int ss_chunks = 0, d_norm = 0;
   float eps = 0.f;
   float* out = nullptr;                  // kEpiStore
+  __nv_bfloat16* out_bf16 = nullptr;     // kEpiStore: bf16 output instead of `out` (TP partials)
   float* x = nullptr;                    // kEpiResid
   __nv_bfloat16* xb = nullptr;           // kEpiResid
   float* ss_out = nullptr;               // kEpiResid [n_out/128][t_stride]

@@ -20,15 +20,16 @@ namespace {
 constexpr int kMaxTp = 8;
 
 struct Ptrs {
-  const float* p[kMaxTp];
+  const __nv_bfloat16* p[kMaxTp];
 };
 
-__global__ void sum_ranks_kernel(Ptrs in, int n_ranks, float* __restrict__ out, size_t n) {
+// bf16 partials, fp32 accumulation in rank order (deterministic), bf16 result
+__global__ void sum_ranks_kernel(Ptrs in, int n_ranks, __nv_bfloat16* __restrict__ out, size_t n) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float a = 0.f;
-    for (int r = 0; r < n_ranks; ++r) a += in.p[r][i];  // rank order: deterministic
-    out[i] = a;
+    for (int r = 0; r < n_ranks; ++r) a += __bfloat162float(in.p[r][i]);
+    out[i] = __float2bfloat16_rn(a);
   }
 }
 
@@ -73,11 +74,11 @@ class LocalGroup : public TpGroup {
   }
   const char* backend() const override { return "local"; }
 
-  cudaError_t allreduce_sum(int rank, float* buf, size_t n, cudaStream_t s) override {
+  cudaError_t allreduce_sum(int rank, __nv_bfloat16* buf, size_t n, cudaStream_t s) override {
     cudaError_t e;
     if (tmp_cap_[rank] < n) {
       if (tmp_[rank]) cudaFree(tmp_[rank]);
-      if ((e = cudaMalloc(&tmp_[rank], n * sizeof(float))) != cudaSuccess) return e;
+      if ((e = cudaMalloc(&tmp_[rank], n * sizeof(__nv_bfloat16))) != cudaSuccess) return e;
       tmp_cap_[rank] = n;
     }
     slots_[rank] = buf;
@@ -85,7 +86,7 @@ class LocalGroup : public TpGroup {
     bar_.wait();  // every rank's buffer is registered and its producer event recorded
     Ptrs in{};
     for (int q = 0; q < size; ++q) {
-      in.p[q] = slots_[q];
+      in.p[q] = reinterpret_cast<const __nv_bfloat16*>(slots_[q]);
       if ((e = cudaStreamWaitEvent(s, ready_[q], 0)) != cudaSuccess) return e;
     }
     sum_ranks_kernel<<<296, 256, 0, s>>>(in, size, tmp_[rank], n);
@@ -94,19 +95,20 @@ class LocalGroup : public TpGroup {
     bar_.wait();  // every rank has enqueued its reads
     for (int q = 0; q < size; ++q)
       if ((e = cudaStreamWaitEvent(s, done_[q], 0)) != cudaSuccess) return e;
-    e = cudaMemcpyAsync(buf, tmp_[rank], n * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    e = cudaMemcpyAsync(buf, tmp_[rank], n * sizeof(__nv_bfloat16), cudaMemcpyDeviceToDevice, s);
     bar_.wait();  // slots_ may be overwritten by the next call only after everyone read them
     return e;
   }
 
   cudaError_t allgather_f2(int rank, const float2* in, float2* out, size_t n, cudaStream_t s) override {
     cudaError_t e;
-    slots_[rank] = reinterpret_cast<float*>(const_cast<float2*>(in));
+    slots_[rank] = const_cast<float2*>(in);
     if ((e = cudaEventRecord(ready_[rank], s)) != cudaSuccess) return e;
     bar_.wait();
     for (int q = 0; q < size; ++q) {
       if ((e = cudaStreamWaitEvent(s, ready_[q], 0)) != cudaSuccess) return e;
-      if ((e = cudaMemcpyAsync(out + q * n, slots_[q], n * sizeof(float2), cudaMemcpyDeviceToDevice, s)) !=
+      if ((e = cudaMemcpyAsync(out + q * n, static_cast<const float2*>(slots_[q]), n * sizeof(float2),
+                               cudaMemcpyDeviceToDevice, s)) !=
           cudaSuccess)
         return e;
     }
@@ -120,9 +122,9 @@ class LocalGroup : public TpGroup {
 
  private:
   Barrier bar_;
-  std::vector<float*> slots_;
+  std::vector<void*> slots_;
   std::vector<cudaEvent_t> ready_, done_;
-  std::vector<float*> tmp_;
+  std::vector<__nv_bfloat16*> tmp_;
   std::vector<size_t> tmp_cap_;
 };
 
@@ -167,9 +169,9 @@ class NcclGroup : public TpGroup {
     if (comm) nccl().comm_destroy(comm);
   }
   const char* backend() const override { return "nccl"; }
-  cudaError_t allreduce_sum(int, float* buf, size_t n, cudaStream_t s) override {
-    return nccl().all_reduce(buf, buf, n, ncclFloat32, ncclSum, comm, s) == ncclSuccess ? cudaSuccess
-                                                                                          : cudaErrorUnknown;
+  cudaError_t allreduce_sum(int, __nv_bfloat16* buf, size_t n, cudaStream_t s) override {
+    return nccl().all_reduce(buf, buf, n, ncclBfloat16, ncclSum, comm, s) == ncclSuccess ? cudaSuccess
+                                                                                           : cudaErrorUnknown;
   }
   cudaError_t allgather_f2(int, const float2* in, float2* out, size_t n, cudaStream_t s) override {
     return nccl().all_gather(in, out, 2 * n, ncclFloat32, comm, s) == ncclSuccess ? cudaSuccess
@@ -178,13 +180,13 @@ class NcclGroup : public TpGroup {
 };
 
 // ------------------------------------------------------------------ kernels
-__global__ void __launch_bounds__(128) resid_add_kernel(const float* __restrict__ part, float* __restrict__ x,
+__global__ void __launch_bounds__(128) resid_add_kernel(const __nv_bfloat16* __restrict__ part, float* __restrict__ x,
                                                         __nv_bfloat16* __restrict__ xb, float* __restrict__ ss,
                                                         int T, int d) {
   __shared__ float red[4];
   const int t = blockIdx.x, c = blockIdx.y * 128 + threadIdx.x;
   const size_t i = static_cast<size_t>(t) * d + c;
-  const float v = x[i] + part[i];
+  const float v = x[i] + __bfloat162float(part[i]);
   x[i] = v;
   xb[i] = __float2bfloat16_rn(v);
   float q = v * v;
@@ -278,7 +280,7 @@ TpGroup* tp_nccl_group_create(const uint8_t* id, int size, int rank, int device,
   return g;
 }
 
-cudaError_t tp_resid_add(const float* part, float* x, __nv_bfloat16* xb, float* ss, int T, int d, cudaStream_t s) {
+cudaError_t tp_resid_add(const __nv_bfloat16* part, float* x, __nv_bfloat16* xb, float* ss, int T, int d, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   resid_add_kernel<<<dim3(T, d / 128), 128, 0, s>>>(part, x, xb, ss, T, d);
   return cudaGetLastError();

@@ -26,8 +26,9 @@ class TpGroup {
  public:
   virtual ~TpGroup() = default;
   int size = 1;
-  // in place: buf = sum over ranks of buf (fp32, n elements); stream-ordered
-  virtual cudaError_t allreduce_sum(int rank, float* buf, size_t n, cudaStream_t s) = 0;
+  // in place: buf = sum over ranks of buf (bf16 partials, n elements: half the bytes of fp32 on
+  // NVLink); stream-ordered
+  virtual cudaError_t allreduce_sum(int rank, __nv_bfloat16* buf, size_t n, cudaStream_t s) = 0;
   // out[r * n + i] = in_r[i] for every rank r (float2 elements); stream-ordered
   virtual cudaError_t allgather_f2(int rank, const float2* in, float2* out, size_t n, cudaStream_t s) = 0;
   virtual const char* backend() const = 0;
@@ -40,7 +41,7 @@ bool tp_nccl_unique_id(uint8_t* out, const char** err);
 
 // x += part; xb = bf16(x); ss[c][t] = sum of squares of 128-column chunk c (row-parallel epilogue
 // after the all-reduce), rows [0, T) of width d.
-cudaError_t tp_resid_add(const float* part, float* x, __nv_bfloat16* xb, float* ss, int T, int d, cudaStream_t s);
+cudaError_t tp_resid_add(const __nv_bfloat16* part, float* x, __nv_bfloat16* xb, float* ss, int T, int d, cudaStream_t s);
 // per-row local (max, lowest global id) over this rank's vocab tiles -> loc[T]
 cudaError_t tp_local_argmax(int n_tiles, int T, const float2* amax, float2* loc, cudaStream_t s);
 // merge the gathered [tp][T] partials: out[t] = lowest id among the maxima
