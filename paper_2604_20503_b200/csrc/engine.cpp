@@ -466,6 +466,12 @@ faser_status faser_release(faser_engine* e, int64_t req_id) {
   });
 }
 
+faser_status faser_last_step_prefill(const faser_engine* e, float* prefill_ms) {
+  if (!e || !prefill_ms) return FASER_EINVAL;
+  *prefill_ms = e->llama ? faser::llama_last_step_prefill(e->llama) : 0.f;
+  return FASER_OK;
+}
+
 faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, float* verify_ms,
                                     float* step_ms) {
   if (!e) return FASER_EINVAL;

@@ -349,7 +349,7 @@ class LlamaEngine {
   int eos = 0;
   std::string err;
   int64_t launches = 0, h2d = 0, d2h = 0;
-  float t_draft = 0.f, t_verify = 0.f, t_step = 0.f;
+  float t_draft = 0.f, t_verify = 0.f, t_step = 0.f, t_prefill = 0.f;
 
   // slots
   Mem s_tok, s_len, s_ncomm, s_maxout, s_done, s_exempt, ptab;
@@ -1196,6 +1196,7 @@ class LlamaEngine {
       forward(draft, wd, f);
       forward(target, wt, f);
     }
+    LCK(record_event(ev[3]));  // end of admission + prefill
     nvtxRangePop();  // faser.admit_prefill
     // ---- early-exit configuration
     const bool capture = cfg.debug_capture != 0;
@@ -1427,6 +1428,7 @@ class LlamaEngine {
     LCK(cudaStreamSynchronize(stream));
     if (ktiming) resolve_kernel_timing();
     cudaEventElapsedTime(&t_draft, ev[0], ev[1]);
+    cudaEventElapsedTime(&t_prefill, ev[0], ev[3]);
     cudaEventElapsedTime(&t_verify, ev[1], ev[2]);
     cudaEventElapsedTime(&t_step, ev[0], ev[2]);
     if (tl_valid) build_timeline();
@@ -1569,6 +1571,7 @@ faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev,
   return FASER_OK;
 }
 
+float llama_last_step_prefill(const LlamaEngine* e) { return e->t_prefill; }
 void llama_last_step_timing(const LlamaEngine* e, float* d, float* v, float* s) {
   if (d) *d = e->t_draft;
   if (v) *v = e->t_verify;

@@ -93,7 +93,7 @@ template <int BN, int ST, int MC>
 __global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ EpiArgs ea, int n_out, int kb_total, int kb_per_split, int splits,
-                int issue) {
+                int issue, int xbox) {
   using C = Cfg<BN, ST, MC>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(128, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producers (one lane group per stage)
-    const int xboxes = (min(BN, T - n0) + kXBox - 1) / kXBox;  // skip all-padding activation boxes
-    const uint32_t xbytes = xboxes * kXBox * kBK * 2;
+    const int xboxes = (min(BN, T - n0) + xbox - 1) / xbox;  // skip all-padding activation boxes
+    const uint32_t xbytes = xboxes * xbox * kBK * 2;
     if (producer) {
       for (int i = pst; i < nkb; i += ngrp) {
         const int s = i % C::kStages;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(128, 1)
           if (b < nw)
             sm100::tma_load_2d_hint(sA + s * C::kAStage + b * kABytes, &tmW, &full[s], kc, mb + b * kBM, pol_w);
           else
-            sm100::tma_load_2d(sB + s * C::kBBytes + (b - nw) * kXBox * 128, &tmX, &full[s], kc, n0 + (b - nw) * kXBox);
+            sm100::tma_load_2d(sB + s * C::kBBytes + (b - nw) * xbox * 128, &tmX, &full[s], kc, n0 + (b - nw) * xbox);
         }
       }
     }
@@ -477,10 +477,27 @@ cudaError_t launch_bn(const GemmOperand& w, const GemmOperand& x, int t, int spl
     const char* e = std::getenv("FASER_TMA_ISSUE");
     return e ? std::atoi(e) : 1;
   }();
-  const int boxes = MC + BN / kXBox;
+  // activation box rows: one box per stage for row tiles >= 64 (FASER_XBOX=32 keeps 32-row boxes)
+  static const int xbox_cap = [] {
+    const char* e = std::getenv("FASER_XBOX");
+    return e ? std::atoi(e) : 256;
+  }();
+  int xbox = kXBox;
+  const CUtensorMap* xm = &x.map;
+  if (x.wide) {
+    for (int i = 2; i >= 0; --i) {
+      const int r = 64 << i;
+      if (((x.wide >> i) & 1) && r <= BN && r <= xbox_cap) {
+        xbox = r;
+        xm = &x.map_rows[i];
+        break;
+      }
+    }
+  }
+  const int boxes = MC + BN / xbox;
   const int issue = mode == 0 ? 101 : mode == 2 ? ST * 100 + 1 : mode == 3 ? 100 + (boxes < 32 ? boxes : 32)
                                                                         : ST * 100 + 32 / ST;
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST, MC>, w.map, x.map, ea, w.rows, kb_total, kps, z, issue);
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<BN, ST, MC>, w.map, *xm, ea, w.rows, kb_total, kps, z, issue, xbox);
 }
 
 }  // namespace
@@ -516,7 +533,16 @@ cudaError_t make_weight_operand(GemmOperand* op, const void* w, int n_out, int k
   return make_operand(op, w, n_out, k, kBM);
 }
 cudaError_t make_act_operand(GemmOperand* op, const void* x, int rows_cap, int k) {
-  return make_operand(op, x, rows_cap, k, kXBox);
+  cudaError_t e = make_operand(op, x, rows_cap, k, kXBox);
+  if (e != cudaSuccess) return e;
+  op->wide = 0;
+  for (int i = 0; i < 3 && (64 << i) <= rows_cap; ++i) {
+    GemmOperand t;
+    if ((e = make_operand(&t, x, rows_cap, k, 64 << i)) != cudaSuccess) return e;
+    op->map_rows[i] = t.map;
+    op->wide |= 1 << i;
+  }
+  return cudaSuccess;
 }
 
 // Launch plan, from a (BN, splits, depth) sweep of graph-timed back-to-back launches on B200

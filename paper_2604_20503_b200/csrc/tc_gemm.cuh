@@ -11,6 +11,12 @@ namespace faser {
 // A bf16 row-major [rows][k] matrix with its TMA descriptor (SWIZZLE_128B, box 64 x box_rows).
 struct GemmOperand {
   CUtensorMap map;
+  // activation operands: the same tensor with 64 / 128 / 256-row boxes (map has 32-row boxes).
+  // One box per pipeline stage for wide row tiles: a TMA box costs ~0.5 us of issue latency per
+  // issuing warp regardless of its size (tools/tma_probe.cu, profiles/r02_tma_box_probe.jsonl),
+  // so four 32-row boxes per stage cap a CTA at a quarter of the 128-row box's ingest.
+  CUtensorMap map_rows[3];
+  int wide = 0;  // bit i: map_rows[i] (64 << i rows per box) valid (box rows <= tensor rows)
   const void* base = nullptr;
   int rows = 0;
   int k = 0;

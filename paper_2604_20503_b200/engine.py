@@ -330,6 +330,12 @@ class ServingEngine:
         _check(lib().faser_last_step_timing(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def last_step_prefill_ms(self):
+        """Admission + prefill part of the last step's draft-lane time (ms)."""
+        a = C.c_float()
+        _check(lib().faser_last_step_prefill(self.h, C.byref(a)))
+        return a.value
+
     def last_step_bytes(self):
         a, b = C.c_int64(), C.c_int64()
         _check(lib().faser_last_step_bytes(self.h, C.byref(a), C.byref(b)))
