@@ -240,7 +240,8 @@ def make_engine(desc, args, local_rank, batch=None, **tp):
             "ov": abi.MODE_FULL, "full": abi.MODE_FULL, "vsd_ee": abi.MODE_VSD_AD_EE}[args.mode]
     return engine.ServingEngine(desc=desc, max_batch=batch or args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
                                 mode=mode, default_spec_length=args.k, max_spec_length=16,
-                                prefill_rows=8192, device=local_rank, **tp)
+                                prefill_rows=8192, device=local_rank,
+                                prefill_lane=0 if (tp or args.no_prefill_lane) else 1, **tp)
 
 
 def tp_bootstrap(dist, rank, make_uid):
@@ -516,11 +517,13 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
     st = {"first": {}, "last": {}}
     dev_clock[0] = 0.0
     launches0 = eng.kernel_launches()
-    acc_ms = {"draft": 0.0, "verify": 0.0}
+    acc_ms = {"prefill": 0.0, "draft": 0.0, "verify": 0.0}
 
     def clock_acc():
         d, v, _ = eng.last_step_timing()
-        acc_ms["draft"] += d
+        pf = eng.last_step_prefill_ms()
+        acc_ms["prefill"] += pf
+        acc_ms["draft"] += d - pf
         acc_ms["verify"] += v
         return clock()
 
@@ -529,6 +532,7 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
         ev0.record(stream)
         t0 = time.perf_counter()
         tokens = run_llama_steps(eng, args.steps, clock_acc, st, feeder, gate=gate, drafter=drafter, hook=hook, book=book)
+        eng.join_lanes()  # the last admissions' prefill (side lane) inside the timed region
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -538,6 +542,7 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
     out = {"B": B, "dev_ms": dev_ms, "tokens": tokens, "steps_run": st.get("steps", 0), "fill_steps": fill_steps,
            "p50_tpot_ms": p50_tpot_ms(st["first"], st["last"]), "launches": launches, "clocks": clk.summary(),
            "wall_s": wall, "draft_ms": acc_ms["draft"] / nsteps, "verify_ms": acc_ms["verify"] / nsteps,
+           "prefill_ms": acc_ms["prefill"] / nsteps,
            "acceptance": st.get("acc", 0) / max(st.get("sub", 1), 1),
            "layer_work": st.get("flr", 0.0) / max(st.get("sub", 1), 1)}
     if want_kstats:
@@ -622,7 +627,8 @@ def llama_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": head["e2e"]["d2h_bytes_per_step"]},
         "gpu_launches": int(head["launches"]),
         "clocks": head["clocks"],
-        "device_ms_per_step": {"draft": head["draft_ms"], "verify_accept": head["verify_ms"]},
+        "device_ms_per_step": {"admit_prefill": head["prefill_ms"], "draft": head["draft_ms"],
+                               "verify_accept": head["verify_ms"]},
         "acceptance": head["acceptance"],
         "layer_work_per_drafted_token": head["layer_work"],
         "fill_steps": head["fill_steps"],
@@ -864,6 +870,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded batch sweep")
+    ap.add_argument("--no-prefill-lane", action="store_true",
+                    help="prefill admissions in the step itself instead of on the side lane")
     ap.add_argument("--trace", type=float, default=0.0,
                     help="replay a bursty arrival trace of this many seconds instead of a fixed backlog")
     ap.add_argument("--trace-rate", type=float, default=26.0, help="mean arrival rate (req/s) of --trace")

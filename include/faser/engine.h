@@ -199,7 +199,11 @@ typedef struct faser_engine_cfg {
   int32_t max_spec_length; /* LLAMA: largest k_i a step may use (verify row capacity); 0 = 16 */
   int32_t prefill_rows;    /* LLAMA: rows per prefill forward chunk; 0 = 8192 */
   int32_t debug_capture;   /* LLAMA: 1 = keep per-stage logits of the last step for validation */
-  int32_t reserved1;
+  int32_t prefill_lane;    /* LLAMA: 1 = newly admitted requests are prefilled on a side stream
+                              (lower priority, own activations) concurrently with the running
+                              batch's draft + verify, and join the batch at the next step (not
+                              with TP, FULL mode or debug_capture); 0 = admission + prefill +
+                              draft + verify in the admission step */
   /* Tensor-parallel verification (config 5): the TARGET is split over tp_size
    * ranks (column-parallel QKV / gate-up, row-parallel O / down + all-reduce, vocab-parallel LM
    * head + all-gathered argmax); the draft is replicated. tp_size <= 1: no TP. Modes VSD and
@@ -275,6 +279,12 @@ int32_t faser_pending_work(const faser_engine* e);
  * verify lane and whole step. */
 faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, float* verify_ms,
                                     float* step_ms);
+/* Makes the engine stream wait for every side lane's enqueued work (the admission-prefill lane),
+ * so an event recorded on faser_engine_stream afterwards covers it. */
+faser_status faser_engine_join_lanes(faser_engine* e);
+/* Part of the last step's draft-lane time spent on admissions + their prefill forwards (ms,
+ * from the step start; 0 for the toy engine). */
+faser_status faser_last_step_prefill(const faser_engine* e, float* prefill_ms);
 /* Bytes the last faser_step copied host->device (step plan + admissions) and
  * device->host (round results). */
 faser_status faser_last_step_bytes(const faser_engine* e, int64_t* h2d, int64_t* d2h);

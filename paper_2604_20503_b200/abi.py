@@ -104,7 +104,7 @@ class EngineCfg(C.Structure):
         ("mode", C.c_int32), ("default_spec_length", C.c_int32), ("exempt_rule", C.c_int32),
         ("exit_policy", ExitPolicy), ("max_pending", C.c_int32), ("pending_tokens", C.c_int32),
         ("max_spec_length", C.c_int32), ("prefill_rows", C.c_int32), ("debug_capture", C.c_int32),
-        ("reserved1", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("tp_group", C.c_void_p),
+        ("prefill_lane", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("tp_group", C.c_void_p),
     ]
 
 

@@ -466,6 +466,11 @@ faser_status faser_release(faser_engine* e, int64_t req_id) {
   });
 }
 
+faser_status faser_engine_join_lanes(faser_engine* e) {
+  if (!e) return FASER_EINVAL;
+  return e->llama ? faser::llama_join_lanes(e->llama) : FASER_OK;
+}
+
 faser_status faser_last_step_prefill(const faser_engine* e, float* prefill_ms) {
   if (!e || !prefill_ms) return FASER_EINVAL;
   *prefill_ms = e->llama ? faser::llama_last_step_prefill(e->llama) : 0.f;

@@ -322,6 +322,24 @@ class LlamaEngine {
   Mem tp_part, tp_loc, tp_all;  // row-parallel partial [rows][d] bf16; argmax partials (float2)
   cudaStream_t stream = nullptr;   // draft lane (and everything in serial mode)
   cudaStream_t vstream = nullptr;  // verify lane of the overlapped (FULL) mode
+  // admission-prefill lane (cfg.prefill_lane): newly admitted requests are prefilled on pstream
+  // (lower priority, own work buffers) while the running batch drafts and verifies on `stream`;
+  // they join the batch at the next step, whose start waits for the prefill
+  cudaStream_t pstream = nullptr;
+  // In-flight prefill batches, oldest first: the requests they prefill stay out of the steps
+  // until their event completes (polled at each step start, never waited on while other
+  // requests can run). Each batch's row metadata lives in its own step blob, so the blobs form a
+  // ring of kBlobs and a blob is reused only once no in-flight batch reads it.
+  struct PfBatch {
+    int blob;
+    std::vector<int64_t> ids;
+  };
+  std::deque<PfBatch> pf_q;
+  cudaEvent_t ev_pf_go = nullptr;
+  cudaEvent_t ev_pf_done[4] = {};  // per blob
+  bool pf_lane = false;
+  LmWork wd_pf, wt_pf;
+  std::vector<int64_t> run;  // the requests this step drafts and verifies
   cudaStream_t fs = nullptr;       // stream the current forward() launches on
   cudaEvent_t ev[4] = {};
   cudaEvent_t ev_chunk[FASER_MAX_SPEC + 1] = {};
@@ -359,8 +377,12 @@ class LlamaEngine {
   LmReqState rq{};
   LmReqState cur_q{};  // rq + this step's per-request arrays (slot, k, ...) in the blob
   // step blob
-  Mem d_blob;
-  char* h_blob = nullptr;
+  static constexpr int kBlobs = 4;
+  Mem d_blobs[kBlobs];
+  char* h_blobs[kBlobs] = {};
+  int blob_i = 0;
+  char* h_blob = nullptr;  // the current step's blob (host, pinned) and its device copy
+  char* d_blob = nullptr;
   size_t blob_cap = 0;
   faser_round_result* h_res = nullptr;
   Mem d_res;
@@ -370,6 +392,7 @@ class LlamaEngine {
     std::vector<int32_t> prompt, committed;
     int32_t max_out = 0, spec = 0, slot = -1, len = 0;
     bool done = false, admitted = false;
+    bool prefilling = false;  // admission prefill in flight on the prefill lane
     std::vector<int32_t> pages;
   };
   std::unordered_map<int64_t, Req> reqs;
@@ -391,7 +414,8 @@ class LlamaEngine {
   ~LlamaEngine() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto& kv : reqs) (void)kv;
-    if (h_blob) cudaFreeHost(h_blob);
+    for (char* hb : h_blobs)
+      if (hb) cudaFreeHost(hb);
     if (h_res) cudaFreeHost(h_res);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -405,6 +429,13 @@ class LlamaEngine {
     if (h_lane) cudaFreeHost(h_lane);
     lanes.reset();
     if (vstream) cudaStreamDestroy(vstream);
+    if (pstream) {
+      cudaStreamSynchronize(pstream);
+      cudaStreamDestroy(pstream);
+    }
+    if (ev_pf_go) cudaEventDestroy(ev_pf_go);
+    for (auto e : ev_pf_done)
+      if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -449,6 +480,19 @@ class LlamaEngine {
       LCK(cudaStreamCreateWithPriority(&vstream, cudaStreamNonBlocking, mode == 1 ? hi : lo));
     }
     fs = stream;
+    pf_lane = cfg.prefill_lane != 0 && !(cfg.tp_size > 1) && cfg.mode != FASER_MODE_FULL && !graph_mode;
+    if (pf_lane) {
+      // the running batch's stream gets the higher priority: prefill CTAs fill the SMs its
+      // latency-bound draft / verify kernels leave idle
+      int lo = 0, hi = 0;
+      LCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      LCK(cudaStreamDestroy(stream));
+      LCK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
+      fs = stream;
+      LCK(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, lo));
+      LCK(cudaEventCreateWithFlags(&ev_pf_go, cudaEventDisableTiming));
+      for (auto& e : ev_pf_done) LCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     for (auto& e : ev) LCK(cudaEventCreate(&e));
     for (auto& e : ev_chunk) LCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto* arr : {ev_d0, ev_d1, ev_v0, ev_v1})
@@ -482,6 +526,11 @@ class LlamaEngine {
     target.build(tsh, m->bigram_a, m->bigram_b, n_pages, max_seq, stream, tp, tp_rank);
     wd.build(dsh, cap, B);
     wt.build(target.sh, cap, verify_rows, cfg.mode >= FASER_MODE_VSD_AD_EE);
+    if (pf_lane) {  // the prefill lane's own activations (no logits: lm rows 1)
+      const int pcap = std::max(prefill_rows, cfg.max_seq_len);
+      wd_pf.build(dsh, pcap, 1);
+      wt_pf.build(target.sh, pcap, 1);
+    }
     if (tp > 1) {
       tp_part.alloc(static_cast<size_t>(cap) * tsh.d * 2);
       tp_loc.alloc(static_cast<size_t>(cap) * 8);
@@ -534,8 +583,12 @@ class LlamaEngine {
                static_cast<size_t>(B) * cfg.max_seq_len * (4 + 16) +   // prompts + prefill rows
                static_cast<size_t>(B) * (9 * 4 + 64) +                  // per-chunk arrays
                sizeof(int32_t) * kLaneInts + 64;                        // lane state
-    LCK(cudaMallocHost(reinterpret_cast<void**>(&h_blob), blob_cap));
-    d_blob.alloc(blob_cap);
+    for (int b = 0; b < (pf_lane ? kBlobs : 1); ++b) {
+      LCK(cudaMallocHost(reinterpret_cast<void**>(&h_blobs[b]), blob_cap));
+      d_blobs[b].alloc(blob_cap);
+    }
+    h_blob = h_blobs[0];
+    d_blob = d_blobs[0].as<char>();
     LCK(cudaMallocHost(reinterpret_cast<void**>(&h_res), sizeof(faser_round_result) * B));
     d_res.alloc(sizeof(faser_round_result) * B);
     for (int s = B - 1; s >= 0; --s) free_slots.push_back(s);
@@ -843,7 +896,7 @@ class LlamaEngine {
   }
   template <class T>
   T* dev_of(const T* host) const {
-    return reinterpret_cast<T*>(d_blob.as<char>() + (reinterpret_cast<const char*>(host) - h_blob));
+    return reinterpret_cast<T*>(d_blob + (reinterpret_cast<const char*>(host) - h_blob));
   }
 
   // PipelineTimeline of the last overlapped step (overlap.cpp:44-91 semantics, measured): event
@@ -899,7 +952,61 @@ class LlamaEngine {
     Nvtx nv_step("faser.step");
     LCK(cudaSetDevice(cfg.device));
     admit_pending();
-    const int n = static_cast<int>(live.size());
+    // prefill-lane step: the requests whose prefill completed run; the new ones are admitted and
+    // prefilled on pstream; those still prefilling sit the step out. With nothing able to run,
+    // the oldest prefill is waited for; with nothing running or prefilling, the new requests are
+    // prefilled and stepped serially (the plain path).
+    bool lane_pf = false;
+    if (pf_lane) {
+      auto retire = [&](bool wait) {
+        while (!pf_q.empty()) {
+          const cudaEvent_t e = ev_pf_done[pf_q.front().blob];
+          if (wait) {
+            LCK(cudaEventSynchronize(e));
+            wait = false;
+          } else {
+            const cudaError_t q = cudaEventQuery(e);
+            if (q == cudaErrorNotReady) break;
+            LCK(q);
+          }
+          for (int64_t id : pf_q.front().ids) {
+            auto it = reqs.find(id);
+            if (it != reqs.end()) it->second.prefilling = false;
+          }
+          pf_q.pop_front();
+        }
+      };
+      retire(false);
+      bool any_ready = false, any_fresh = false;
+      for (int64_t id : live) {
+        const Req& r = reqs.at(id);
+        if (!r.admitted) any_fresh = true;
+        else if (!r.prefilling) any_ready = true;
+      }
+      if (!any_ready && !pf_q.empty()) {  // nothing can run before the oldest prefill ends
+        retire(true);
+        retire(false);
+        any_ready = true;
+      }
+      lane_pf = any_fresh && any_ready && cfg.debug_capture == 0 &&
+                !(cfg.mode == FASER_MODE_FULL && plan && plan->overlap.enabled);
+      // this step's blob must not be read by an in-flight prefill
+      blob_i = (blob_i + 1) % kBlobs;
+      for (bool busy = true; busy;) {
+        busy = false;
+        for (const PfBatch& b : pf_q) busy |= b.blob == blob_i;
+        if (busy) retire(true);
+      }
+      h_blob = h_blobs[blob_i];
+      d_blob = d_blobs[blob_i].as<char>();
+    }
+    run.clear();
+    for (int64_t id : live) {
+      const Req& r = reqs.at(id);
+      if (r.prefilling) continue;
+      if (!lane_pf || r.admitted) run.push_back(id);
+    }
+    const int n = static_cast<int>(run.size());
     *n_out = n;
     if (n == 0) return;
     if (cap < n) throw LFail{FASER_ECAPACITY, "result capacity smaller than live batch"};
@@ -914,11 +1021,8 @@ class LlamaEngine {
     };
     std::vector<LmAdmit> admits;
     std::vector<int64_t> newly;
-    for (int i = 0; i < n; ++i) {
-      Req& r = reqs.at(live[i]);
-      if (r.admitted) continue;
-      newly.push_back(r.id);
-    }
+    for (int64_t id : live)
+      if (!reqs.at(id).admitted) newly.push_back(id);
     // ---- per request k' and ordering
     struct Ent {
       int live_idx, k;
@@ -927,7 +1031,7 @@ class LlamaEngine {
     int kmax = 0, total = 0, maxctx = 0;
     int64_t ctx_sum = 0;
     for (int i = 0; i < n; ++i) {
-      Req& r = reqs.at(live[i]);
+      Req& r = reqs.at(run[i]);
       const int remaining = r.max_out - static_cast<int>(r.committed.size());
       int k = std::min(r.spec, remaining);
       k = std::min(k, max_spec);
@@ -936,7 +1040,7 @@ class LlamaEngine {
     }
     std::stable_sort(ents.begin(), ents.end(), [](const Ent& a, const Ent& b) { return a.k > b.k; });
     for (int i = 0; i < n; ++i) {
-      Req& r = reqs.at(live[ents[i].live_idx]);
+      Req& r = reqs.at(run[ents[i].live_idx]);
       kmax = std::max(kmax, ents[i].k);
       total += ents[i].k;
       // draft & verify write positions len-1 .. len+k-2
@@ -966,7 +1070,7 @@ class LlamaEngine {
     {
       int row = 0;
       for (int i = 0; i < n; ++i) {
-        Req& r = reqs.at(live[ents[i].live_idx]);
+        Req& r = reqs.at(run[ents[i].live_idx]);
         b_slot[i] = r.slot;
         b_k[i] = ents[i].k;
         b_spec[i] = r.spec;
@@ -1016,7 +1120,7 @@ class LlamaEngine {
         h.pos0 = carve<int32_t>(off, n);
         int row = 0;
         for (int i = 0; i < n; ++i) {
-          Req& r = reqs.at(live[ents[i].live_idx]);
+          Req& r = reqs.at(run[ents[i].live_idx]);
           const int j1 = std::min(ents[i].k, q0 + c);
           h.first[i] = row;
           h.nn[i] = std::max(0, j1 - q0);
@@ -1125,7 +1229,7 @@ class LlamaEngine {
       }
     }
     const size_t blob_bytes = off;
-    LCK(cudaMemcpyAsync(d_blob.p, h_blob, blob_bytes, cudaMemcpyHostToDevice, stream));
+    LCK(cudaMemcpyAsync(d_blob, h_blob, blob_bytes, cudaMemcpyHostToDevice, stream));
     h2d = static_cast<int64_t>(blob_bytes);
     d2h = static_cast<int64_t>(sizeof(faser_round_result)) * n;
 
@@ -1173,6 +1277,12 @@ class LlamaEngine {
     LCK(lm_ptab_scatter(ptab.as<int>(), max_pages, dev_of(b_tr), n_tr, stream));
     LCK(lm_admit(sl, dev_of(b_adm), static_cast<int>(newly.size()), stream));
     launches += (n_tr > 0) + (!newly.empty());
+    cudaStream_t ps = stream;  // stream of the admission prefill
+    if (lane_pf && !chunks.empty()) {
+      LCK(cudaEventRecord(ev_pf_go, stream));  // slot rows + page table written
+      LCK(cudaStreamWaitEvent(pstream, ev_pf_go, 0));
+      ps = pstream;
+    }
     for (const Chunk& c : chunks) {
       RowsDev pr;
       pr.n_rows = dev_of(c.nrows);
@@ -1184,7 +1294,7 @@ class LlamaEngine {
       pr.req_n = dev_of(c.nn);
       pr.req_slot = dev_of(c.rslot);
       pr.req_pos0 = dev_of(c.pos0);
-      LCK(lm_prefill_tokens(sl, pr, c.T, stream));
+      LCK(lm_prefill_tokens(sl, pr, c.T, ps));
       ++launches;
       Fwd f;
       f.rows = pr;
@@ -1192,9 +1302,15 @@ class LlamaEngine {
       f.n_req = c.nreq;
       f.max_rows = c.maxrows;
       f.max_ctx = c.maxctx;
-      fs = stream;  // (fs may still name the verify lane of the previous overlapped step)
-      forward(draft, wd, f);
-      forward(target, wt, f);
+      fs = ps;  // (fs may still name the verify lane of the previous overlapped step)
+      forward(draft, ps == stream ? wd : wd_pf, f);
+      forward(target, ps == stream ? wt : wt_pf, f);
+    }
+    fs = stream;
+    if (ps != stream) {
+      LCK(cudaEventRecord(ev_pf_done[blob_i], pstream));
+      pf_q.push_back({blob_i, newly});
+      for (int64_t id : newly) reqs.at(id).prefilling = true;
     }
     LCK(record_event(ev[3]));  // end of admission + prefill
     nvtxRangePop();  // faser.admit_prefill
@@ -1436,10 +1552,13 @@ class LlamaEngine {
     // ---- host bookkeeping: commit mirror, page rollback, retire finished requests
     for (int64_t id : newly) reqs.at(id).admitted = true;
     std::vector<int64_t> keep;
-    keep.reserve(n);
+    keep.reserve(live.size());
+    if (pf_lane)  // admitted or still prefilling on the lane: drafted from a later step
+      for (int64_t id : live)
+        if (reqs.at(id).prefilling) keep.push_back(id);
     for (int p = 0; p < n; ++p) {
       const faser_round_result& rr = h_res[p];
-      Req& r = reqs.at(live[p]);
+      Req& r = reqs.at(run[p]);
       r.committed.insert(r.committed.end(), rr.tokens, rr.tokens + rr.committed);
       r.len += rr.committed;
       r.done = rr.done != 0;
@@ -1572,6 +1691,11 @@ faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev,
 }
 
 float llama_last_step_prefill(const LlamaEngine* e) { return e->t_prefill; }
+faser_status llama_join_lanes(LlamaEngine* e) {
+  return lguard(e, [&] {
+    if (!e->pf_q.empty()) LCK(cudaStreamWaitEvent(e->stream, e->ev_pf_done[e->pf_q.back().blob], 0));
+  });
+}
 void llama_last_step_timing(const LlamaEngine* e, float* d, float* v, float* s) {
   if (d) *d = e->t_draft;
   if (v) *v = e->t_verify;

