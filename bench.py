@@ -547,7 +547,10 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
            "layer_work": st.get("flr", 0.0) / max(st.get("sub", 1), 1)}
     if want_kstats:
         # per-kernel-class CUDA-event timing over steps that immediately follow the timed region
-        # (event records between launches would perturb the PDL overlap being timed)
+        # (event records between launches would perturb the PDL overlap being timed); the
+        # prefill lane is off for them, so each class is timed without a co-running prefill
+        if not args.no_prefill_lane:
+            eng.set_prefill_lane(False)
         eng.set_kernel_timing(True)
         run_llama_steps(eng, max(args.steps // 2, 3), clock, {"first": {}, "last": {}}, feeder, gate=gate,
                         drafter=drafter, hook=hook, book=book)

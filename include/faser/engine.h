@@ -279,6 +279,9 @@ int32_t faser_pending_work(const faser_engine* e);
  * verify lane and whole step. */
 faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, float* verify_ms,
                                     float* step_ms);
+/* Switches the admission-prefill lane of an engine created with prefill_lane = 1 off (0: the
+ * next step drains it and admissions are prefilled in-step again) or back on (1). */
+faser_status faser_set_prefill_lane(faser_engine* e, int32_t on);
 /* Makes the engine stream wait for every side lane's enqueued work (the admission-prefill lane),
  * so an event recorded on faser_engine_stream afterwards covers it. */
 faser_status faser_engine_join_lanes(faser_engine* e);

@@ -466,6 +466,12 @@ faser_status faser_release(faser_engine* e, int64_t req_id) {
   });
 }
 
+faser_status faser_set_prefill_lane(faser_engine* e, int32_t on) {
+  if (!e) return FASER_EINVAL;
+  if (!e->llama) return on ? FASER_EINVAL : FASER_OK;
+  return faser::llama_set_prefill_lane(e->llama, on);
+}
+
 faser_status faser_engine_join_lanes(faser_engine* e) {
   if (!e) return FASER_EINVAL;
   return e->llama ? faser::llama_join_lanes(e->llama) : FASER_OK;

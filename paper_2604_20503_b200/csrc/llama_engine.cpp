@@ -957,7 +957,7 @@ class LlamaEngine {
     // the oldest prefill is waited for; with nothing running or prefilling, the new requests are
     // prefilled and stepped serially (the plain path).
     bool lane_pf = false;
-    if (pf_lane) {
+    if (pstream) {  // the lane exists (cfg.prefill_lane); pf_lane: currently used
       auto retire = [&](bool wait) {
         while (!pf_q.empty()) {
           const cudaEvent_t e = ev_pf_done[pf_q.front().blob];
@@ -977,6 +977,7 @@ class LlamaEngine {
         }
       };
       retire(false);
+      while (!pf_lane && !pf_q.empty()) retire(true);  // lane switched off: drain it
       bool any_ready = false, any_fresh = false;
       for (int64_t id : live) {
         const Req& r = reqs.at(id);
@@ -988,7 +989,7 @@ class LlamaEngine {
         retire(false);
         any_ready = true;
       }
-      lane_pf = any_fresh && any_ready && cfg.debug_capture == 0 &&
+      lane_pf = pf_lane && any_fresh && any_ready && cfg.debug_capture == 0 &&
                 !(cfg.mode == FASER_MODE_FULL && plan && plan->overlap.enabled);
       // this step's blob must not be read by an in-flight prefill
       blob_i = (blob_i + 1) % kBlobs;
@@ -1691,6 +1692,12 @@ faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev,
 }
 
 float llama_last_step_prefill(const LlamaEngine* e) { return e->t_prefill; }
+faser_status llama_set_prefill_lane(LlamaEngine* e, int on) {
+  return lguard(e, [&] {
+    if (on && !e->pstream) throw LFail{FASER_EINVAL, "the engine was created without prefill_lane"};
+    e->pf_lane = on != 0;
+  });
+}
 faser_status llama_join_lanes(LlamaEngine* e) {
   return lguard(e, [&] {
     if (!e->pf_q.empty()) LCK(cudaStreamWaitEvent(e->stream, e->ev_pf_done[e->pf_q.back().blob], 0));

@@ -330,6 +330,9 @@ class ServingEngine:
         _check(lib().faser_last_step_timing(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def set_prefill_lane(self, on):
+        _check(lib().faser_set_prefill_lane(self.h, 1 if on else 0), self.h)
+
     def join_lanes(self):
         """Engine stream waits for the admission-prefill lane (before a closing timing event)."""
         _check(lib().faser_engine_join_lanes(self.h), self.h)
