@@ -140,6 +140,12 @@ extern "C" faser_status faser_k_attention(const void* q, const void* kv, const i
   kvd.ptab = ptab;
   kvd.max_pages = max_pages;
   kvd.layer_stride = 0;
+  // TMA view of the pool (the engine's default page path): the pool holds at least
+  // n_req * max_pages pages (request i's table row is i)
+  GemmOperand kv_op;
+  const int64_t kv_rows = static_cast<int64_t>(n_req) * max_pages * n_kv * 2 * 64;
+  if (kv_rows < (int64_t(1) << 31) && make_operand(&kv_op, kv, static_cast<int>(kv_rows), hd, 64) == cudaSuccess)
+    kvd.tma = &kv_op.map;
   cudaError_t e = lm_attention(m, rows, n_req, max_rows, max_ctx, kvd, 0, static_cast<const __nv_bfloat16*>(q),
                                static_cast<__nv_bfloat16*>(out), static_cast<float*>(scratch),
                                static_cast<size_t>(scratch_bytes), s);

@@ -90,7 +90,8 @@ struct KvDev {
   int max_pages;
   int64_t layer_stride;  // elements per layer
   // TMA view of the pool as [rows = layers*pages*n_kv*2*64][hd] with 64x64 boxes and the 128 B
-  // swizzle the attention kernel's shared-memory layout uses (hd 64 only; nullptr = cp.async)
+  // swizzle the attention kernel's shared-memory layout uses (hd 128: two boxes per page row
+  // block; nullptr = cp.async)
   const CUtensorMap* tma = nullptr;
 };
 

@@ -67,10 +67,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Swizzled smem tile [64 keys][HD] bf16: 16-byte chunk c of row r lives at chunk c ^ (r & 7).
+// Swizzled smem tile [64 keys][HD] bf16 in the TMA SWIZZLE_128B box layout: HD/64 boxes of
+// [64 rows][128 B]; 16-byte chunk c of row r lives in box c / 8 at chunk (c % 8) ^ (r & 7).
+// The cp.async path writes the same layout, so TMA and cp.async pages are interchangeable.
 template <int HD>
 __device__ __forceinline__ int swz(int row, int chunk) {
-  return row * (HD * 2) + ((chunk ^ (row & 7)) << 4);
+  return (chunk >> 3) * (64 * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
 
 // MT = 16-row M tiles per CTA in GROUP mode (128 threads per tile): the tiles of one (request,
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int s_last;
   __shared__ __align__(8) uint64_t full[kAttnStages<HD>];
-  const bool tma = HD == 64 && use_tma && PPS == 1;
+  const bool tma = use_tma && PPS == 1;
   // let the next (PDL-launched) GEMM start streaming its weights while attention runs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -171,12 +173,15 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   const int64_t layer_rows = kv.layer_stride / HD;
   auto load_tile = [&](int t, int buf, int h) {
     const int page = t - t0 < kMaxPagesPerCta ? s_page[t - t0] : kv.ptab[static_cast<int64_t>(slot) * kv.max_pages + t];
-    if (tma) {  // one thread, two 8 KB boxes (K, V) with the hardware swizzle
-      if (threadIdx.x == 0) {
+    if (tma) {  // 2 * HD/64 boxes of [64][64] (K and V halves, hardware swizzle), one issuing
+                // warp each: a warp's TMA boxes are served one after another (~0.5 us each)
+      const int wb = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0 && wb < 2 * (HD / 64)) {
         const int row = static_cast<int>(layer * layer_rows + (static_cast<int64_t>(page) * n_kv + kvh) * 2 * 64);
-        sm100::mbar_arrive_expect_tx(&full[buf], 2 * kTileBytes);
-        sm100::tma_load_2d(smem + buf * 2 * kTileBytes, &kvmap, &full[buf], 0, row);
-        sm100::tma_load_2d(smem + buf * 2 * kTileBytes + kTileBytes, &kvmap, &full[buf], 0, row + 64);
+        if (wb == 0) sm100::mbar_arrive_expect_tx(&full[buf], 2 * kTileBytes);  // the stage's one arrival
+        const int kvsel = wb & 1, hb = wb >> 1;  // K / V, 64-column half
+        sm100::tma_load_2d(smem + buf * 2 * kTileBytes + kvsel * kTileBytes + hb * 64 * 128, &kvmap, &full[buf],
+                           hb * 64, row + kvsel * 64);
       }
       return;
     }
@@ -492,8 +497,8 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   }
 }
 
-bool want_tma_env() {
-  static const bool v = getenv("FASER_ATTN_TMA") && getenv("FASER_ATTN_TMA")[0] == '1';
+bool want_tma_env() {  // TMA page loads unless FASER_ATTN_TMA=0
+  static const bool v = !(getenv("FASER_ATTN_TMA") && getenv("FASER_ATTN_TMA")[0] == '0');
   return v;
 }
 
@@ -510,10 +515,10 @@ cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int
   });
   dim3 grid(n_req, m.n_kv, blocks * n_split);
   static const CUtensorMap dummy{};  // read-only placeholder when TMA is off
-  // TMA page loads (one thread, hardware swizzle) measured equal to the cp.async path on B200
-  // (config 3, B = 1/32/128): opt-in FASER_ATTN_TMA=1
+  // TMA page loads (one thread per CTA, hardware swizzle; round 1 measured them equal to the
+  // cp.async path): the default whenever the pool has a TMA view (FASER_ATTN_TMA=0: cp.async)
   static const bool want_tma = want_tma_env();
-  const bool use_tma = want_tma && kv.tma != nullptr && HD == 64;
+  const bool use_tma = want_tma && kv.tma != nullptr && PPS == 1;
   attn_kernel<HD, ROWS, MT, PPS><<<grid, 128 * MT, kSmem, s>>>(use_tma ? *kv.tma : dummy, use_tma ? 1 : 0, rows, kv, layer,
                                                           m.n_q, m.n_kv, qbuf, obuf, part_o, part_ml, counters,
                                                           n_split, rows_cap, blocks, scale_log2);

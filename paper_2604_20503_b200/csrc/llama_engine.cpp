@@ -189,7 +189,7 @@ struct LmModel {
     kv_layer_stride = static_cast<int64_t>(n_pages) * s.n_kv * 2 * kPage * s.hd;
     kv.alloc(static_cast<size_t>(kv_layer_stride) * s.layers * 2);
     LCK(cudaMemsetAsync(kv.p, 0, kv.bytes, st));  // stale pages must be finite (masked P*V)
-    if (s.hd == 64) {  // TMA view of the pool for the attention kernel's page loads
+    {  // TMA view of the pool for the attention kernel's page loads ([rows][hd], 64 x 64 boxes)
       const int64_t rows = kv_layer_stride * s.layers / s.hd;
       kv_tma = rows < (int64_t(1) << 31) && make_operand(&kv_op, kv.p, static_cast<int>(rows), s.hd, 64) == cudaSuccess;
     }
