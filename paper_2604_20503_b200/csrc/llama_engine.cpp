@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -336,8 +337,13 @@ class LlamaEngine {
   };
   std::deque<PfBatch> pf_q;
   cudaEvent_t ev_pf_go = nullptr;
-  cudaEvent_t ev_pf_done[4] = {};  // per blob
+  static constexpr int kBlobs = 16;  // > the prefill batches in flight at B = 256 (admission bursts)
+  cudaEvent_t ev_pf_done[kBlobs] = {};  // per blob
   bool pf_lane = false;
+  bool pf_defer = false;  // this step: new requests wait for the lane to drain
+  int pf_in_flight_cap = 2;  // FASER_PF_INFLIGHT
+  double pf_wait_ms = 0.0;  // host time blocked on a prefill (nothing runnable / blob ring full)
+  int64_t pf_waits = 0;
   LmWork wd_pf, wt_pf;
   std::vector<int64_t> run;  // the requests this step drafts and verifies
   cudaStream_t fs = nullptr;       // stream the current forward() launches on
@@ -377,7 +383,6 @@ class LlamaEngine {
   LmReqState rq{};
   LmReqState cur_q{};  // rq + this step's per-request arrays (slot, k, ...) in the blob
   // step blob
-  static constexpr int kBlobs = 4;
   Mem d_blobs[kBlobs];
   char* h_blobs[kBlobs] = {};
   int blob_i = 0;
@@ -413,6 +418,9 @@ class LlamaEngine {
 
   ~LlamaEngine() {
     if (stream) cudaStreamSynchronize(stream);
+    if (getenv("FASER_PF_DEBUG") && pstream)
+      fprintf(stderr, "prefill lane: %lld host waits, %.2f ms blocked; host step %.1f ms (main enqueue %.1f, prefill enqueue %.1f, sync %.1f)\n",
+              static_cast<long long>(pf_waits), pf_wait_ms, h_step_ms, h_main_ms, h_pfenq_ms, h_sync_ms);
     for (auto& kv : reqs) (void)kv;
     for (char* hb : h_blobs)
       if (hb) cudaFreeHost(hb);
@@ -490,6 +498,7 @@ class LlamaEngine {
       LCK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
       fs = stream;
       LCK(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, lo));
+      if (getenv("FASER_PF_INFLIGHT")) pf_in_flight_cap = std::max(1, atoi(getenv("FASER_PF_INFLIGHT")));
       LCK(cudaEventCreateWithFlags(&ev_pf_go, cudaEventDisableTiming));
       for (auto& e : ev_pf_done) LCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
@@ -948,8 +957,15 @@ class LlamaEngine {
     I.n_events = static_cast<int32_t>(tl_events.size());
   }
 
+  double h_step_ms = 0.0, h_pfenq_ms = 0.0, h_sync_ms = 0.0, h_main_ms = 0.0;
   void step(const faser_step_plan* plan, faser_round_result* out, int cap, int* n_out) {
     Nvtx nv_step("faser.step");
+    const auto hs0 = std::chrono::steady_clock::now();
+    struct HAcc {
+      double& acc;
+      std::chrono::steady_clock::time_point t0;
+      ~HAcc() { acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+    } hacc{h_step_ms, hs0};
     LCK(cudaSetDevice(cfg.device));
     admit_pending();
     // prefill-lane step: the requests whose prefill completed run; the new ones are admitted and
@@ -957,12 +973,16 @@ class LlamaEngine {
     // the oldest prefill is waited for; with nothing running or prefilling, the new requests are
     // prefilled and stepped serially (the plain path).
     bool lane_pf = false;
+    pf_defer = false;
     if (pstream) {  // the lane exists (cfg.prefill_lane); pf_lane: currently used
       auto retire = [&](bool wait) {
         while (!pf_q.empty()) {
           const cudaEvent_t e = ev_pf_done[pf_q.front().blob];
           if (wait) {
+            const auto w0 = std::chrono::steady_clock::now();
             LCK(cudaEventSynchronize(e));
+            pf_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+            ++pf_waits;
             wait = false;
           } else {
             const cudaError_t q = cudaEventQuery(e);
@@ -991,6 +1011,10 @@ class LlamaEngine {
       }
       lane_pf = pf_lane && any_fresh && any_ready && cfg.debug_capture == 0 &&
                 !(cfg.mode == FASER_MODE_FULL && plan && plan->overlap.enabled);
+      // at most kPfInFlight prefill batches queued on the lane: more would fill the device's
+      // launch queue and block the host's enqueue of the running batch; the new requests wait
+      // (unadmitted, out of the step) until the lane drains
+      pf_defer = lane_pf && static_cast<int>(pf_q.size()) >= pf_in_flight_cap;
       // this step's blob must not be read by an in-flight prefill
       blob_i = (blob_i + 1) % kBlobs;
       for (bool busy = true; busy;) {
@@ -1007,6 +1031,7 @@ class LlamaEngine {
       if (r.prefilling) continue;
       if (!lane_pf || r.admitted) run.push_back(id);
     }
+    if (pf_defer) lane_pf = false;  // ready requests run; the new ones sit this step out
     const int n = static_cast<int>(run.size());
     *n_out = n;
     if (n == 0) return;
@@ -1022,8 +1047,9 @@ class LlamaEngine {
     };
     std::vector<LmAdmit> admits;
     std::vector<int64_t> newly;
-    for (int64_t id : live)
-      if (!reqs.at(id).admitted) newly.push_back(id);
+    if (!pf_defer)
+      for (int64_t id : live)
+        if (!reqs.at(id).admitted) newly.push_back(id);
     // ---- per request k' and ordering
     struct Ent {
       int live_idx, k;
@@ -1278,12 +1304,10 @@ class LlamaEngine {
     LCK(lm_ptab_scatter(ptab.as<int>(), max_pages, dev_of(b_tr), n_tr, stream));
     LCK(lm_admit(sl, dev_of(b_adm), static_cast<int>(newly.size()), stream));
     launches += (n_tr > 0) + (!newly.empty());
-    cudaStream_t ps = stream;  // stream of the admission prefill
-    if (lane_pf && !chunks.empty()) {
-      LCK(cudaEventRecord(ev_pf_go, stream));  // slot rows + page table written
-      LCK(cudaStreamWaitEvent(pstream, ev_pf_go, 0));
-      ps = pstream;
-    }
+    // admission prefill forwards on stream `ps`: in the step (serial) or on the prefill lane,
+    // where they are enqueued after the running batch's work so the host's launch time for
+    // them never delays the batch
+    auto enqueue_prefill = [&](cudaStream_t ps) {
     for (const Chunk& c : chunks) {
       RowsDev pr;
       pr.n_rows = dev_of(c.nrows);
@@ -1308,10 +1332,13 @@ class LlamaEngine {
       forward(target, ps == stream ? wt : wt_pf, f);
     }
     fs = stream;
-    if (ps != stream) {
-      LCK(cudaEventRecord(ev_pf_done[blob_i], pstream));
-      pf_q.push_back({blob_i, newly});
-      for (int64_t id : newly) reqs.at(id).prefilling = true;
+    };
+    const bool pf_on_lane = lane_pf && !chunks.empty();
+    if (pf_on_lane) {
+      LCK(cudaEventRecord(ev_pf_go, stream));  // slot rows + page table written
+      LCK(cudaStreamWaitEvent(pstream, ev_pf_go, 0));
+    } else {
+      enqueue_prefill(stream);
     }
     LCK(record_event(ev[3]));  // end of admission + prefill
     nvtxRangePop();  // faser.admit_prefill
@@ -1519,6 +1546,15 @@ class LlamaEngine {
       LCK(cudaEventRecord(ev_dend, ds));
       LCK(cudaStreamWaitEvent(stream, ev_dend, 0));
     }
+    h_main_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hs0).count();
+    if (pf_on_lane) {  // the admissions' prefill, behind the batch's work in host order
+      const auto e0 = std::chrono::steady_clock::now();
+      enqueue_prefill(pstream);
+      h_pfenq_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - e0).count();
+      LCK(cudaEventRecord(ev_pf_done[blob_i], pstream));
+      pf_q.push_back({blob_i, newly});
+      for (int64_t id : newly) reqs.at(id).prefilling = true;
+    }
     if (use_graph) {
       capturing = false;
       cudaGraph_t g = nullptr;
@@ -1542,7 +1578,11 @@ class LlamaEngine {
         std::memcpy(&dbg_drafted[static_cast<size_t>(ents[i].live_idx) * FASER_MAX_SPEC],
                     &dr[static_cast<size_t>(i) * FASER_MAX_SPEC], FASER_MAX_SPEC * 4);
     }
-    LCK(cudaStreamSynchronize(stream));
+    {
+      const auto s0 = std::chrono::steady_clock::now();
+      LCK(cudaStreamSynchronize(stream));
+      h_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
+    }
     if (ktiming) resolve_kernel_timing();
     cudaEventElapsedTime(&t_draft, ev[0], ev[1]);
     cudaEventElapsedTime(&t_prefill, ev[0], ev[3]);
@@ -1554,9 +1594,9 @@ class LlamaEngine {
     for (int64_t id : newly) reqs.at(id).admitted = true;
     std::vector<int64_t> keep;
     keep.reserve(live.size());
-    if (pf_lane)  // admitted or still prefilling on the lane: drafted from a later step
+    if (pf_lane)  // prefilling on the lane or deferred: drafted from a later step
       for (int64_t id : live)
-        if (reqs.at(id).prefilling) keep.push_back(id);
+        if (reqs.at(id).prefilling || (pf_defer && !reqs.at(id).admitted)) keep.push_back(id);
     for (int p = 0; p < n; ++p) {
       const faser_round_result& rr = h_res[p];
       Req& r = reqs.at(run[p]);
