@@ -556,6 +556,21 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
                         drafter=drafter, hook=hook, book=book)
         out["kstats"] = eng.kernel_stats()
         eng.set_kernel_timing(False)
+        # in-stream class costs: verify time of interleaved steps with all kernels, without the
+        # projection GEMMs (skip mask 30) and without attention (mask 1); no events between
+        # launches, so PDL overlap is intact. The skipping steps compute garbage, which is why
+        # this runs last, right before the engine is closed.
+        vt = {-1: [], 30: [], 1: []}
+        for i in range(18):
+            if not eng.live_requests():
+                break
+            m = (-1, 30, 1)[i % 3]
+            eng.debug_set_skip_mask(m)
+            feeder()
+            eng.step()
+            vt[m].append(eng.last_step_timing()[1])
+        eng.debug_set_skip_mask(-1)
+        out["instream_verify_ms"] = {str(k): sum(v) / len(v) for k, v in vt.items() if v}
     eng.close()
     if not want_e2e:
         return out
@@ -638,6 +653,9 @@ def llama_ours(args, rank, world, local_rank):
         "wall_s_timed": head["wall_s"],
     }
     line["roofline"], line["kernels"] = kernel_roofline(head["kstats"], B * args.k)
+    inst = instream_roofline(head, desc, line["kernels"])
+    if inst and line["roofline"]:
+        line["roofline"]["instream"] = inst
     line["verify_forward_roofline"] = llama_roofline(desc, B, args.k, head["verify_ms"])
     sweep = []
     for p, (d_ms, tok, _, _) in zip(points, agg):
@@ -654,6 +672,33 @@ def llama_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def instream_roofline(head, desc, kernels):
+    """The verify GEMM and attention classes' cost inside the step stream (PDL overlap intact):
+    verify time with every kernel minus verify time with the class skipped (interleaved steps,
+    FASER_SKIP masks through faser_debug_set_skip_mask), per launch, against the same
+    algorithmic bytes per launch as the event-timed classes."""
+    v = head.get("instream_verify_ms") or {}
+    if "-1" not in v or "30" not in v or not kernels:
+        return None
+    pk, src = peaks()
+    L = desc.target.layers
+    res = {"method": "verify ms with all kernels minus with the class skipped, interleaved steps, / launches",
+           "verify_ms": v["-1"]}
+    for cls, mask, per_layer in (("verify_gemm", "30", 4), ("verify_attention", "1", 1)):
+        if cls not in kernels or mask not in v:
+            continue
+        us = 1e3 * (v["-1"] - v[mask]) / (L * per_layer)
+        if us <= 0:
+            continue
+        gbs = kernels[cls]["bytes_per_launch"] / (us * 1e-6) / 1e9
+        res[cls] = {"avg_launch_us": us, "achieved_GBs": gbs, "frac_hbm": gbs / pk["hbm_gbs"]}
+        if kernels[cls].get("flops_per_launch"):
+            tfs = kernels[cls]["flops_per_launch"] / (us * 1e-6) / 1e12
+            peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+            res[cls].update({"achieved_TFs": tfs, "frac_tensor": tfs / peak})
+    return res
 
 
 def kernel_roofline(kstats, rows):

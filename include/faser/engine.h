@@ -282,6 +282,11 @@ faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, floa
 /* Switches the admission-prefill lane of an engine created with prefill_lane = 1 off (0: the
  * next step drains it and admissions are prefilled in-step again) or back on (1). */
 faser_status faser_set_prefill_lane(faser_engine* e, int32_t on);
+/* Timing experiments only (results become invalid): kernel classes the following steps skip,
+ * bitmask 1 attention, 2 qkv, 4 o, 8 gate/up, 16 down of the target verify forward (+ 32: of the
+ * prefill forwards instead); -1 restores FASER_SKIP. The bench derives in-stream class costs
+ * from the verify time with and without a class. */
+faser_status faser_debug_set_skip_mask(faser_engine* e, int32_t mask);
 /* Makes the engine stream wait for every side lane's enqueued work (the admission-prefill lane),
  * so an event recorded on faser_engine_stream afterwards covers it. */
 faser_status faser_engine_join_lanes(faser_engine* e);

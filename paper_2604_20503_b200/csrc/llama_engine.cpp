@@ -340,6 +340,7 @@ class LlamaEngine {
   static constexpr int kBlobs = 16;  // > the prefill batches in flight at B = 256 (admission bursts)
   cudaEvent_t ev_pf_done[kBlobs] = {};  // per blob
   bool pf_lane = false;
+  int skip_mask = -1;  // faser_debug_set_skip_mask (timing experiments); -1: FASER_SKIP
   bool pf_defer = false;  // this step: new requests wait for the lane to drain
   int pf_in_flight_cap = 2;  // FASER_PF_INFLIGHT
   double pf_wait_ms = 0.0;  // host time blocked on a prefill (nothing runnable / blob ring full)
@@ -768,7 +769,8 @@ class LlamaEngine {
     const double abytes = static_cast<double>(f.kv_tokens) * 2 * s.n_kv * s.hd * 2 + 4.0 * T * s.n_q * s.hd;
     // timing experiments only (FASER_SKIP bitmask, target verify forward): 1 attention, 2 qkv,
     // 4 o, 8 gate/up, 16 down — results are garbage, the step time shows each class's share
-    static const int skip_env = getenv("FASER_SKIP") ? atoi(getenv("FASER_SKIP")) : 0;
+    static const int skip_env0 = getenv("FASER_SKIP") ? atoi(getenv("FASER_SKIP")) : 0;
+    const int skip_env = skip_mask >= 0 ? skip_mask : skip_env0;
     // (bit 32: apply the mask to prefill forwards of both models instead)
     const int skip = (skip_env & 32) ? (!f.logits ? (skip_env & 31) : 0) : ((f.logits && is_target) ? skip_env : 0);
     for (int l = 0; l < s.layers; ++l) {
@@ -1732,6 +1734,9 @@ faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev,
 }
 
 float llama_last_step_prefill(const LlamaEngine* e) { return e->t_prefill; }
+faser_status llama_set_skip_mask(LlamaEngine* e, int mask) {
+  return lguard(e, [&] { e->skip_mask = mask; });
+}
 faser_status llama_set_prefill_lane(LlamaEngine* e, int on) {
   return lguard(e, [&] {
     if (on && !e->pstream) throw LFail{FASER_EINVAL, "the engine was created without prefill_lane"};

@@ -330,6 +330,10 @@ class ServingEngine:
         _check(lib().faser_last_step_timing(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def debug_set_skip_mask(self, mask):
+        """Timing experiments only: kernel classes the following steps skip (results invalid)."""
+        _check(lib().faser_debug_set_skip_mask(self.h, int(mask)), self.h)
+
     def set_prefill_lane(self, on):
         _check(lib().faser_set_prefill_lane(self.h, 1 if on else 0), self.h)
 
