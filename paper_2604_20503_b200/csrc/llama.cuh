@@ -117,6 +117,11 @@ cudaError_t lm_embed(const LlamaShape& m, const __nv_bfloat16* emb, RowsDev rows
 // argmax_lowest over the per-128-vocab-tile (max, lowest id) partials of the logits epilogue.
 cudaError_t lm_argmax_reduce(int n_tiles, RowsDev rows, int rows_cap, const float2* amax, int* out,
                              cudaStream_t s);
+// GQA-packed verify / decode rows on tcgen05 (llama_attn_tc.cu): one CTA per (request, kv head),
+// S and O in TMEM; used by lm_attention when G >= 4, <= 64 packed rows, no KV split.
+bool attn_tc_applies(const LlamaShape& m, int max_rows_per_req, int max_ctx, const KvDev& kv);
+cudaError_t lm_attention_tc(const LlamaShape& m, RowsDev rows, int n_req, KvDev kv, int layer,
+                            const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, cudaStream_t s);
 // Causal attention of every row over its request's paged KV (GQA packed, mma.sync bf16).
 cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req,
                          int max_ctx, KvDev kv, int layer, const __nv_bfloat16* qbuf,

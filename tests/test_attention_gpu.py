@@ -58,13 +58,39 @@ def run_case(L, n_q, n_kv, hd, rows_per_req, ctx, seed=0):
             assert err < 3e-2, (i, h, err)
 
 
+# "batch": enough (request, kv head) units that no KV split is wanted (with FASER_ATTN_TC=1, GQA
+# groups of >= 4 heads take the tcgen05 kernel, llama_attn_tc.cu): odd / even page counts,
+# 1..1500 keys
+BATCH_ROWS = [4] * 20 + [1, 2, 3, 5, 8, 4, 4, 4]
+BATCH_CTX = [4, 63, 64, 65, 127, 128, 129, 191, 192, 193, 255, 256, 257, 600, 640, 700, 900, 1000, 1280, 1500,
+             1, 2, 70, 300, 64, 130, 500, 777]
+
+
 @pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (12, 12, 64), (32, 8, 128), (8, 8, 128)])
-@pytest.mark.parametrize("shape", ["decode", "verify", "prefill", "ragged"])
+@pytest.mark.parametrize("shape", ["decode", "verify", "prefill", "ragged", "batch"])
 def test_attention_matches_fp32(L, n_q, n_kv, hd, shape):
     rows, ctx = {
         "decode": ([1] * 6, [1, 63, 64, 65, 300, 1000]),
         "verify": ([4, 5, 1, 10, 3], [5, 200, 640, 77, 1500]),
         "prefill": ([96, 33], [96, 33]),
         "ragged": ([2, 70, 1, 16], [2, 900, 129, 16]),
+        "batch": (BATCH_ROWS, BATCH_CTX),
     }[shape]
+    if shape == "batch" and n_q // n_kv * max(rows) > 64:
+        rows = [min(r, 64 // (n_q // n_kv)) for r in rows]
     run_case(L, n_q, n_kv, hd, rows, ctx, seed=n_q + hd)
+
+
+@pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (32, 8, 128)])
+def test_tcgen05_attention_matches_fp32(n_q, n_kv, hd):
+    """The opt-in tcgen05 attention (FASER_ATTN_TC=1, read once per process) in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_attention_gpu as t; "
+            "from paper_2604_20503_b200 import engine; "
+            f"t.run_case(engine.lib(), {n_q}, {n_kv}, {hd}, t.BATCH_ROWS, t.BATCH_CTX, seed=5)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "FASER_ATTN_TC": "1"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
