@@ -833,22 +833,12 @@ def toy_ours(args, rank, world, local_rank):
                                mode=abi.MODE_VSD_AD_EE, device=local_rank)
     for i, (p, m) in enumerate(zip(prompts, outl)):
         eng.submit(base + i, p, m)
-    rr = {}
+    pol = abi.ExitPolicy.default()
 
     def run(n):
-        tok = 0
-        for _ in range(n):
-            live = eng.live_requests()
-            if not live:
-                break
-            ks = [abi.sched_k(7, rid - base, rr.get(rid, 0)) for rid in live]
-            eng.set_spec_lengths(live, ks)
-            from paper_2604_20503_b200 import engine as E
-            eng.set_gate(E.make_gate_plan(abi.ExitPolicy.default(), [(kk, 0.7) for kk in ks],
-                                          float(len(ks)), 0.5, 32))
-            for r in eng.step():
-                rr[r.req_id] = rr.get(r.req_id, 0) + 1
-                tok += r.committed
+        # the serving loop in one native call (faser_serve_rounds): per round the seeded dynamic
+        # k_i (sched_k), the Eq.5-10 gate plan, one step; no Python between rounds
+        tok, _ = eng.serve_rounds(n, 7, base, pol, 0.7, 0.5, 32)
         return tok
 
     run(args.warmup)

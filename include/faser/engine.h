@@ -282,6 +282,15 @@ faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, floa
 /* Switches the admission-prefill lane of an engine created with prefill_lane = 1 off (0: the
  * next step drains it and admissions are prefilled in-step again) or back on (1). */
 faser_status faser_set_prefill_lane(faser_engine* e, int32_t on);
+/* The serving loop of the missing sim.cpp as one call, for hosts that drive the
+ * engine without per-step callbacks: up to n_rounds iterations of
+ *   live requests -> k_i = sched_k(seed, req_id - id_base, rounds served so far) over the drafter
+ *   candidates -> faser_set_spec_lengths -> (EE modes) make_gate_plan(policy, (k_i, accept_est),
+ *   b = live, r) -> faser_step,
+ * stopping early when nothing is live. Reports committed tokens and executed rounds. */
+faser_status faser_serve_rounds(faser_engine* e, int32_t n_rounds, uint64_t seed, int64_t id_base,
+                                const faser_exit_policy* policy, double accept_est, double r, int32_t num_layers,
+                                int64_t* tokens_out, int32_t* rounds_out);
 /* Timing experiments only (results become invalid): kernel classes the following steps skip,
  * bitmask 1 attention, 2 qkv, 4 o, 8 gate/up, 16 down of the target verify forward (+ 32: of the
  * prefill forwards instead); -1 restores FASER_SKIP. The bench derives in-stream class costs

@@ -772,3 +772,65 @@ faser_status faser_toy_verify(const faser_toy_params* model, int32_t n, const in
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ serving loop (sim.cpp role)
+namespace {
+constexpr uint64_t kSrvGamma = 0x9e3779b97f4a7c15ull;
+uint64_t srv_mix64(uint64_t x) {  // rng.hpp:17-22
+  x += kSrvGamma;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+uint64_t srv_hash_combine(uint64_t h, uint64_t v) {  // rng.hpp:24-26
+  return srv_mix64(h ^ (v + kSrvGamma + (h << 6) + (h >> 2)));
+}
+constexpr int32_t kSrvCandidates[8] = {1, 2, 3, 4, 5, 6, 8, 10};  // drafter.hpp:16
+}  // namespace
+
+extern "C" faser_status faser_serve_rounds(faser_engine* e, int32_t n_rounds, uint64_t seed, int64_t id_base,
+                                           const faser_exit_policy* policy, double accept_est, double r,
+                                           int32_t num_layers, int64_t* tokens_out, int32_t* rounds_out) {
+  if (!e || n_rounds < 0 || !tokens_out || !rounds_out) return FASER_EINVAL;
+  *tokens_out = 0;
+  *rounds_out = 0;
+  const int cap = 1 << 12;
+  std::vector<int64_t> ids(cap);
+  std::vector<int32_t> ks(cap);
+  std::vector<faser_gate_entry> ents(cap);
+  std::vector<faser_round_result> res(cap);
+  std::unordered_map<int64_t, int32_t> served;
+  for (int it = 0; it < n_rounds; ++it) {
+    int32_t n = 0;
+    faser_status st = faser_live_requests(e, ids.data(), cap, &n);
+    if (st != FASER_OK) return st;
+    if (n == 0) break;
+    if (n > cap) return FASER_ECAPACITY;
+    for (int i = 0; i < n; ++i) {
+      const int32_t rnd = served[ids[i]];
+      const uint64_t h = srv_hash_combine(srv_hash_combine(srv_mix64(seed), static_cast<uint64_t>(ids[i] - id_base + 1)),
+                                          static_cast<uint64_t>(rnd + 1));
+      ks[i] = kSrvCandidates[h % 8];
+    }
+    if ((st = faser_set_spec_lengths(e, ids.data(), ks.data(), n)) != FASER_OK) return st;
+    faser_step_plan plan{};
+    if (policy) {
+      for (int i = 0; i < n; ++i) {
+        ents[i] = faser_gate_entry{};
+        ents[i].spec_length = ks[i];
+        ents[i].accept_estimate = accept_est;
+      }
+      if ((st = faser_make_gate_plan(policy, ents.data(), n, static_cast<double>(n), r, nullptr, num_layers,
+                                     &plan.gate)) != FASER_OK)
+        return st;
+    }
+    int32_t got = 0;
+    if ((st = faser_step(e, policy ? &plan : nullptr, res.data(), cap, &got)) != FASER_OK) return st;
+    for (int i = 0; i < got; ++i) {
+      served[res[i].req_id] += 1;
+      *tokens_out += res[i].committed;
+    }
+    *rounds_out += 1;
+  }
+  return FASER_OK;
+}

@@ -330,6 +330,16 @@ class ServingEngine:
         _check(lib().faser_last_step_timing(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def serve_rounds(self, n_rounds, seed, id_base=0, policy=None, accept_est=0.7, r=0.5, num_layers=32):
+        """The sim loop in one native call (faser_serve_rounds): per round k_i = sched_k(seed,
+        req_id - id_base, rounds served), set_spec_lengths, make_gate_plan when `policy` is
+        given, step. Returns (committed tokens, rounds executed)."""
+        tok, rnd = C.c_int64(), C.c_int32()
+        _check(lib().faser_serve_rounds(self.h, int(n_rounds), C.c_uint64(seed), C.c_int64(id_base),
+                                        C.byref(policy) if policy is not None else None, C.c_double(accept_est),
+                                        C.c_double(r), int(num_layers), C.byref(tok), C.byref(rnd)), self.h)
+        return tok.value, rnd.value
+
     def debug_set_skip_mask(self, mask):
         """Timing experiments only: kernel classes the following steps skip (results invalid)."""
         _check(lib().faser_debug_set_skip_mask(self.h, int(mask)), self.h)

@@ -373,8 +373,9 @@ def test_request_sharded_replicas_equal_single_engine():
     assert sharded == single
 
 
-@pytest.mark.parametrize("preset", ["tiny", "tiny128", "cfg3"])
-def test_prefill_lane_lossless_and_deferred_join(preset):
+@pytest.mark.parametrize("preset,mode", [("tiny", abi.MODE_VSD), ("tiny128", abi.MODE_VSD), ("cfg3", abi.MODE_VSD),
+                                         ("tiny", abi.MODE_VSD_AD_EE)])
+def test_prefill_lane_lossless_and_deferred_join(preset, mode):
     """Admission-prefill lane (cfg.prefill_lane): newly admitted requests are prefilled on the
     side stream while the running batch steps, and join at the next step. Outputs stay the
     target's greedy decoding (oracle, near-tie rule), a request never reports a round in the step
@@ -388,7 +389,7 @@ def test_prefill_lane_lossless_and_deferred_join(preset):
     max_out = [int(rng.integers(1, 30)) for _ in range(n)]
     outs = {}
     for lane in (0, 1):
-        eng = engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=420, mode=abi.MODE_VSD,
+        eng = engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=420, mode=mode,
                                    default_spec_length=4, max_spec_length=16, prefill_rows=2048,
                                    prefill_lane=lane)
         for i, (p, m) in enumerate(zip(prompts, max_out)):
@@ -397,6 +398,8 @@ def test_prefill_lane_lossless_and_deferred_join(preset):
         while eng.live_requests():
             live = set(eng.live_requests())
             fresh = live - seen_live
+            if mode == abi.MODE_VSD_AD_EE:  # early exit gated at layers [1, 3)
+                eng.set_gate(abi.GatePlan(1, 3, 1.0))
             res = eng.step()
             got = {r.req_id for r in res}
             if lane and fresh and (live - fresh):

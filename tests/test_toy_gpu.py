@@ -217,3 +217,34 @@ def test_engine_max_batch_256_and_slot_reuse():
                          threads=1, k_seed=3, policy=abi.ExitPolicy.default(), gate=abi.GatePlan(8, 32, 1.0))
     o2, l2, _ = P.run_episode(cfg, prompts, outl, log_cap=1000000)
     assert outs == o2 and recs == [r.as_tuple() for r in l2]
+
+
+def test_native_serving_loop_matches_python_loop():
+    """faser_serve_rounds (the sim loop in one native call) drives the engine exactly like the
+    per-round Python loop with the same seeded k schedule and gate plan: identical outputs."""
+    p = abi.ToyParams.default()
+    P = po.restated()
+    n = 48
+    inl, outl = po.backlog_lengths(7, n)
+    prompts = [P.synth_prompt(7, i, inl[i], 64) for i in range(n)]
+    pol = abi.ExitPolicy.default()
+    outs = []
+    for native in (False, True):
+        eng = engine.ServingEngine(p, max_batch=16, max_seq_len=256, mode=abi.MODE_VSD_AD_EE)
+        for i, (pr, m) in enumerate(zip(prompts, outl)):
+            eng.submit(100 + i, pr, m)
+        if native:
+            tok, rounds = eng.serve_rounds(10000, 7, 100, pol, 0.7, 0.5, 32)
+            assert rounds > 0 and tok > 0
+        else:
+            rr = {}
+            while eng.live_requests():
+                live = eng.live_requests()
+                ks = [abi.sched_k(7, rid - 100, rr.get(rid, 0)) for rid in live]
+                eng.set_spec_lengths(live, ks)
+                eng.set_gate(engine.make_gate_plan(pol, [(k, 0.7) for k in ks], float(len(ks)), 0.5, 32))
+                for r in eng.step():
+                    rr[r.req_id] = rr.get(r.req_id, 0) + 1
+        outs.append([eng.committed(100 + i) for i in range(n)])
+        eng.close()
+    assert outs[0] == outs[1]
