@@ -65,6 +65,8 @@ struct Cfg {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint32_t map_cta(uint32_t saddr, int rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
@@ -281,22 +283,39 @@ __global__ void __launch_bounds__(128, 1)
   #pragma unroll
       for (int z = 0; z < 16; ++z) rb[z] = z < splits ? map_cta(base, z) : 0u;
       const int c4 = threadIdx.x & 31, tq = threadIdx.x >> 5;  // 4 rows (float4) x 4 tokens per pass
-      for (int t = ts + tq; t < te; t += 4) {
-        const uint32_t off = (t * kBM + c4 * 4) * 4;
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      // two passes per round: every DSMEM load of the round is issued before any sum or store
+      // (one remote latency per round instead of one per pass); sums stay in rank order
+      for (int t = ts + tq; t < te; t += 8) {
+        const int t2 = t + 4;
+        const bool two = t2 < te;
+        float4 v[2][16];
   #pragma unroll
         for (int z = 0; z < 16; ++z) {
           if (z < splits) {
-            const float4 v = ld_dsmem4(rb[z] + off);
-            a.x += v.x;
-            a.y += v.y;
-            a.z += v.z;
-            a.w += v.w;
+            v[0][z] = ld_dsmem4(rb[z] + (t * kBM + c4 * 4) * 4);
+            if (two) v[1][z] = ld_dsmem4(rb[z] + (t2 * kBM + c4 * 4) * 4);
           }
         }
-        // only this CTA reads its own slice rows, so the in-place write is race-free
-        *reinterpret_cast<float4*>(S + t * kBM + c4 * 4) = a;
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  #pragma unroll
+          for (int z = 0; z < 16; ++z) {
+            if (z < splits) {
+              a.x += v[h][z].x;
+              a.y += v[h][z].y;
+              a.z += v[h][z].z;
+              a.w += v[h][z].w;
+            }
+          }
+          // only this CTA reads its own slice rows, so the in-place write is race-free
+          *reinterpret_cast<float4*>(S + (h ? t2 : t) * kBM + c4 * 4) = a;
+        }
       }
+      // done reading the peers' partials: let them proceed (their exit / next tile waits only
+      // for this arrive), while this CTA runs its epilogue
+      cluster_arrive();
       __syncthreads();
     }
     __syncthreads();  // (the per-token prologue was written by warps 2-3 during the mainloop)
@@ -415,7 +434,7 @@ __global__ void __launch_bounds__(128, 1)
         *reinterpret_cast<__nv_bfloat162*>(ea.h + static_cast<size_t>(n0 + t) * ea.ffn + j0 + w) = __floats2bfloat162_rn(h0, h1);
       }
     }
-  if (splits > 1) cluster_sync();  // peers may still be reading this CTA's partial
+  if (splits > 1) cluster_wait();  // peers may still be reading this CTA's partial
   __syncthreads();                 // the staging tile is reused by the next weight tile
   }
   if (threadIdx.x == 0) stamp(ea, 5);
