@@ -241,7 +241,8 @@ def make_engine(desc, args, local_rank, batch=None, **tp):
     return engine.ServingEngine(desc=desc, max_batch=batch or args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
                                 mode=mode, default_spec_length=args.k, max_spec_length=16,
                                 prefill_rows=8192, device=local_rank,
-                                prefill_lane=0 if (tp or args.no_prefill_lane) else 1, **tp)
+                                prefill_lane=0 if (tp or args.no_prefill_lane) else 1,
+                                exempt_rule=2 if getattr(args, "recovery", False) else 1, **tp)
 
 
 def tp_bootstrap(dist, rank, make_uid):
@@ -908,6 +909,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded batch sweep")
+    ap.add_argument("--recovery", action="store_true",
+                    help="EE modes: recovery on prune (exempt_rule 2, beyond the reference's semantics)")
     ap.add_argument("--no-prefill-lane", action="store_true",
                     help="prefill admissions in the step itself instead of on the side lane")
     ap.add_argument("--trace", type=float, default=0.0,

@@ -192,7 +192,11 @@ typedef struct faser_engine_cfg {
   int32_t max_seq_len;     /* prompt + max_out capacity per request */
   int32_t mode;            /* FASER_MODE_*: EE modes use verify_with_early_exit */
   int32_t default_spec_length; /* fixed_spec_len, config.hpp:51 (4) */
-  int32_t exempt_rule;     /* 1: exempt = committed_before + pruned_at.first for one round */
+  int32_t exempt_rule;     /* 1: exempt = committed_before + pruned_at.first for one round;
+                              2 (LLAMA, EE modes except FULL; beyond the reference's semantics):
+                              recovery on prune - the first pruned row keeps running to full depth
+                              and its final argmax is committed as the recovery token after a clean
+                              prune (still greedy-lossless), no exemption; false_prune is exact */
   faser_exit_policy exit_policy;
   int32_t max_pending;     /* capacity of the submitted-not-admitted queue */
   int32_t pending_tokens;  /* device staging arena for submitted prompts (tokens) */

@@ -255,6 +255,8 @@ faser_status faser_engine_create(const faser_model_desc* model, const faser_engi
     if (cfg->max_seq_len < 2) throw Fail{FASER_EINVAL, "max_seq_len must be >= 2"};
     if (cfg->mode < FASER_MODE_VSD || cfg->mode > FASER_MODE_FULL)
       throw Fail{FASER_EINVAL, "unknown mode"};
+    if (cfg->exempt_rule != 0 && cfg->exempt_rule != 1)
+      throw Fail{FASER_EINVAL, "the toy engine follows the reference's rules: exempt_rule 0 or 1"};
     const faser_exit_policy& p = cfg->exit_policy;
     if (p.k_init < 1 || p.k_final < 1 || p.k_final > p.k_init)
       throw Fail{FASER_EINVAL, "exit policy thresholds must satisfy k_init >= k_final >= 1"};

@@ -457,6 +457,9 @@ class LlamaEngine {
     if (cfg.max_batch < 1 || cfg.max_batch > 1024) throw LFail{FASER_EINVAL, "max_batch out of range [1, 1024]"};
     if (cfg.max_seq_len < 2) throw LFail{FASER_EINVAL, "max_seq_len must be >= 2"};
     if (cfg.mode < FASER_MODE_VSD || cfg.mode > FASER_MODE_FULL) throw LFail{FASER_EINVAL, "unknown mode"};
+    if (cfg.exempt_rule < 0 || cfg.exempt_rule > 2) throw LFail{FASER_EINVAL, "exempt_rule must be 0, 1 or 2"};
+    if (cfg.exempt_rule == 2 && cfg.mode == FASER_MODE_FULL)
+      throw LFail{FASER_EINVAL, "recovery on prune (exempt_rule 2) is a serial-verify mode; not with FULL"};
     const faser_exit_policy& p = cfg.exit_policy;
     if (p.k_init < 1 || p.k_final < 1 || p.k_final > p.k_init)
       throw LFail{FASER_EINVAL, "exit policy thresholds must satisfy k_init >= k_final >= 1"};
@@ -836,7 +839,8 @@ class LlamaEngine {
         if (f.capture) capture_stage(layer, m, w, f);
         LCK(lm_exit_rank(sl, cur_q, rows, w.rank_cnt.as<int>(), s.vocab / 128, T, f.k_table[layer], T, fs));
         launches += 3 + (T + 127) / 128;
-        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), fs, f.q0));
+        LCK(lm_frontier_compact(sl, cur_q, rows, f.n_req, layer, w.src_of.as<int>(), fs, f.q0,
+                                cfg.exempt_rule == 2 ? 1 : 0, s.layers));
         LCK(lm_gather_rows(rows, w.src_of.as<int>(), s.d, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(),
                            w.ss.as<float>(), w.xs.as<float>(), w.xbs.as<__nv_bfloat16>(), w.sss.as<float>(),
                            fs));

@@ -298,7 +298,10 @@ __global__ void exit_rank_kernel(LmSlots sl, LmReqState rq, RowsDev rows, const 
 // One thread per request (n <= 1024), single CTA.
 // q0: first drafted position of these rows (0, or the chunk start in the overlapped mode, where
 // row (i, q0 + jl) sits at local index jl of request i).
-__global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, int* src_of, int q0) {
+// recover = 1 (exempt_rule 2, beyond the reference): the first pruned row keeps running to full
+// depth so its final argmax can be committed as the recovery token; rows after it are dropped.
+__global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, int* src_of, int q0, int recover,
+                                int layers) {
   __shared__ int scan[1024];
   const int i = threadIdx.x;
   int keep = 0, old_first = 0, pos0 = 0;
@@ -313,7 +316,10 @@ __global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, i
       const uint32_t f = rq.failmask[i] & live;
       if (f) {
         const int j = __ffs(f) - 1;
-        for (int jj = j; jj < act; ++jj) rq.prune_layer[i * kMS + jj] = layer;
+        // (recovery mode: the previous recovery row, index act, stops here too)
+        const int hi = (recover && rq.pr[2 * i] >= 0) ? act + 1 : act;
+        for (int jj = j; jj < hi; ++jj) rq.prune_layer[i * kMS + jj] = layer;
+        if (recover) rq.prune_layer[i * kMS + j] = layers;  // runs to full depth
         act = j;
         rq.active[i] = act;
         rq.pr[2 * i] = j;
@@ -323,7 +329,7 @@ __global__ void frontier_kernel(LmReqState rq, RowsDev rows, int n, int layer, i
       }
     }
     rq.failmask[i] = 0u;
-    keep = act - q0;
+    keep = act - q0 + ((recover && rq.pr[2 * i] >= 0) ? 1 : 0);  // (+ the recovery row)
     if (q0 == 0 && keep < 1) keep = 1;  // row 0 survives (force-verify, sdcore.cpp:150-166)
     keep = keep < 0 ? 0 : (keep < old_n ? keep : old_n);
   }
@@ -517,6 +523,8 @@ __global__ void accept_commit_kernel(LmSlots sl, LmReqState rq, RowsDev rows, St
       break;
     }
   }
+  const bool recover = ctl.exempt_rule == 2;
+  if (recover && pruned && !mismatch && active > 0 && pr_j < count) rec = truth[pr_j];  // the kept row's argmax
   if (ee && active == 0) {  // progress guarantee: force-verify token 0
     if (d[0] == truth[0]) {
       acc = 1;
@@ -551,6 +559,9 @@ __global__ void accept_commit_kernel(LmSlots sl, LmReqState rq, RowsDev rows, St
   // false_prune needs the full-depth argmax of the pruned row, which a pruned verify never
   // computes (that is the saving); reported as -1 = "not evaluated" on this path.
   o.false_prune = (pruned && !mismatch && acc == pr_j && pr_j < count) ? -1 : 0;
+  // recovery mode evaluates the pruned row at full depth: false_prune is exact there
+  if (recover && pruned && !mismatch && acc == pr_j && pr_j < count && active > 0)
+    o.false_prune = d[pr_j] == truth[pr_j] ? 1 : 0;
   const int npl = ee ? rq.n_pl[r] : 0;
   o.n_prune_layers = npl;
   for (int i = 0; i < npl; ++i) o.prune_layers[i] = rq.pl[r * kMS + i];
@@ -582,7 +593,8 @@ __global__ void accept_commit_kernel(LmSlots sl, LmReqState rq, RowsDev rows, St
   sl.ncomm[slot] = nc;
   sl.done[slot] = done;
   int ex = sl.exempt[slot];
-  if (ctl.exempt_rule) ex = pruned ? ncomm0 + pr_j : -1;
+  if (ctl.exempt_rule == 1) ex = pruned ? ncomm0 + pr_j : -1;
+  if (recover) ex = -1;  // the pruned position is resolved by the recovery token
   sl.exempt[slot] = ex;
   rr->done = done;
   rr->exempt_position = ex;
@@ -699,11 +711,11 @@ cudaError_t lm_exit_rank(LmSlots sl, LmReqState rq, RowsDev rows, const int* cnt
   return cudaGetLastError();
 }
 cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
-                                int* src_of, cudaStream_t s, int q0) {
+                                int* src_of, cudaStream_t s, int q0, int recover, int layers) {
   (void)sl;
   if (n <= 0) return cudaSuccess;
   if (n > 1024) return cudaErrorInvalidValue;
-  frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, layer, src_of, q0);
+  frontier_kernel<<<1, cdiv(n, 32) * 32, 0, s>>>(rq, rows, n, layer, src_of, q0, recover, layers);
   return cudaGetLastError();
 }
 cudaError_t lm_chunk_frontier(LmReqState rq, RowsDev rows, int n, int q, int q0, int first, int layers, int eos,

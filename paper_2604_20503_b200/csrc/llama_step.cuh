@@ -63,7 +63,9 @@ struct StepCtl {
   int layers;      // target layers (L)
   int eos;
   int early_exit;  // 1: verify_with_early_exit semantics
-  int exempt_rule; // 1: exempt = committed_before + pruned_at.first for the next round
+  int exempt_rule; // 1: exempt = committed_before + pruned_at.first for the next round;
+                   // 2: recovery on prune (beyond the reference: the first pruned row runs to
+                   //    full depth and its argmax is committed, no exemption)
 };
 
 // draft step t: rows = sorted requests [0, n_t); row r = request r, 1 row each at position
@@ -106,8 +108,9 @@ cudaError_t lm_exit_rank(LmSlots sl, LmReqState rq, RowsDev rows, const int* cnt
 // src_of[new_row] = old row; the residual (x fp32, xb bf16, ss per-chunk sums of squares) is
 // gathered through scratch buffers of the same shapes.
 // q0 = first drafted position of the rows (0, or the chunk start in the overlapped mode).
+// recover = 1 (exempt_rule 2): the first pruned row stays to full depth (recovery token).
 cudaError_t lm_frontier_compact(LmSlots sl, LmReqState rq, RowsDev rows, int n, int layer,
-                                int* src_of, cudaStream_t s, int q0 = 0);
+                                int* src_of, cudaStream_t s, int q0 = 0, int recover = 0, int layers = 0);
 // Overlapped (FULL) verify, before chunk q (drafted positions [q0, q0 + rows)): a request stays on
 // the frontier iff no earlier row was pruned (active > q0), rejected (drafted != truth) or EOS;
 // otherwise its rows of the chunk are cancelled (reset, overlap.cpp:44-91). The chunk's rows are

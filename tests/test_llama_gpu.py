@@ -419,3 +419,48 @@ def test_prefill_lane_lossless_and_deferred_join(preset, mode):
                     assert gap_rel(z) <= LOGIT_TOL, (i, j)
     finally:
         tgt.close()
+
+
+@pytest.mark.parametrize("preset", ["tiny", "tiny128"])
+def test_recovery_on_prune_lossless(preset):
+    """exempt_rule 2 (beyond the reference): the first pruned row runs to full depth and its
+    argmax is committed after a clean prune. Outputs stay the target's greedy decoding (oracle,
+    near-tie rule); every clean prune commits accepted + 1 tokens; no exemption is carried."""
+    desc = llama.PRESETS[preset](target_bigram=1.5 if preset == "tiny" else None)
+    V = desc.target.vocab
+    pol = abi.ExitPolicy(1, 4, 1)
+    eng = engine.ServingEngine(desc=desc, max_batch=6, max_seq_len=320, mode=abi.MODE_VSD_AD_EE,
+                               default_spec_length=5, max_spec_length=16, prefill_rows=2048,
+                               exit_policy=pol, exempt_rule=2)
+    rng = np.random.default_rng(23)
+    prompts = rand_prompts(V, 10, rng)
+    max_out = [int(rng.integers(4, 40)) for _ in range(10)]
+    for i, (p, m) in enumerate(zip(prompts, max_out)):
+        eng.submit(i, p, m)
+    n_pruned = n_recovered = 0
+    L = desc.target.layers
+    while eng.live_requests():
+        eng.set_gate(abi.GatePlan(1, min(4, L), 1.0))
+        for r in eng.step():
+            o = r.outcome
+            assert r.exempt_position == -1
+            if o.has_pruned:
+                n_pruned += 1
+                if o.accepted_count == o.pruned_index and o.pruned_index > 0:
+                    assert o.has_recovery, "a clean prune must commit the kept row's argmax"
+                    n_recovered += 1
+                    assert o.false_prune in (0, 1)
+            assert r.committed <= o.accepted_count + (1 if o.has_recovery else 0)
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
+    try:
+        for i, (p, m) in enumerate(zip(prompts, max_out)):
+            got, ref = eng.committed(i), tgt.greedy(p, m, V - 1)
+            if got != ref:
+                j = next(q for q in range(min(len(got), len(ref))) if got[q] != ref[q])
+                z = tgt.logits(p + ref[:j + 1], len(p) + j - 1)[0][0]
+                assert gap_rel(z) <= LOGIT_TOL, (i, j)
+    finally:
+        tgt.close()
+    if preset == "tiny":
+        assert n_pruned > 0 and n_recovered > 0  # the case exercises pruning and recovery
+    eng.close()
