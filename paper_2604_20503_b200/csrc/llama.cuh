@@ -120,7 +120,9 @@ cudaError_t lm_argmax_reduce(int n_tiles, RowsDev rows, int rows_cap, const floa
 // GQA-packed verify / decode rows on tcgen05 (llama_attn_tc.cu): one CTA per (request, kv head),
 // S and O in TMEM; used by lm_attention when G >= 4, <= 64 packed rows, no KV split.
 bool attn_tc_applies(const LlamaShape& m, int max_rows_per_req, int max_ctx, const KvDev& kv);
-cudaError_t lm_attention_tc(const LlamaShape& m, RowsDev rows, int n_req, KvDev kv, int layer,
+// prefill / long-row blocks on the same kernel in 128-row tiles (ROWS work of lm_attention)
+bool attn_tc_rows_applies(const LlamaShape& m, int max_ctx, const KvDev& kv);
+cudaError_t lm_attention_tc(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req, KvDev kv, int layer,
                             const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, cudaStream_t s);
 // Causal attention of every row over its request's paged KV (GQA packed, mma.sync bf16).
 cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req,

@@ -558,7 +558,9 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   }
   // tensor-core path (llama_attn_tc.cu) for GQA-packed rows when no KV split is wanted
   if (n_split == 1 && !rows_mode && attn_tc_applies(m, max_rows_per_req, max_ctx, kv))
-    return lm_attention_tc(m, rows, n_req, kv, layer, qbuf, obuf, s);
+    return lm_attention_tc(m, rows, n_req, max_rows_per_req, kv, layer, qbuf, obuf, s);
+  if (rows_mode && attn_tc_rows_applies(m, max_ctx, kv))
+    return lm_attention_tc(m, rows, n_req, max_rows_per_req, kv, layer, qbuf, obuf, s);
   const size_t per_split = static_cast<size_t>(rows_cap) * m.n_q * (m.hd * 4 + 8);
   while (n_split > 1 && per_split * n_split > body_bytes) --n_split;
   float* part_o = body;

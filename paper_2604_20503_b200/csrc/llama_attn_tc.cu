@@ -1,19 +1,25 @@
-// llama_attn_tc.cu — K3 on the 5th-generation tensor cores for GQA-packed verify / decode rows.
+// llama_attn_tc.cu — K3 on the 5th-generation tensor cores.
 //
-// One CTA per (request, kv head): the G query heads sharing the KV head are packed with the
-// request's rows into the UMMA M dimension (m = row * G + g, M <= 64, padded to a 128-row tile;
-// the padding rows are never read back). Per step of 128 keys (two 64-token pages):
+// One CTA per (request, kv head, 128-row tile): the G query heads sharing the KV head are packed
+// with the request's rows into the UMMA M dimension (m = row * G + g, tiles of 128 packed rows;
+// a request with <= 64 packed rows spreads them over all four softmax warps, padding rows are
+// never read back). Per step of 128 keys (two 64-token pages):
 //   S  = Q K^T      tcgen05.mma M128 x N128, K = head_dim; A = Q (smem, K-major SW128),
-//                   B = the two K pages as TMA wrote them ([key][hd], K-major SW128); S in TMEM
+//                   B = the two K pages as TMA wrote them ([key][hd], K-major SW128); S in TMEM,
+//                   double-buffered (S of step u+1 is issued before P V of step u)
 //   softmax         4 warps, thread t = packed row t: its 128 scores come out of TMEM with
-//                   tcgen05.ld (no shuffles), causal mask, running max / sum, the O rescale on
-//                   TMEM (tcgen05.ld / st), P = exp2(S - m) as bf16 into smem (K-major SW128)
+//                   tcgen05.ld (no shuffles); unmasked steps skip the causal compares; running
+//                   max / sum on the raw scores (one FFMA + one MUFU.EX2 per key); the O rescale
+//                   on TMEM is lazy (only when the max grew by 2^8); P = exp2(S - m) as bf16 into
+//                   smem (K-major SW128, double-buffered for hd 64)
 //   O += P V        tcgen05.mma M128 x N(head_dim), K = 128 keys; A = P, B = the two V pages
 //                   read MN-major ([key][hd] rows = K, head_dim contiguous = N), O in TMEM
 // Warp roles: warps 0-3 softmax / epilogue, warp 4 TMA producer (pages into a ring of steps),
 // warp 5 MMA issuer. The epilogue divides O by the row sums and writes bf16 rows.
-// Dispatch (llama_attn.cu, opt-in FASER_ATTN_TC=1): GROUP rows with G >= 4, M <= 64, no KV split,
-// TMA view of the pool. Measured slower than the mma.sync kernel (see attn_tc_applies).
+// Dispatch (llama_attn.cu): ROW blocks (> 64 packed rows per request: prefill, long verify) by
+// default — about 2x the mma.sync kernel there; GQA-packed GROUP rows opt-in (FASER_ATTN_TC=1),
+// where the one-CTA-per-SM footprint (512 TMEM columns, 145-193 KB smem) loses to mma.sync's
+// occupancy at large batch (profiles/r02_attn_tc_ab.txt).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -42,8 +48,10 @@ struct TcCfg {
   static constexpr int kStages = HD == 64 ? 3 : 2;
   static constexpr int kQ = kAtoms * 128 * 128;           // Q tile [atom][128 rows][128 B]
   static constexpr int kP = 2 * 128 * 128;                // P tile [2 atoms of 64 keys][128 rows][128 B]
-  static constexpr int kSmem = 1024 + kQ + kStages * kStep + kP;
-  static constexpr uint32_t kTmemCols = 256;              // S [0, 128), O [128, 128 + HD)
+  static constexpr int kPBufs = HD == 64 ? 2 : 1;         // P double-buffered where smem allows
+  static constexpr int kSmem = 1024 + kQ + kStages * kStep + kPBufs * kP;
+  static constexpr uint32_t kTmemCols = 512;              // S0 [0,128), S1 [128,256), O [256, 256 + HD)
+  static constexpr float kRescaleLog2 = 8.f;              // lazy O rescale once the max grows by 2^8
 };
 
 __device__ __forceinline__ uint64_t desc_sw128_k(uint32_t saddr) { return sm100::desc_sw128(saddr); }
@@ -86,6 +94,11 @@ __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) 
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {  // one MUFU.EX2
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -93,7 +106,8 @@ template <int HD>
 __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap kvmap, RowsDev rows,
                                                                  KvDev kv, int layer, int n_q, int n_kv,
                                                                  const __nv_bfloat16* __restrict__ qbuf,
-                                                                 __nv_bfloat16* __restrict__ obuf, float scale_log2) {
+                                                                 __nv_bfloat16* __restrict__ obuf, float scale_log2,
+                                                                 int spread) {
   using C = TcCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -101,7 +115,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   uint8_t* sKV = sQ + C::kQ;
   uint8_t* sP = sKV + C::kStages * C::kStep;
   __shared__ __align__(8) uint64_t full[C::kStages], empty[C::kStages];
-  __shared__ __align__(8) uint64_t s_full, p_full, o_done;
+  __shared__ __align__(8) uint64_t s_full[2], p_full[2], pv_done[2];  // by step parity
   __shared__ uint32_t tmem_slot;
   __shared__ int s_page[kMaxPagesTc];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -110,10 +124,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   const int nr = rows.req_n[req];
   const int gs = 31 - __clz(n_q / n_kv);
   const int G = 1 << gs, gm = G - 1;
-  const int M = nr << gs;
-  if (M == 0) return;
+  const int Mreq = nr << gs;
+  const int m0 = blockIdx.z * 128;  // this CTA's 128 packed rows (prefill: several tiles per unit)
+  if (m0 >= Mreq) return;
+  const int M = min(128, Mreq - m0);  // live rows of the tile (tile-relative)
   const int first = rows.req_first[req], pos0 = rows.req_pos0[req], slot = rows.req_slot[req];
-  const int key_end = pos0 + nr;  // keys [0, key_end)
+  const int key_end = pos0 + ((m0 + M - 1) >> gs) + 1;  // keys [0, key_end) for the tile's last row
   const int tiles = (key_end + 63) / 64;
   const int nsteps = (tiles + 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -125,20 +141,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       sm100::mbar_init(&full[s], 1);
       sm100::mbar_init(&empty[s], 1);
     }
-    sm100::mbar_init(&s_full, 1);
-    sm100::mbar_init(&p_full, 128);
-    sm100::mbar_init(&o_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&s_full[b], 1);
+      sm100::mbar_init(&p_full[b], 128);
+      sm100::mbar_init(&pv_done[b], 1);
+    }
     sm100::fence_mbar_init();
   }
   if (warp == 0) sm100::tmem_alloc<C::kTmemCols>(&tmem_slot);
-  // Q rows -> smem (K-major SW128): packed row m = r * G + g goes to tile row
-  // t = (m % 4) * 32 + m / 4, so the <= 64 live rows spread over the four TMEM lane quarters
-  // (one per softmax warp) instead of crowding the first
+  // Q rows -> smem (K-major SW128): tile row t holds packed row m0 + m (m = r * G + g). With
+  // `spread` (<= 64 live rows) t = (m % 4) * 32 + m / 4, so the rows spread over the four TMEM
+  // lane quarters (one per softmax warp) instead of crowding the first
   for (int e = threadIdx.x; e < M * (HD / 8); e += kTcThreads) {
     const int m = e / (HD / 8), c = e % (HD / 8);
-    const int t = ((m & 3) << 5) | (m >> 2);
+    const int t = spread ? (((m & 3) << 5) | (m >> 2)) : m;
+    const int mg = m0 + m;
     const uint4 v = *reinterpret_cast<const uint4*>(
-        qbuf + (static_cast<int64_t>(first + (m >> gs)) * n_q + kvh * G + (m & gm)) * HD + c * 8);
+        qbuf + (static_cast<int64_t>(first + (mg >> gs)) * n_q + kvh * G + (mg & gm)) * HD + c * 8);
     *reinterpret_cast<uint4*>(sQ + (c >> 3) * (128 * 128) + t * 128 + (((c & 7) ^ (t & 7)) << 4)) = v;
   }
   fence_proxy_async();  // generic smem writes (Q) visible to the tensor core (async proxy)
@@ -146,7 +165,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + 128;
+  const uint32_t tO = tmem + 256;  // S(u) at tmem + (u % 2) * 128
 
   if (warp == 4) {
     // ---------------------------------------------------------------- TMA producer
@@ -176,84 +195,83 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(128, kKeysPerStep);
       constexpr uint32_t idesc_o = sm100::idesc_bf16_f32(128, HD) | (1u << 16);  // B (V) MN-major
       const uint32_t q0 = sm100::smem_u32(sQ), p0 = sm100::smem_u32(sP);
-      for (int u = 0; u < nsteps; ++u) {
+      // S(u) is issued before PV(u-1), so the tensor core computes the next scores while the
+      // softmax warps work on the current ones (S double-buffered in TMEM, P in smem)
+      auto issue_s = [&](int u) {
         const int s = u % C::kStages;
-        sm100::mbar_wait(&full[s], (u / C::kStages) & 1);  // (softmax u-1 finished with S: p_full u-1)
+        sm100::mbar_wait(&full[s], (u / C::kStages) & 1);
         sm100::tc_fence_after();
         const uint32_t k0 = sm100::smem_u32(sKV + s * C::kStep);
-        // S = Q K^T over head_dim (16 per instruction)
 #pragma unroll
-        for (int j = 0; j < HD / 16; ++j) {
+        for (int j = 0; j < HD / 16; ++j) {  // S = Q K^T over head_dim, 16 per instruction
           const uint64_t da = desc_sw128_k(q0 + (j >> 2) * (128 * 128)) + 2 * (j & 3);
           const uint64_t db = desc_sw128_k(k0 + (j >> 2) * C::kHalf) + 2 * (j & 3);
-          sm100::mma_bf16(tS, da, db, idesc_s, j > 0 ? 1u : 0u);
+          sm100::mma_bf16(tmem + (u & 1) * 128, da, db, idesc_s, j > 0 ? 1u : 0u);
         }
-        sm100::mma_commit(&s_full);
-        // O += P V over the step's 128 keys, once softmax u wrote P (and rescaled O)
-        sm100::mbar_wait(&p_full, u & 1);
+        sm100::mma_commit(&s_full[u & 1]);
+      };
+      auto issue_pv = [&](int u) {  // O += P(u) V(u), once softmax u wrote P (and rescaled O)
+        sm100::mbar_wait(&p_full[u & 1], (u >> 1) & 1);
         sm100::tc_fence_after();
-        const uint32_t v0 = k0 + C::kAtoms * C::kHalf;
+        const int s = u % C::kStages;
+        const uint32_t v0 = sm100::smem_u32(sKV + s * C::kStep) + C::kAtoms * C::kHalf;
+        const uint32_t pb = p0 + (u % C::kPBufs) * C::kP;
 #pragma unroll
         for (int j = 0; j < kKeysPerStep / 16; ++j) {
-          const uint64_t da = desc_sw128_k(p0 + (j >> 2) * (128 * 128)) + 2 * (j & 3);
+          const uint64_t da = desc_sw128_k(pb + (j >> 2) * (128 * 128)) + 2 * (j & 3);
           const uint64_t db = desc_sw128_mn(v0 + j * 16 * 128, C::kHalf);  // 16 keys = 2 groups of 8 rows
           sm100::mma_bf16(tO, da, db, idesc_o, (u > 0 || j > 0) ? 1u : 0u);
         }
         sm100::mma_commit(&empty[s]);
-        sm100::mma_commit(&o_done);
+        sm100::mma_commit(&pv_done[u & 1]);
+      };
+      issue_s(0);
+      for (int u = 1; u < nsteps; ++u) {
+        issue_s(u);
+        issue_pv(u - 1);
       }
+      issue_pv(nsteps - 1);
     }
   } else {
     // ---------------------------------------------------------------- softmax + epilogue
-    const int t = threadIdx.x;                  // tile row = TMEM lane
-    const int m = ((t & 31) << 2) | (t >> 5);   // its packed row
-    const int lim = m < M ? pos0 + (m >> gs) : -1;  // last key this row sees
+    const int t = threadIdx.x;                                // tile row = TMEM lane
+    const int m = spread ? (((t & 31) << 2) | (t >> 5)) : t;  // its tile-relative packed row
+    const int mg = m0 + m;
+    const int lim = m < M ? pos0 + (mg >> gs) : -1;           // last key this row sees
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    float mrun = kNegBigT, lrun = 0.f;
+    // warp-uniform: the smallest causal limit among the warp's live rows (steps entirely below it
+    // need no masking; padded rows compute garbage that only their own, never-written rows see)
+    const int wlim = __reduce_min_sync(0xffffffffu, m < M ? lim : 0x7fffffff);
+    float mused = kNegBigT, lrun = 0.f;  // reference max of P and O (lazily raised), row sum
     for (int u = 0; u < nsteps; ++u) {
-      sm100::mbar_wait(&s_full, u & 1);
+      sm100::mbar_wait(&s_full[u & 1], (u >> 1) & 1);
       sm100::tc_fence_after();
       const int kb = u * kKeysPerStep;
       uint32_t sr[kKeysPerStep];
 #pragma unroll
       for (int c = 0; c < kKeysPerStep / 32; ++c)
-        tmem_ld32_nw(tS + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        tmem_ld32_nw(tmem + (u & 1) * 128 + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_wait_ld();
-      float mx = mrun;
+      const bool full_step = kb + kKeysPerStep - 1 <= wlim;  // no key of the step is masked
+      float mx4[4] = {kNegBigT, kNegBigT, kNegBigT, kNegBigT};  // independent chains, raw scores
+      if (full_step) {
 #pragma unroll
-      for (int i = 0; i < kKeysPerStep; ++i)
-        if (kb + i <= lim) mx = fmaxf(mx, __uint_as_float(sr[i]) * scale_log2);
-      const float alpha = exp2f(mrun - mx);
-      // P(u) overwrites P(u-1): PV u-1 must have read it (and O must be final before the rescale)
-      if (u > 0) {
-        sm100::mbar_wait(&o_done, (u - 1) & 1);
+        for (int i = 0; i < kKeysPerStep; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[i]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < kKeysPerStep; ++i)
+          if (kb + i <= lim) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[i]));
+      }
+      const float mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      const float mx = mraw > kNegBigT ? mraw * scale_log2 : kNegBigT;  // (scale > 0)
+      if (u == 0) {
+        mused = mx;
+      } else if (__any_sync(0xffffffffu, mx > mused + C::kRescaleLog2)) {
+        // the warp raises its reference max: O must be current (PV u-1 landed) to rescale it
+        sm100::mbar_wait(&pv_done[(u - 1) & 1], ((u - 1) >> 1) & 1);
         sm100::tc_fence_after();
-      }
-      // P = exp2(S - m) as bf16 into smem (K-major SW128: keys 0..63 atom 0, 64..127 atom 1)
-      float sum = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < kKeysPerStep / 8; ++ch) {
-        float p8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int key = kb + ch * 8 + i;
-          p8[i] = key <= lim ? exp2f(__uint_as_float(sr[ch * 8 + i]) * scale_log2 - mx) : 0.f;
-          sum += p8[i];
-        }
-        uint4 pk;
-        __nv_bfloat162 b0 = __floats2bfloat162_rn(p8[0], p8[1]), b1 = __floats2bfloat162_rn(p8[2], p8[3]);
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(p8[4], p8[5]), b3 = __floats2bfloat162_rn(p8[6], p8[7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&b0);
-        pk.y = *reinterpret_cast<uint32_t*>(&b1);
-        pk.z = *reinterpret_cast<uint32_t*>(&b2);
-        pk.w = *reinterpret_cast<uint32_t*>(&b3);
-        *reinterpret_cast<uint4*>(sP + (ch >> 3) * (128 * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4)) = pk;
-      }
-      lrun = lrun * alpha + sum;
-      mrun = mx;
-      // rescale the running O (PV u-1 has landed); tcgen05.ld/st are warp-collective, so the
-      // warp skips only when none of its rows' max moved
-      if (u > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        const float mnew = fmaxf(mused, mx);
+        const float alpha = exp2f(mused - mnew);
         uint32_t orr[HD];
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c)
@@ -267,13 +285,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
           tmem_st32(tO + lane_off + c * 32, v);
         }
         tmem_wait_st();
+        lrun *= alpha;
+        mused = mnew;
       }
+      // P(u) reuses the buffer PV(u - kPBufs) read
+      if (u >= C::kPBufs) {
+        const int w = u - C::kPBufs;
+        sm100::mbar_wait(&pv_done[w & 1], (w >> 1) & 1);
+      }
+      uint8_t* pbuf = sP + (u % C::kPBufs) * C::kP;
+      // P = exp2(S - m_ref) as bf16 (K-major SW128: keys 0..63 atom 0, 64..127 atom 1)
+      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+      const float nm = -mused;
+#pragma unroll
+      for (int ch = 0; ch < kKeysPerStep / 8; ++ch) {
+        float p8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float e = ex2(fmaf(__uint_as_float(sr[ch * 8 + i]), scale_log2, nm));
+          p8[i] = (full_step || kb + ch * 8 + i <= lim) ? e : 0.f;
+          sum4[i & 3] += p8[i];
+        }
+        uint4 pk;
+        __nv_bfloat162 b0 = __floats2bfloat162_rn(p8[0], p8[1]), b1 = __floats2bfloat162_rn(p8[2], p8[3]);
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(p8[4], p8[5]), b3 = __floats2bfloat162_rn(p8[6], p8[7]);
+        pk.x = *reinterpret_cast<uint32_t*>(&b0);
+        pk.y = *reinterpret_cast<uint32_t*>(&b1);
+        pk.z = *reinterpret_cast<uint32_t*>(&b2);
+        pk.w = *reinterpret_cast<uint32_t*>(&b3);
+        *reinterpret_cast<uint4*>(pbuf + (ch >> 3) * (128 * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4)) = pk;
+      }
+      lrun += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       fence_proxy_async();  // P (generic smem writes) visible to the tensor core
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&p_full);
+      sm100::mbar_arrive(&p_full[u & 1]);
     }
     // ---- epilogue: O / l -> bf16 rows
-    sm100::mbar_wait(&o_done, (nsteps - 1) & 1);
+    sm100::mbar_wait(&pv_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
     sm100::tc_fence_after();
     const float inv = lrun > 0.f ? 1.f / lrun : 0.f;
 #pragma unroll
@@ -281,7 +329,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       float v[32];
       sm100::tmem_ld32(tO + lane_off + c * 32, v);
       if (m < M) {
-        __nv_bfloat16* od = obuf + (static_cast<int64_t>(first + (m >> gs)) * n_q + kvh * G + (m & gm)) * HD + c * 32;
+        __nv_bfloat16* od = obuf + (static_cast<int64_t>(first + (mg >> gs)) * n_q + kvh * G + (mg & gm)) * HD + c * 32;
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           uint4 pk;
@@ -307,36 +355,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
 }
 
 template <int HD>
-cudaError_t launch_tc(const LlamaShape& m, RowsDev rows, int n_req, KvDev kv, int layer, const __nv_bfloat16* qbuf,
-                      __nv_bfloat16* obuf, float scale_log2, cudaStream_t s) {
+cudaError_t launch_tc(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req, KvDev kv, int layer,
+                      const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, float scale_log2, cudaStream_t s) {
   using C = TcCfg<HD>;
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
-  dim3 grid(n_req, m.n_kv, 1);
+  const int Mmax = max_rows_per_req * (m.n_q / m.n_kv);
+  dim3 grid(n_req, m.n_kv, (Mmax + 127) / 128);
   attn_tc_kernel<HD><<<grid, kTcThreads, C::kSmem, s>>>(*kv.tma, rows, kv, layer, m.n_q, m.n_kv, qbuf, obuf,
-                                                       scale_log2);
+                                                       scale_log2, Mmax <= 64 ? 1 : 0);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+bool attn_tc_rows_applies(const LlamaShape& m, int max_ctx, const KvDev& kv) {
+  // prefill / long-row blocks (> 64 packed rows): 128-row tiles keep all four softmax warps busy
+  // (FASER_ATTN_TC_ROWS=0 keeps the mma.sync ROWS kernel)
+  static const bool on = !(getenv("FASER_ATTN_TC_ROWS") && getenv("FASER_ATTN_TC_ROWS")[0] == '0');
+  return on && kv.tma != nullptr && (m.hd == 64 || m.hd == 128) && (max_ctx + 63) / 64 <= kMaxPagesTc;
+}
+
 bool attn_tc_applies(const LlamaShape& m, int max_rows_per_req, int max_ctx, const KvDev& kv) {
-  // opt-in (FASER_ATTN_TC=1): parity-green, but slower than the mma.sync kernel on B200 — the
-  // per-step softmax over 128 keys runs on one warp per SM sub-partition (one 145-193 KB CTA
-  // per SM) and is latency-bound at ~4 us per step (profiles/r02_attn_tc_ab.txt)
+  // opt-in (FASER_ATTN_TC=1): parity-green; on par with the mma.sync kernel at 32 requests (hd 64)
+  // but slower at 128 requests and at hd 128 — one CTA per SM (512 TMEM columns) against
+  // mma.sync's several (profiles/r02_attn_tc_ab.txt)
   static const bool on = getenv("FASER_ATTN_TC") && getenv("FASER_ATTN_TC")[0] == '1';
   const int G = m.n_q / m.n_kv;
   return on && kv.tma != nullptr && (m.hd == 64 || m.hd == 128) && G >= 4 && max_rows_per_req * G <= 64 &&
          (max_ctx + 63) / 64 <= kMaxPagesTc;
 }
 
-cudaError_t lm_attention_tc(const LlamaShape& m, RowsDev rows, int n_req, KvDev kv, int layer,
+cudaError_t lm_attention_tc(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req, KvDev kv, int layer,
                             const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, cudaStream_t s) {
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(m.hd));
-  if (m.hd == 64) return launch_tc<64>(m, rows, n_req, kv, layer, qbuf, obuf, scale_log2, s);
-  return launch_tc<128>(m, rows, n_req, kv, layer, qbuf, obuf, scale_log2, s);
+  if (m.hd == 64) return launch_tc<64>(m, rows, n_req, max_rows_per_req, kv, layer, qbuf, obuf, scale_log2, s);
+  return launch_tc<128>(m, rows, n_req, max_rows_per_req, kv, layer, qbuf, obuf, scale_log2, s);
 }
 
 }  // namespace faser
