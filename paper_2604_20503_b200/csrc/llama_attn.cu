@@ -22,6 +22,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "llama.cuh"
@@ -555,6 +556,14 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
     n_split = (target + base - 1) / base;
     const int max_split = (tiles + 1) / 2 < 16 ? (tiles + 1) / 2 : 16;  // >= 2 pages per split
     if (n_split > max_split) n_split = max_split;
+  }
+  static int dbg = getenv("FASER_ATTN_DEBUG") ? atoi(getenv("FASER_ATTN_DEBUG")) : 0;
+  if (dbg > 0) {
+    --dbg;
+    fprintf(stderr, "[attn] n_req %d max_rows %d max_ctx %d Mmax %d split %d tma %d group_tc %d rows_tc %d\n", n_req,
+            max_rows_per_req, max_ctx, Mmax, n_split, kv.tma != nullptr,
+            int(!rows_mode && attn_tc_applies(m, max_rows_per_req, max_ctx, kv)),
+            int(rows_mode && attn_tc_rows_applies(m, max_ctx, kv)));
   }
   // tensor-core path (llama_attn_tc.cu) for GQA-packed rows when no KV split is wanted
   if (n_split == 1 && !rows_mode && attn_tc_applies(m, max_rows_per_req, max_ctx, kv))

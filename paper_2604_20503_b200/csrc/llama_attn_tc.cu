@@ -7,19 +7,20 @@
 //   S  = Q K^T      tcgen05.mma M128 x N128, K = head_dim; A = Q (smem, K-major SW128),
 //                   B = the two K pages as TMA wrote them ([key][hd], K-major SW128); S in TMEM,
 //                   double-buffered (S of step u+1 is issued before P V of step u)
-//   softmax         4 warps, thread t = packed row t: its 128 scores come out of TMEM with
-//                   tcgen05.ld (no shuffles); unmasked steps skip the causal compares; running
+//   softmax         8 warps: thread (quarter, half) owns tile row t and 64 of the step's keys,
+//                   read out of TMEM with tcgen05.ld (no shuffles), the two halves' row maxima
+//                   combined through smem; unmasked steps skip the causal compares; running
 //                   max / sum on the raw scores (one FFMA + one MUFU.EX2 per key); the O rescale
 //                   on TMEM is lazy (only when the max grew by 2^8); P = exp2(S - m) as bf16 into
 //                   smem (K-major SW128, double-buffered for hd 64)
 //   O += P V        tcgen05.mma M128 x N(head_dim), K = 128 keys; A = P, B = the two V pages
 //                   read MN-major ([key][hd] rows = K, head_dim contiguous = N), O in TMEM
-// Warp roles: warps 0-3 softmax / epilogue, warp 4 TMA producer (pages into a ring of steps),
-// warp 5 MMA issuer. The epilogue divides O by the row sums and writes bf16 rows.
+// Warp roles: warps 0-7 softmax / epilogue, warp 8 TMA producer (pages into a ring of steps),
+// warp 9 MMA issuer. The epilogue divides O by the row sums and writes bf16 rows.
 // Dispatch (llama_attn.cu): ROW blocks (> 64 packed rows per request: prefill, long verify) by
-// default — about 2x the mma.sync kernel there; GQA-packed GROUP rows opt-in (FASER_ATTN_TC=1),
-// where the one-CTA-per-SM footprint (512 TMEM columns, 145-193 KB smem) loses to mma.sync's
-// occupancy at large batch (profiles/r02_attn_tc_ab.txt).
+// default — about 2x the mma.sync kernel there; GQA-packed GROUP rows by default above 32 packed
+// rows (where mma.sync reads each page twice); at <= 32 the one-CTA-per-SM footprint (512 TMEM
+// columns, 145-193 KB smem) loses to mma.sync's occupancy (profiles/r02_attn_tc_ab.txt).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,7 +37,9 @@ namespace faser {
 namespace {
 
 constexpr float kNegBigT = -1e30f;
-constexpr int kTcThreads = 192;     // 4 softmax warps + producer + MMA issuer
+constexpr int kSmWarps = 8;         // softmax: 4 TMEM lane quarters x 2 key halves
+constexpr int kTcThreads = (kSmWarps + 2) * 32;  // + TMA producer + MMA issuer
+constexpr int kProdWarp = kSmWarps, kMmaWarp = kSmWarps + 1;
 constexpr int kKeysPerStep = 128;   // two pages
 constexpr int kMaxPagesTc = 512;
 
@@ -116,6 +119,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   uint8_t* sP = sKV + C::kStages * C::kStep;
   __shared__ __align__(8) uint64_t full[C::kStages], empty[C::kStages];
   __shared__ __align__(8) uint64_t s_full[2], p_full[2], pv_done[2];  // by step parity
+  __shared__ float xmax[2][2][128];  // [step parity][key half][tile row]: partial row maxima
+  __shared__ float xsum[2][128];     // [key half][tile row]: partial row sums
   __shared__ uint32_t tmem_slot;
   __shared__ int s_page[kMaxPagesTc];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
     }
     for (int b = 0; b < 2; ++b) {
       sm100::mbar_init(&s_full[b], 1);
-      sm100::mbar_init(&p_full[b], 128);
+      sm100::mbar_init(&p_full[b], kSmWarps * 32);
       sm100::mbar_init(&pv_done[b], 1);
     }
     sm100::fence_mbar_init();
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   const uint32_t tmem = tmem_slot;
   const uint32_t tO = tmem + 256;  // S(u) at tmem + (u % 2) * 128
 
-  if (warp == 4) {
+  if (warp == kProdWarp) {
     // ---------------------------------------------------------------- TMA producer
     // one lane per TMA box (K/V x page x head_dim atom): a lane's boxes are served one after
     // another, so the step's 4 (hd 64) or 8 (hd 128) boxes are issued by as many lanes
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
                            row + kvsel * 64);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(128, kKeysPerStep);
@@ -234,55 +239,66 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
     }
   } else {
     // ---------------------------------------------------------------- softmax + epilogue
-    const int t = threadIdx.x;                                // tile row = TMEM lane
+    // warp w: TMEM lane quarter w % 4 (tile rows 32 (w % 4) ..), key half kh = w / 4 of each step
+    // (64 keys, P atom kh, O columns [kh HD/2, (kh + 1) HD/2) for rescale and epilogue); the two
+    // warps of a quarter combine their row maxima through smem at every step (named barrier)
+    constexpr int kHalfKeys = kKeysPerStep / 2;
+    const int qw = warp & 3, kh = warp >> 2;
+    const int t = qw * 32 + lane;                             // tile row = TMEM lane
     const int m = spread ? (((t & 31) << 2) | (t >> 5)) : t;  // its tile-relative packed row
     const int mg = m0 + m;
     const int lim = m < M ? pos0 + (mg >> gs) : -1;           // last key this row sees
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    const uint32_t ocol = kh * (HD / 2);
+    auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(1 + qw) : "memory"); };
     // warp-uniform: the smallest causal limit among the warp's live rows (steps entirely below it
     // need no masking; padded rows compute garbage that only their own, never-written rows see)
     const int wlim = __reduce_min_sync(0xffffffffu, m < M ? lim : 0x7fffffff);
-    float mused = kNegBigT, lrun = 0.f;  // reference max of P and O (lazily raised), row sum
+    float mused = kNegBigT, lrun = 0.f;  // reference max of P and O (lazily raised), partial row sum
     for (int u = 0; u < nsteps; ++u) {
       sm100::mbar_wait(&s_full[u & 1], (u >> 1) & 1);
       sm100::tc_fence_after();
-      const int kb = u * kKeysPerStep;
-      uint32_t sr[kKeysPerStep];
+      const int kb = u * kKeysPerStep + kh * kHalfKeys;
+      uint32_t sr[kHalfKeys];
 #pragma unroll
-      for (int c = 0; c < kKeysPerStep / 32; ++c)
-        tmem_ld32_nw(tmem + (u & 1) * 128 + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      for (int c = 0; c < kHalfKeys / 32; ++c)
+        tmem_ld32_nw(tmem + (u & 1) * 128 + kh * kHalfKeys + lane_off + c * 32,
+                     *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_wait_ld();
-      const bool full_step = kb + kKeysPerStep - 1 <= wlim;  // no key of the step is masked
+      const bool full_step = kb + kHalfKeys - 1 <= wlim;  // no key of this half is masked
       float mx4[4] = {kNegBigT, kNegBigT, kNegBigT, kNegBigT};  // independent chains, raw scores
       if (full_step) {
 #pragma unroll
-        for (int i = 0; i < kKeysPerStep; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[i]));
+        for (int i = 0; i < kHalfKeys; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[i]));
       } else {
 #pragma unroll
-        for (int i = 0; i < kKeysPerStep; ++i)
+        for (int i = 0; i < kHalfKeys; ++i)
           if (kb + i <= lim) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[i]));
       }
-      const float mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      xmax[u & 1][kh][t] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      pair_sync();
+      const float mraw = fmaxf(xmax[u & 1][0][t], xmax[u & 1][1][t]);  // same value in both halves
       const float mx = mraw > kNegBigT ? mraw * scale_log2 : kNegBigT;  // (scale > 0)
       if (u == 0) {
         mused = mx;
       } else if (__any_sync(0xffffffffu, mx > mused + C::kRescaleLog2)) {
-        // the warp raises its reference max: O must be current (PV u-1 landed) to rescale it
+        // the quarter raises its reference max (both halves decide alike): O must be current (PV
+        // u-1 landed) to rescale it; each half rescales its O columns
         sm100::mbar_wait(&pv_done[(u - 1) & 1], ((u - 1) >> 1) & 1);
         sm100::tc_fence_after();
         const float mnew = fmaxf(mused, mx);
         const float alpha = exp2f(mused - mnew);
-        uint32_t orr[HD];
+        uint32_t orr[HD / 2];
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c)
-          tmem_ld32_nw(tO + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&orr[c * 32]));
+        for (int c = 0; c < HD / 64; ++c)
+          tmem_ld32_nw(tO + ocol + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&orr[c * 32]));
         tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < HD / 64; ++c) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(orr[c * 32 + i]) * alpha;
-          tmem_st32(tO + lane_off + c * 32, v);
+          tmem_st32(tO + ocol + lane_off + c * 32, v);
         }
         tmem_wait_st();
         lrun *= alpha;
@@ -293,12 +309,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
         const int w = u - C::kPBufs;
         sm100::mbar_wait(&pv_done[w & 1], (w >> 1) & 1);
       }
-      uint8_t* pbuf = sP + (u % C::kPBufs) * C::kP;
-      // P = exp2(S - m_ref) as bf16 (K-major SW128: keys 0..63 atom 0, 64..127 atom 1)
+      // P = exp2(S - m_ref) as bf16 (K-major SW128: this half's 64 keys are P atom kh)
+      uint8_t* pbuf = sP + (u % C::kPBufs) * C::kP + kh * (128 * 128);
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};
       const float nm = -mused;
 #pragma unroll
-      for (int ch = 0; ch < kKeysPerStep / 8; ++ch) {
+      for (int ch = 0; ch < kHalfKeys / 8; ++ch) {
         float p8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -313,23 +329,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
         pk.y = *reinterpret_cast<uint32_t*>(&b1);
         pk.z = *reinterpret_cast<uint32_t*>(&b2);
         pk.w = *reinterpret_cast<uint32_t*>(&b3);
-        *reinterpret_cast<uint4*>(pbuf + (ch >> 3) * (128 * 128) + t * 128 + (((ch & 7) ^ (t & 7)) << 4)) = pk;
+        *reinterpret_cast<uint4*>(pbuf + t * 128 + ((ch ^ (t & 7)) << 4)) = pk;
       }
       lrun += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       fence_proxy_async();  // P (generic smem writes) visible to the tensor core
       sm100::tc_fence_before();
       sm100::mbar_arrive(&p_full[u & 1]);
     }
-    // ---- epilogue: O / l -> bf16 rows
+    // ---- epilogue: O / l -> bf16 rows (each half its O columns; l = both halves' sums)
+    xsum[kh][t] = lrun;
+    pair_sync();
+    const float l = xsum[0][t] + xsum[1][t];
     sm100::mbar_wait(&pv_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
     sm100::tc_fence_after();
-    const float inv = lrun > 0.f ? 1.f / lrun : 0.f;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < HD / 64; ++c) {
       float v[32];
-      sm100::tmem_ld32(tO + lane_off + c * 32, v);
+      sm100::tmem_ld32(tO + ocol + lane_off + c * 32, v);
       if (m < M) {
-        __nv_bfloat16* od = obuf + (static_cast<int64_t>(first + (mg >> gs)) * n_q + kvh * G + (mg & gm)) * HD + c * 32;
+        __nv_bfloat16* od =
+            obuf + (static_cast<int64_t>(first + (mg >> gs)) * n_q + kvh * G + (mg & gm)) * HD + ocol + c * 32;
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           uint4 pk;
@@ -379,13 +399,16 @@ bool attn_tc_rows_applies(const LlamaShape& m, int max_ctx, const KvDev& kv) {
 }
 
 bool attn_tc_applies(const LlamaShape& m, int max_rows_per_req, int max_ctx, const KvDev& kv) {
-  // opt-in (FASER_ATTN_TC=1): parity-green; on par with the mma.sync kernel at 32 requests (hd 64)
-  // but slower at 128 requests and at hd 128 — one CTA per SM (512 TMEM columns) against
-  // mma.sync's several (profiles/r02_attn_tc_ab.txt)
-  static const bool on = getenv("FASER_ATTN_TC") && getenv("FASER_ATTN_TC")[0] == '1';
+  // GQA-packed GROUP rows: by default only above 32 packed rows, where the mma.sync kernel needs
+  // two 32-row blocks per (request, kv head) and so reads the KV pages twice; at <= 32 rows it keeps
+  // several CTAs per SM and wins (one CTA per SM here: 512 TMEM columns). FASER_ATTN_TC=1 takes
+  // every GROUP shape, =0 none (profiles/r02_attn_tc_ab.txt, r02_attn_group_split.txt)
+  static const char* env = getenv("FASER_ATTN_TC");
+  static const int force = env ? (env[0] == '1' ? 1 : 0) : -1;
   const int G = m.n_q / m.n_kv;
-  return on && kv.tma != nullptr && (m.hd == 64 || m.hd == 128) && G >= 4 && max_rows_per_req * G <= 64 &&
-         (max_ctx + 63) / 64 <= kMaxPagesTc;
+  const bool shape = kv.tma != nullptr && (m.hd == 64 || m.hd == 128) && G >= 4 && max_rows_per_req * G <= 64 &&
+                     (max_ctx + 63) / 64 <= kMaxPagesTc;
+  return shape && (force == 1 || (force < 0 && max_rows_per_req * G > 32));
 }
 
 cudaError_t lm_attention_tc(const LlamaShape& m, RowsDev rows, int n_req, int max_rows_per_req, KvDev kv, int layer,

@@ -58,8 +58,8 @@ def run_case(L, n_q, n_kv, hd, rows_per_req, ctx, seed=0):
             assert err < 3e-2, (i, h, err)
 
 
-# "batch": enough (request, kv head) units that no KV split is wanted (with FASER_ATTN_TC=1, GQA
-# groups of >= 4 heads take the tcgen05 kernel, llama_attn_tc.cu): odd / even page counts,
+# "batch": enough (request, kv head) units that no KV split is wanted (GQA groups of >= 4 heads
+# with > 32 packed rows take the tcgen05 kernel, llama_attn_tc.cu): odd / even page counts,
 # 1..1500 keys
 BATCH_ROWS = [4] * 20 + [1, 2, 3, 5, 8, 4, 4, 4]
 BATCH_CTX = [4, 63, 64, 65, 127, 128, 129, 191, 192, 193, 255, 256, 257, 600, 640, 700, 900, 1000, 1280, 1500,
@@ -82,15 +82,21 @@ def test_attention_matches_fp32(L, n_q, n_kv, hd, shape):
 
 
 @pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (32, 8, 128)])
-def test_tcgen05_attention_matches_fp32(n_q, n_kv, hd):
-    """The opt-in tcgen05 attention (FASER_ATTN_TC=1, read once per process) in a subprocess."""
+@pytest.mark.parametrize("kernels", ["tcgen05", "mma_sync"])
+def test_attention_dispatch_variants(n_q, n_kv, hd, kernels):
+    """The non-default dispatches (env read once per process, so in a subprocess): tcgen05 for
+    every GQA-packed GROUP shape (FASER_ATTN_TC=1), or the mma.sync kernels everywhere
+    (FASER_ATTN_TC=0, FASER_ATTN_TC_ROWS=0)."""
     import os
     import subprocess
     import sys
+    env = {"tcgen05": {"FASER_ATTN_TC": "1"}, "mma_sync": {"FASER_ATTN_TC": "0", "FASER_ATTN_TC_ROWS": "0"}}[kernels]
     code = ("import sys; sys.path.insert(0, 'tests'); import test_attention_gpu as t; "
-            "from paper_2604_20503_b200 import engine; "
-            f"t.run_case(engine.lib(), {n_q}, {n_kv}, {hd}, t.BATCH_ROWS, t.BATCH_CTX, seed=5)")
+            "from paper_2604_20503_b200 import engine; L = engine.lib(); "
+            f"t.run_case(L, {n_q}, {n_kv}, {hd}, t.BATCH_ROWS, t.BATCH_CTX, seed=5); "
+            f"t.run_case(L, {n_q}, {n_kv}, {hd}, [96, 33], [96, 33], seed=6); "
+            f"t.run_case(L, {n_q}, {n_kv}, {hd}, [2, 70, 1, 16], [2, 900, 129, 16], seed=7)")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "FASER_ATTN_TC": "1"},
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

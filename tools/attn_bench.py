@@ -15,19 +15,26 @@ L = engine.lib()
 
 
 def run(n_req, rows, ctx, n_q=32, n_kv=4, hd=64, iters=20):
-    max_pages = (ctx + 63) // 64 + 1
+    # ATTN_BENCH_RAGGED=1: per-request contexts uniform in [ctx/4, 7 ctx/4] (mean ctx), as in a
+    # continuous batch; max_ctx (grid / split decisions) is the longest
+    ragged = os.environ.get("ATTN_BENCH_RAGGED") == "1"
+    g = torch.Generator().manual_seed(1)
+    ctxs = [int(torch.randint(max(rows, ctx // 4), ctx * 7 // 4 + 1, (1,), generator=g)) if ragged else ctx
+            for _ in range(n_req)]
+    max_ctx = max(ctxs)
+    max_pages = (max_ctx + 63) // 64 + 1
     kvs = [torch.randn(n_req * max_pages, n_kv, 2, 64, hd, device="cuda").to(torch.bfloat16) for _ in range(iters)]
     ptab = torch.randperm(n_req * max_pages, device="cuda").to(torch.int32).view(n_req, max_pages).contiguous()
     q = torch.randn(n_req * rows, n_q, hd, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     t = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")
-    first, n, pos0 = t([i * rows for i in range(n_req)]), t([rows] * n_req), t([ctx - rows] * n_req)
+    first, n, pos0 = t([i * rows for i in range(n_req)]), t([rows] * n_req), t([c - rows for c in ctxs])
     scratch = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
 
     def call(s, kv):
         assert L.faser_k_attention(C.c_void_p(q.data_ptr()), C.c_void_p(kv.data_ptr()), C.c_void_p(ptab.data_ptr()),
                                    max_pages, n_req, C.c_void_p(first.data_ptr()), C.c_void_p(n.data_ptr()),
-                                   C.c_void_p(pos0.data_ptr()), rows, ctx, n_q, n_kv, hd, C.c_void_p(out.data_ptr()),
+                                   C.c_void_p(pos0.data_ptr()), rows, max_ctx, n_q, n_kv, hd, C.c_void_p(out.data_ptr()),
                                    C.c_void_p(scratch.data_ptr()), scratch.numel(), C.c_void_p(s)) == 0
     call(torch.cuda.current_stream().cuda_stream, kvs[0])
     g = torch.cuda.CUDAGraph()
@@ -43,8 +50,8 @@ def run(n_req, rows, ctx, n_q=32, n_kv=4, hd=64, iters=20):
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / iters
-    kvb = n_req * ctx * n_kv * 2 * hd * 2
-    return {"n_req": n_req, "rows": rows, "ctx": ctx, "n_q": n_q, "n_kv": n_kv, "hd": hd, "us": round(us, 2),
+    kvb = sum(ctxs) * n_kv * 2 * hd * 2
+    return {"n_req": n_req, "rows": rows, "ctx": ctx, "ragged": ragged, "max_ctx": max_ctx, "n_q": n_q, "n_kv": n_kv, "hd": hd, "us": round(us, 2),
             "kv_GBs": round(kvb / us / 1e3, 1)}
 
 
