@@ -24,7 +24,10 @@ from paper_2604_20503_b200 import engine  # noqa: E402
 
 L = engine.lib()
 SHAPES = {"cfg3": {"qkv": (2560, 2048), "o": (2048, 2048), "gu": (11264, 2048), "down": (2048, 5632)},
-          "cfg4": {"qkv": (6144, 4096), "o": (4096, 4096), "gu": (28672, 4096), "down": (4096, 14336)}}
+          "cfg4": {"qkv": (6144, 4096), "o": (4096, 4096), "gu": (28672, 4096), "down": (4096, 14336)},
+          # config-3 draft (llama-68m shape) and its LM head (the draft's other GEMM per step)
+          "draft": {"qkv": (2304, 768), "o": (768, 768), "gu": (6144, 768), "down": (768, 3072)},
+          "draft_lm": {"lm": (32000, 768)}}
 
 
 def main():
