@@ -225,6 +225,12 @@ def p50_tpot_ms(first, last):
     return 1e3 * statistics.median(tp) if tp else None
 
 
+def mean_tpot_ms(first, last):
+    """metrics.hpp:45's mean over requests, of each request's per-token time inside the window"""
+    tp = [(last[r][0] - first[r]) / (last[r][1] - 1) for r in last if last[r][1] >= 2]
+    return 1e3 * statistics.fmean(tp) if tp else None
+
+
 # ------------------------------------------------------------------ Llama workload (config 3)
 IN_RANGE, OUT_RANGE = (128, 1024), (64, 256)
 
@@ -541,7 +547,8 @@ def serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e, want_kst
     dev_ms = ev0.elapsed_time(ev1)
     nsteps = max(st.get("steps", 0), 1)
     out = {"B": B, "dev_ms": dev_ms, "tokens": tokens, "steps_run": st.get("steps", 0), "fill_steps": fill_steps,
-           "p50_tpot_ms": p50_tpot_ms(st["first"], st["last"]), "launches": launches, "clocks": clk.summary(),
+           "p50_tpot_ms": p50_tpot_ms(st["first"], st["last"]), "mean_tpot_ms": mean_tpot_ms(st["first"], st["last"]),
+           "accepted_draft": st.get("acc", 0), "launches": launches, "clocks": clk.summary(),
            "wall_s": wall, "draft_ms": acc_ms["draft"] / nsteps, "verify_ms": acc_ms["verify"] / nsteps,
            "prefill_ms": acc_ms["prefill"] / nsteps,
            "acceptance": st.get("acc", 0) / max(st.get("sub", 1), 1),
@@ -640,6 +647,9 @@ def llama_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts (synth_prompt), random-init weights",
         "p50_tpot_ms": head["p50_tpot_ms"],
+        "mean_tpot_ms": head["mean_tpot_ms"],
+        # accepted drafted tokens per second (metrics.hpp:53; committed = these + recovery tokens), rank 0
+        "accepted_draft_tokens_per_s": head["accepted_draft"] / (head["dev_ms"] / 1e3),
         "config": llama_config(args, world, B),
         "e2e": {"value": tokens2 / e2e_s, "unit": UNIT, "p50_tpot_ms": head["e2e"]["p50_tpot_ms"],
                 "h2d_bytes_per_step": head["e2e"]["h2d_bytes_per_step"],

@@ -552,7 +552,11 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
   const int tiles = (max_ctx + 63) / 64;
   int n_split = 1;
   static const int target = getenv("FASER_ATTN_CTAS") ? atoi(getenv("FASER_ATTN_CTAS")) : 148;
-  if (base < target / 2 && tiles >= 4) {
+  // a split costs a partial write + counter + merge round trip (~4 us with one M tile per CTA,
+  // ~7 us with two) against ~0.65 us per page a CTA no longer walks: worth it only for long
+  // contexts (profiles/r02_attn_split_small_batch.txt)
+  const int min_tiles = mt == 2 ? 24 : 12;
+  if (base < target / 2 && tiles >= min_tiles) {
     n_split = (target + base - 1) / base;
     const int max_split = (tiles + 1) / 2 < 16 ? (tiles + 1) / 2 : 16;  // >= 2 pages per split
     if (n_split > max_split) n_split = max_split;
