@@ -34,8 +34,11 @@ namespace {
 constexpr float kNegBig = -1e30f;
 constexpr int kMaxPagesPerCta = 256;
 // pipeline depth (pages of K+V in flight): latency-bound decode wants many pages in flight
+#ifndef FASER_ATTN_STAGES
+#define FASER_ATTN_STAGES 3
+#endif
 template <int HD>
-constexpr int kAttnStages = 3;
+constexpr int kAttnStages = FASER_ATTN_STAGES;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),

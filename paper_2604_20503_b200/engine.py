@@ -17,7 +17,8 @@ import numpy as np
 from . import abi
 
 _LIB = None
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfaser_b200.so")
+# FASER_LIB: an alternative build of the same library (compile-time A/B variants, tools/build_variant.py)
+LIB_PATH = os.environ.get("FASER_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfaser_b200.so")
 
 
 class FaserError(RuntimeError):
