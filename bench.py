@@ -351,7 +351,9 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
     Returns the committed tokens; state["steps"] counts the steps actually executed and
     state["finished"] the requests that completed."""
     tokens = 0
+    prof = HOST_PROF if os.environ.get("BENCH_HOST_PROF") == "1" else None
     for _ in range(n_steps):
+        t_a = time.perf_counter()
         if feeder is not None:
             feeder()
         live = eng.live_requests()
@@ -365,7 +367,9 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
             eng.set_gate(gate)
         if hook is not None:
             hook(eng, live, ks or [eng.cfg.default_spec_length] * len(live))
+        t_b = time.perf_counter()
         res = eng.step()
+        t_c = time.perf_counter()
         state["steps"] = state.get("steps", 0) + 1
         for r in res:
             state["acc"] = state.get("acc", 0) + r.outcome.accepted_count
@@ -381,7 +385,16 @@ def run_llama_steps(eng, n_steps, clock, state, feeder=None, gate=None, drafter=
                 state["first"].setdefault(r.req_id, now)
                 n0 = state["last"].get(r.req_id, (0, 0))[1]
                 state["last"][r.req_id] = (now, n0 + r.committed)
+        if prof is not None:
+            t_d = time.perf_counter()
+            prof["pre_ms"] += 1e3 * (t_b - t_a)
+            prof["step_ms"] += 1e3 * (t_c - t_b)
+            prof["post_ms"] += 1e3 * (t_d - t_c)
+            prof["steps"] += 1
     return tokens
+
+
+HOST_PROF = {"pre_ms": 0.0, "step_ms": 0.0, "post_ms": 0.0, "steps": 0}  # BENCH_HOST_PROF=1
 
 
 def drafter_r(eng):
@@ -680,6 +693,8 @@ def llama_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = llama_cpu_sample(desc, args, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
+    if os.environ.get("BENCH_HOST_PROF") == "1":
+        print("host per step (all run_llama_steps calls): " + json.dumps({k: (v / max(HOST_PROF["steps"], 1) if k != "steps" else v) for k, v in HOST_PROF.items()}), file=sys.stderr)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
