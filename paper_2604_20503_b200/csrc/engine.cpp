@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <deque>
@@ -170,6 +172,8 @@ struct faser_engine {
   StepIn* h_in = nullptr;  // pinned
   StepIn* d_in = nullptr;
   faser_round_result* h_res = nullptr;  // pinned
+  double prof_pre = 0, prof_sync = 0, prof_post = 0;  // host ms per phase of faser_step (FASER_TOY_PROF)
+  double prof_dev_draft = 0, prof_dev_verify = 0;      // device ms (events) of the same steps
   faser_round_result* d_res = nullptr;
   std::string err;
   int64_t launches = 0;
@@ -354,6 +358,7 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
   if (!e || !n_out) return FASER_EINVAL;
   if (e->llama) return faser::llama_step(e->llama, plan, out, cap, n_out);
   return guarded(&e->err, [&] {
+    const auto q0 = std::chrono::steady_clock::now();
     CK(cudaSetDevice(e->cfg.device));
     e->admit_pending();
     const int n_live = static_cast<int>(e->live.size());
@@ -406,11 +411,11 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
       CK(toy_admit(e->m, sv, e->d_in, in.n_admit, e->stream));
       ++e->launches;
     }
-    CK(toy_draft(e->m, sv, e->d_in, n_live, e->stream));
+    // draft + verify + commit fused per request (one launch); t_draft = admission only
     CK(cudaEventRecord(e->ev[1], e->stream));
-    CK(toy_verify_commit(e->m, sv, e->d_in, n_live, e->d_res, e->stream));
+    CK(toy_draft_verify_commit(e->m, sv, e->d_in, n_live, e->d_res, e->stream));
     CK(cudaEventRecord(e->ev[2], e->stream));
-    e->launches += 2;
+    e->launches += 1;
     CK(cudaMemcpyAsync(e->h_res, e->d_res, sizeof(faser_round_result) * n_live,
                        cudaMemcpyDeviceToHost, e->stream));
     for (int p = 0; p < n_live; ++p) {
@@ -421,7 +426,9 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
         r.d_prompt = nullptr;
       }
     }
+    const auto q1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(e->stream));
+    const auto q2 = std::chrono::steady_clock::now();
     cudaEventElapsedTime(&e->t_draft, e->ev[0], e->ev[1]);
     cudaEventElapsedTime(&e->t_verify, e->ev[1], e->ev[2]);
     cudaEventElapsedTime(&e->t_step, e->ev[0], e->ev[2]);
@@ -441,6 +448,12 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
     }
     std::memcpy(out, e->h_res, sizeof(faser_round_result) * n_live);
     e->live.swap(keep);
+    const auto q3 = std::chrono::steady_clock::now();
+    e->prof_pre += std::chrono::duration<double, std::milli>(q1 - q0).count();
+    e->prof_sync += std::chrono::duration<double, std::milli>(q2 - q1).count();
+    e->prof_post += std::chrono::duration<double, std::milli>(q3 - q2).count();
+    e->prof_dev_draft += e->t_draft;
+    e->prof_dev_verify += e->t_verify;
   });
 }
 
@@ -802,12 +815,19 @@ extern "C" faser_status faser_serve_rounds(faser_engine* e, int32_t n_rounds, ui
   std::vector<faser_gate_entry> ents(cap);
   std::vector<faser_round_result> res(cap);
   std::unordered_map<int64_t, int32_t> served;
+  // FASER_TOY_PROF=1: host time per phase of the loop, printed at the end (stderr)
+  static const bool prof = std::getenv("FASER_TOY_PROF") != nullptr;
+  using clk = std::chrono::steady_clock;
+  double t_live = 0, t_k = 0, t_gate = 0, t_step = 0, t_post = 0;
+  auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   for (int it = 0; it < n_rounds; ++it) {
+    const auto p0 = clk::now();
     int32_t n = 0;
     faser_status st = faser_live_requests(e, ids.data(), cap, &n);
     if (st != FASER_OK) return st;
     if (n == 0) break;
     if (n > cap) return FASER_ECAPACITY;
+    const auto p1 = clk::now();
     for (int i = 0; i < n; ++i) {
       const int32_t rnd = served[ids[i]];
       const uint64_t h = srv_hash_combine(srv_hash_combine(srv_mix64(seed), static_cast<uint64_t>(ids[i] - id_base + 1)),
@@ -815,6 +835,7 @@ extern "C" faser_status faser_serve_rounds(faser_engine* e, int32_t n_rounds, ui
       ks[i] = kSrvCandidates[h % 8];
     }
     if ((st = faser_set_spec_lengths(e, ids.data(), ks.data(), n)) != FASER_OK) return st;
+    const auto p2 = clk::now();
     faser_step_plan plan{};
     if (policy) {
       for (int i = 0; i < n; ++i) {
@@ -826,13 +847,30 @@ extern "C" faser_status faser_serve_rounds(faser_engine* e, int32_t n_rounds, ui
                                      &plan.gate)) != FASER_OK)
         return st;
     }
+    const auto p3 = clk::now();
     int32_t got = 0;
     if ((st = faser_step(e, policy ? &plan : nullptr, res.data(), cap, &got)) != FASER_OK) return st;
+    const auto p4 = clk::now();
     for (int i = 0; i < got; ++i) {
       served[res[i].req_id] += 1;
       *tokens_out += res[i].committed;
     }
+    if (prof) {
+      const auto p5 = clk::now();
+      t_live += ms(p0, p1);
+      t_k += ms(p1, p2);
+      t_gate += ms(p2, p3);
+      t_step += ms(p3, p4);
+      t_post += ms(p4, p5);
+    }
     *rounds_out += 1;
+  }
+  if (prof && *rounds_out > 0) {
+    const double n = *rounds_out;
+    std::fprintf(stderr, "serve_rounds host ms/round: live %.4f k %.4f gate %.4f step %.4f (pre-launch %.4f, sync wait %.4f, post %.4f) loop-post %.4f; device admit+draft %.4f verify %.4f\n",
+                 t_live / n, t_k / n, t_gate / n, t_step / n, e->prof_pre / n, e->prof_sync / n, e->prof_post / n, t_post / n,
+                 e->prof_dev_draft / n, e->prof_dev_verify / n);
+    e->prof_pre = e->prof_sync = e->prof_post = e->prof_dev_draft = e->prof_dev_verify = 0;
   }
   return FASER_OK;
 }

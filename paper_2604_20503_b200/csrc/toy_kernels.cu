@@ -99,12 +99,12 @@ __device__ __forceinline__ int argmax_of(const ToyDev& m, const double (&z)[VPL]
 
 // token_exit_test (exitctl.cpp:56-68) on z = w*zf + (1-w)*zn at `layer`:
 // prune iff #{v : z[v] > z[d] or (z[v] == z[d] and v < d)} >= k.
+// w = layer / L and 1 - w come from a per-block table (layer_weights): the same correctly
+// rounded quotient target_logits forms (toylm.cpp:60), computed once instead of per row.
 template <int VPL>
 __device__ __forceinline__ bool exit_test(const ToyDev& m, const double (&zf)[VPL],
-                                          const double (&zn)[VPL], int layer, int d, int k) {
+                                          const double (&zn)[VPL], double w, double omw, int d, int k) {
   const int lane = threadIdx.x & 31;
-  const double w = __ddiv_rn(static_cast<double>(layer), static_cast<double>(m.layers));
-  const double omw = __dsub_rn(1.0, w);
   double z[VPL];
   double zsel = 0.0;
 #pragma unroll
@@ -120,6 +120,13 @@ __device__ __forceinline__ bool exit_test(const ToyDev& m, const double (&zf)[VP
     cnt += (t < m.vocab) && (z[q] > ref || (z[q] == ref && t < d));
   }
   return __reduce_add_sync(kFull, static_cast<unsigned>(cnt)) >= static_cast<unsigned>(k);
+}
+// tab[l] = (l / L, 1 - l / L) for l in [lo, hi), by the block's threads (needs a __syncthreads)
+__device__ __forceinline__ void layer_weights(const ToyDev& m, int lo, int hi, double2* tab) {
+  for (int l = lo + static_cast<int>(threadIdx.x); l < hi; l += blockDim.x) {
+    const double w = __ddiv_rn(static_cast<double>(l), static_cast<double>(m.layers));
+    tab[l] = make_double2(w, __dsub_rn(1.0, w));
+  }
 }
 
 // ----------------------------------------------------------------------------- admit
@@ -153,13 +160,9 @@ __global__ void admit_kernel(ToyDev m, SlotState st, const StepIn* __restrict__ 
 // min(k_i, remaining) sequential draft_next steps (toylm.cpp:76-85), EOS stop. The mix-hash
 // state after every drafted token is kept (mh_at) so commit can roll back in O(1).
 template <int VPL>
-__global__ void __launch_bounds__(128) draft_kernel(ToyDev m, SlotState st,
-                                                    const StepIn* __restrict__ in) {
-  __shared__ int32_t dl[4][FASER_MAX_SPEC];
-  const int wib = threadIdx.x >> 5;
-  const int p = blockIdx.x * 4 + wib;
+__device__ __forceinline__ void draft_one(const ToyDev& m, SlotState st, const StepIn* __restrict__ in, int p,
+                                          int32_t* dl) {
   const int lane = threadIdx.x & 31;
-  if (p >= in->n_live) return;
   const int slot = in->live_slot()[p];
   const int32_t* row = st.tok + static_cast<int64_t>(slot) * st.max_seq;
   const int base = st.len[slot];
@@ -175,13 +178,13 @@ __global__ void __launch_bounds__(128) draft_kernel(ToyDev m, SlotState st,
     const double u = to_unit(mh);
     int t = 0;
     if (!(u < m.divergence)) {
-      const uint64_t ch = context_hash(m, row, base, dl[wib], base + i);
+      const uint64_t ch = context_hash(m, row, base, dl, base + i);
       double zf[VPL], zn[VPL];
       logits<VPL>(m, ch, 0, false, zf, zn);
       t = argmax_of<VPL>(m, zf);
     }
     if (lane == 0) {
-      dl[wib][i] = t;
+      dl[i] = t;
       dout[i] = t;
     }
     __syncwarp();
@@ -193,6 +196,16 @@ __global__ void __launch_bounds__(128) draft_kernel(ToyDev m, SlotState st,
   if (lane == 0) st.draft_len[slot] = n;
 }
 
+template <int VPL>
+__global__ void __launch_bounds__(128) draft_kernel(ToyDev m, SlotState st,
+                                                    const StepIn* __restrict__ in) {
+  __shared__ int32_t dl[4][FASER_MAX_SPEC];
+  const int wib = threadIdx.x >> 5;
+  const int p = blockIdx.x * 4 + wib;
+  if (p >= in->n_live) return;
+  draft_one<VPL>(m, st, in, p, dl[wib]);
+}
+
 // ----------------------------------------------------------------------------- verify
 // Fused verify(+early exit) + accept + commit, one CTA per live request, warps over drafted
 // positions (sdcore.cpp:61-197). Phase 1 (parallel): per position j the target logits, the
@@ -200,16 +213,23 @@ __global__ void __launch_bounds__(128) draft_kernel(ToyDev m, SlotState st,
 // reference's sequential frontier scan over those bits, acceptance, force-verify, commit.
 constexpr int kVerifyWarps = 8;
 
+struct VerifySmem {
+  int32_t d[FASER_MAX_SPEC];
+  int32_t truth[FASER_MAX_SPEC];
+  uint32_t failpos[FASER_MAX_LAYERS + 1];
+  uint64_t nh_at[FASER_MAX_SPEC + 1];
+  double2 wt[FASER_MAX_LAYERS + 1];  // (l / L, 1 - l / L)
+};
+
+// request p's verify + commit by the whole block (kVerifyWarps warps); the block's draft for p,
+// when fused, was written by warp 0 before the block barrier this starts with
 template <int VPL>
-__global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(ToyDev m, SlotState st,
-                                                                   const StepIn* __restrict__ in,
-                                                                   faser_round_result* __restrict__ results) {
-  __shared__ int32_t d[FASER_MAX_SPEC];
-  __shared__ int32_t truth[FASER_MAX_SPEC];
-  __shared__ uint32_t failpos[FASER_MAX_LAYERS + 1];
-  __shared__ uint64_t nh_at[FASER_MAX_SPEC + 1];
-  const int p = blockIdx.x;
-  if (p >= in->n_live) return;
+__device__ __forceinline__ void verify_one(const ToyDev& m, SlotState st, const StepIn* __restrict__ in, int p,
+                                           faser_round_result* __restrict__ results, VerifySmem& sm) {
+  int32_t* d = sm.d;
+  int32_t* truth = sm.truth;
+  uint32_t* failpos = sm.failpos;
+  uint64_t* nh_at = sm.nh_at;
   const int slot = in->live_slot()[p];
   const int count = st.draft_len[slot];
   const int base = st.len[slot];
@@ -221,6 +241,7 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(ToyDev m, Slo
   for (int j = threadIdx.x; j < count; j += blockDim.x)
     d[j] = st.draft[static_cast<int64_t>(slot) * FASER_MAX_SPEC + j];
   for (int l = threadIdx.x; l <= FASER_MAX_LAYERS; l += blockDim.x) failpos[l] = 0u;
+  if (ee) layer_weights(m, lo, hi, sm.wt);
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,7 +259,7 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(ToyDev m, Slo
     if (lane == 0) truth[j] = tj;
     if (ee && ncomm0 + j != exempt) {  // one-round re-entry exemption (sdcore.cpp:118-119)
       for (int l = lo; l < hi; ++l) {
-        if (exit_test<VPL>(m, zf, zn, l, d[j], in->k_table[l]) && lane == 0)
+        if (exit_test<VPL>(m, zf, zn, sm.wt[l].x, sm.wt[l].y, d[j], in->k_table[l]) && lane == 0)
           atomicOr(&failpos[l], 1u << j);
       }
     }
@@ -371,6 +392,32 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(ToyDev m, Slo
   rr->committed = c;
 }
 
+template <int VPL>
+__global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(ToyDev m, SlotState st,
+                                                                   const StepIn* __restrict__ in,
+                                                                   faser_round_result* __restrict__ results) {
+  __shared__ VerifySmem sm;
+  const int p = blockIdx.x;
+  if (p >= in->n_live) return;
+  verify_one<VPL>(m, st, in, p, results, sm);
+}
+
+// One launch per round: block p drafts request p on warp 0 (the other warps wait at the
+// barrier) and then verifies + commits it with all warps — no grid-wide draft/verify boundary,
+// so a request with a short draft starts verifying while others still draft.
+template <int VPL>
+__global__ void __launch_bounds__(kVerifyWarps * 32) draft_verify_kernel(ToyDev m, SlotState st,
+                                                                         const StepIn* __restrict__ in,
+                                                                         faser_round_result* __restrict__ results) {
+  __shared__ VerifySmem sm;
+  __shared__ int32_t dl[FASER_MAX_SPEC];
+  const int p = blockIdx.x;
+  if (p >= in->n_live) return;
+  if (threadIdx.x < 32) draft_one<VPL>(m, st, in, p, dl);
+  __syncthreads();  // the draft (global st.draft / draft_len / mh_at) is visible block-wide
+  verify_one<VPL>(m, st, in, p, results, sm);
+}
+
 // ----------------------------------------------------------------------------- rows
 template <int VPL>
 __global__ void __launch_bounds__(128) rows_kernel(ToyDev m, int op, int n,
@@ -449,6 +496,14 @@ cudaError_t toy_verify_commit(const ToyDev& m, SlotState st, const StepIn* in_de
                               faser_round_result* results, cudaStream_t stream) {
   if (n_live <= 0) return cudaSuccess;
   FASER_VPL_SWITCH(m.vocab, (verify_kernel<VPL><<<n_live, kVerifyWarps * 32, 0, stream>>>(
+                                m, st, in_dev, results)));
+  return cudaGetLastError();
+}
+
+cudaError_t toy_draft_verify_commit(const ToyDev& m, SlotState st, const StepIn* in_dev, int n_live,
+                                    faser_round_result* results, cudaStream_t stream) {
+  if (n_live <= 0) return cudaSuccess;
+  FASER_VPL_SWITCH(m.vocab, (draft_verify_kernel<VPL><<<n_live, kVerifyWarps * 32, 0, stream>>>(
                                 m, st, in_dev, results)));
   return cudaGetLastError();
 }

@@ -92,6 +92,9 @@ cudaError_t toy_draft(const ToyDev& m, SlotState st, const StepIn* in_dev, int n
                       cudaStream_t stream);
 cudaError_t toy_verify_commit(const ToyDev& m, SlotState st, const StepIn* in_dev, int n_live,
                               faser_round_result* results, cudaStream_t stream);
+// draft (warp 0 of block p) + verify + commit of request p in one launch (the engine's step)
+cudaError_t toy_draft_verify_commit(const ToyDev& m, SlotState st, const StepIn* in_dev, int n_live,
+                                    faser_round_result* results, cudaStream_t stream);
 // Row ops for the stateless API: op 0 final_and_noise, 1 target_logits(layers), 2 target_next,
 // 3 draft_next.
 cudaError_t toy_rows(const ToyDev& m, int op, int n, const int32_t* tokens, const int64_t* off,

@@ -126,7 +126,7 @@ def test_engine_episode_matches_reference_golden(golden, name):
         outs, recs, st = serving.run_backlog(eng, prompts, e["out_len"], k_mode=e["k_mode"],
                                              fixed_k=e["fixed_k"], k_seed=e["k_seed"],
                                              gate=abi.GatePlan(8, 32, 1.0))
-        assert eng.kernel_launches() >= 2 * st["rounds"]
+        assert eng.kernel_launches() >= st["rounds"]  # one fused draft+verify+commit launch per round
     assert outs == e["outputs"]
     h = hashlib.sha256()
     for r in recs:
