@@ -1,0 +1,7 @@
+#!/bin/bash
+# round-2 GPU call 69: toy round as a cached CUDA graph per (n_live, n_admit)
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_toy_gpu.py -q -x > gpurun_out/r69_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r69_tests.log
+grep -q "rc=0" gpurun_out/r69_tests.log || exit 3
+FASER_TOY_PROF=1 timeout 300 python bench.py --workload toy --steps 200 --warmup 20 > gpurun_out/r69_toy.json 2> gpurun_out/r69_toy.err
+FASER_TOY_GRAPH=0 FASER_TOY_PROF=1 timeout 300 python bench.py --workload toy --steps 200 --warmup 20 > gpurun_out/r69_toy_nograph.json 2>> gpurun_out/r69_toy.err
