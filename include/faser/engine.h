@@ -280,8 +280,8 @@ faser_status faser_release(faser_engine* e, int64_t req_id);
 /* Number of live + pending requests. */
 int32_t faser_pending_work(const faser_engine* e);
 /* Device time (ms, CUDA events on the engine stream) of the last faser_step: draft lane,
- * verify lane and whole step. (Toy engine: the draft runs fused with verify + commit in one
- * launch, so draft_ms covers the admission kernel and verify_ms the fused round.) */
+ * verify lane and whole step. (Toy engine: admission, draft, verify and commit run as one
+ * launch per round, so draft_ms is 0 and verify_ms is the round.) */
 faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, float* verify_ms,
                                     float* step_ms);
 /* Switches the admission-prefill lane of an engine created with prefill_lane = 1 off (0: the

@@ -179,6 +179,15 @@ struct faser_engine {
   int64_t launches = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   float t_draft = 0.f, t_verify = 0.f, t_step = 0.f;
+  bool t_pending = false;
+  const bool prof_on = std::getenv("FASER_TOY_PROF") != nullptr;
+  void resolve_timing() {
+    if (!t_pending) return;
+    cudaEventElapsedTime(&t_draft, ev[0], ev[1]);
+    cudaEventElapsedTime(&t_verify, ev[1], ev[2]);
+    cudaEventElapsedTime(&t_step, ev[0], ev[2]);
+    t_pending = false;
+  }
 
   struct Req {
     int64_t id;
@@ -189,7 +198,7 @@ struct faser_engine {
     int32_t slot = -1;
     bool done = false;
     bool initialized = false;  // admit kernel enqueued
-    int32_t* d_prompt = nullptr;  // stream-ordered device copy until admitted
+    std::vector<int32_t> prompt;  // host copy until admitted (uploaded inline with that round's StepIn)
   };
   std::unordered_map<int64_t, Req> reqs;
   std::deque<int64_t> pending;
@@ -199,8 +208,6 @@ struct faser_engine {
   ~faser_engine() {
     if (llama) faser::llama_engine_destroy(llama);
     if (stream) cudaStreamSynchronize(stream);
-    for (auto& kv : reqs)
-      if (kv.second.d_prompt) cudaFree(kv.second.d_prompt);
     if (h_in) cudaFreeHost(h_in);
     if (h_res) cudaFreeHost(h_res);
     if (d_in) cudaFree(d_in);
@@ -276,7 +283,7 @@ faser_status faser_engine_create(const faser_model_desc* model, const faser_engi
     // slot rows hold prompt ++ committed plus one round of speculative headroom
     const int row = cfg->max_seq_len + FASER_MAX_SPEC + 2;
     e->slots.alloc(cfg->max_batch, row);
-    const size_t in_cap = StepIn::capacity(cfg->max_batch);
+    const size_t in_cap = StepIn::capacity(cfg->max_batch, static_cast<int64_t>(cfg->max_batch) * cfg->max_seq_len);
     CK(cudaMallocHost(reinterpret_cast<void**>(&e->h_in), in_cap));
     CK(cudaMalloc(reinterpret_cast<void**>(&e->d_in), in_cap));
     CK(cudaMallocHost(&e->h_res, sizeof(faser_round_result) * cfg->max_batch));
@@ -312,11 +319,7 @@ faser_status faser_submit(faser_engine* e, int64_t req_id, const int32_t* prompt
     r.prompt_len = len;
     r.spec_length = e->cfg.default_spec_length;
     r.done = max_out == 0;  // Request::done invariant: |committed| == max_out
-    CK(cudaSetDevice(e->cfg.device));
-    if (!r.done) {
-      CK(cudaMallocAsync(&r.d_prompt, sizeof(int32_t) * len, e->stream));
-      CK(cudaMemcpyAsync(r.d_prompt, prompt, sizeof(int32_t) * len, cudaMemcpyHostToDevice, e->stream));
-    }
+    if (!r.done) r.prompt.assign(prompt, prompt + len);
     r.committed.reserve(max_out);
     e->reqs.emplace(req_id, std::move(r));
     if (max_out > 0) e->pending.push_back(req_id);
@@ -367,9 +370,15 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
     if (cap < n_live) throw Fail{FASER_ECAPACITY, "result capacity smaller than live batch"};
     StepIn& in = *e->h_in;
     const int L = e->toy.layers;
-    int n_admit = 0;
-    for (int p = 0; p < n_live; ++p) n_admit += !e->reqs.at(e->live[p]).initialized;
-    in.layout(n_live, n_admit);
+    int n_admit = 0, n_ptok = 0;
+    for (int p = 0; p < n_live; ++p) {
+      const faser_engine::Req& r = e->reqs.at(e->live[p]);
+      if (!r.initialized) {
+        ++n_admit;
+        n_ptok += r.prompt_len;
+      }
+    }
+    in.layout(n_live, n_admit, n_ptok);
     in.early_exit = e->cfg.mode >= FASER_MODE_VSD_AD_EE ? 1 : 0;
     in.commit = 1;
     in.exempt_rule = e->cfg.exempt_rule;
@@ -386,7 +395,8 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
     } else if (faser_k_table(&e->cfg.exit_policy, L, in.k_table) != FASER_OK) {
       throw Fail{FASER_EINVAL, "invalid exit policy"};
     }
-    int ai = 0;
+    int ai = 0, toff = 0;
+    const int32_t* d_tok = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(e->d_in) + in.off_tok);
     for (int p = 0; p < n_live; ++p) {
       faser_engine::Req& r = e->reqs.at(e->live[p]);
       in.live_slot()[p] = r.slot;
@@ -394,7 +404,11 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
       in.req_id()[p] = r.id;
       if (!r.initialized) {
         AdmitEntry& a = in.admit()[ai++];
-        a.src = r.d_prompt;
+        std::memcpy(in.tok() + toff, r.prompt.data(), sizeof(int32_t) * r.prompt_len);
+        a.src = d_tok + toff;
+        toff += r.prompt_len;
+        std::vector<int32_t>().swap(r.prompt);
+        r.initialized = true;
         a.slot = r.slot;
         a.len = r.prompt_len;
         a.max_out = r.max_out;
@@ -407,31 +421,18 @@ faser_status faser_step(faser_engine* e, const faser_step_plan* plan, faser_roun
     e->d2h_bytes = static_cast<int64_t>(sizeof(faser_round_result)) * n_live;
     SlotState sv = e->slots.view(e->cfg.max_seq_len + FASER_MAX_SPEC + 2);
     CK(cudaEventRecord(e->ev[0], e->stream));
-    if (in.n_admit) {
-      CK(toy_admit(e->m, sv, e->d_in, in.n_admit, e->stream));
-      ++e->launches;
-    }
-    // draft + verify + commit fused per request (one launch); t_draft = admission only
+    // admission + draft + verify + commit fused per request (one launch; t_draft = 0)
     CK(cudaEventRecord(e->ev[1], e->stream));
     CK(toy_draft_verify_commit(e->m, sv, e->d_in, n_live, e->d_res, e->stream));
     CK(cudaEventRecord(e->ev[2], e->stream));
     e->launches += 1;
     CK(cudaMemcpyAsync(e->h_res, e->d_res, sizeof(faser_round_result) * n_live,
                        cudaMemcpyDeviceToHost, e->stream));
-    for (int p = 0; p < n_live; ++p) {
-      faser_engine::Req& r = e->reqs.at(e->live[p]);
-      if (!r.initialized) {
-        r.initialized = true;
-        CK(cudaFreeAsync(r.d_prompt, e->stream));
-        r.d_prompt = nullptr;
-      }
-    }
     const auto q1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(e->stream));
     const auto q2 = std::chrono::steady_clock::now();
-    cudaEventElapsedTime(&e->t_draft, e->ev[0], e->ev[1]);
-    cudaEventElapsedTime(&e->t_verify, e->ev[1], e->ev[2]);
-    cudaEventElapsedTime(&e->t_step, e->ev[0], e->ev[2]);
+    e->t_pending = true;  // resolved on demand (faser_last_step_timing): three driver calls per round
+    if (e->prof_on) e->resolve_timing();
     std::vector<int64_t> keep;
     keep.reserve(n_live);
     for (int p = 0; p < n_live; ++p) {
@@ -510,6 +511,7 @@ faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, floa
     faser::llama_last_step_timing(e->llama, draft_ms, verify_ms, step_ms);
     return FASER_OK;
   }
+  const_cast<faser_engine*>(e)->resolve_timing();
   if (draft_ms) *draft_ms = e->t_draft;
   if (verify_ms) *verify_ms = e->t_verify;
   if (step_ms) *step_ms = e->t_step;

@@ -101,25 +101,22 @@ __device__ __forceinline__ int argmax_of(const ToyDev& m, const double (&z)[VPL]
 // prune iff #{v : z[v] > z[d] or (z[v] == z[d] and v < d)} >= k.
 // w = layer / L and 1 - w come from a per-block table (layer_weights): the same correctly
 // rounded quotient target_logits forms (toylm.cpp:60), computed once instead of per row.
+// z[d] is formed by every lane from the row's (zf[d], zn[d]) (broadcast once per row) with the
+// same rounded operations lane d % 32 applies to its own entry, so it is bit-identical to it;
+// the count is one ballot per vocab stripe.
 template <int VPL>
-__device__ __forceinline__ bool exit_test(const ToyDev& m, const double (&zf)[VPL],
-                                          const double (&zn)[VPL], double w, double omw, int d, int k) {
+__device__ __forceinline__ bool exit_test(const ToyDev& m, const double (&zf)[VPL], const double (&zn)[VPL],
+                                          double zf_d, double zn_d, double w, double omw, int d, int k) {
   const int lane = threadIdx.x & 31;
-  double z[VPL];
-  double zsel = 0.0;
-#pragma unroll
-  for (int q = 0; q < VPL; ++q) {
-    z[q] = __dadd_rn(__dmul_rn(w, zf[q]), __dmul_rn(omw, zn[q]));
-    if (q == (d >> 5)) zsel = z[q];
-  }
-  const double ref = __shfl_sync(kFull, zsel, d & 31);
+  const double ref = __dadd_rn(__dmul_rn(w, zf_d), __dmul_rn(omw, zn_d));
   int cnt = 0;
 #pragma unroll
   for (int q = 0; q < VPL; ++q) {
     const int t = lane + 32 * q;
-    cnt += (t < m.vocab) && (z[q] > ref || (z[q] == ref && t < d));
+    const double z = __dadd_rn(__dmul_rn(w, zf[q]), __dmul_rn(omw, zn[q]));
+    cnt += __popc(__ballot_sync(kFull, (t < m.vocab) && (z > ref || (z == ref && t < d))));
   }
-  return __reduce_add_sync(kFull, static_cast<unsigned>(cnt)) >= static_cast<unsigned>(k);
+  return cnt >= k;
 }
 // tab[l] = (l / L, 1 - l / L) for l in [lo, hi), by the block's threads (needs a __syncthreads)
 __device__ __forceinline__ void layer_weights(const ToyDev& m, int lo, int hi, double2* tab) {
@@ -132,11 +129,8 @@ __device__ __forceinline__ void layer_weights(const ToyDev& m, int lo, int hi, d
 // ----------------------------------------------------------------------------- admit
 // One warp per admitted request: copy its context into the slot row and fold the running
 // hash states hash_tokens(noise_seed, ctx) / hash_tokens(mix_seed, ctx) (rng.hpp:28-32).
-__global__ void admit_kernel(ToyDev m, SlotState st, const StepIn* __restrict__ in) {
-  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__device__ __forceinline__ void admit_one(const ToyDev& m, SlotState st, const AdmitEntry& a) {
   const int lane = threadIdx.x & 31;
-  if (e >= in->n_admit) return;
-  const AdmitEntry a = in->admit()[e];
   const int32_t* src = a.src;
   int32_t* row = st.tok + static_cast<int64_t>(a.slot) * st.max_seq;
   for (int i = lane; i < a.len; i += 32) row[i] = src[i];
@@ -153,6 +147,12 @@ __global__ void admit_kernel(ToyDev m, SlotState st, const StepIn* __restrict__ 
     st.done[a.slot] = 0;
     st.exempt[a.slot] = a.exempt;
   }
+}
+
+__global__ void admit_kernel(ToyDev m, SlotState st, const StepIn* __restrict__ in) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= in->n_admit) return;
+  admit_one(m, st, in->admit()[e]);
 }
 
 // ----------------------------------------------------------------------------- draft
@@ -258,8 +258,19 @@ __device__ __forceinline__ void verify_one(const ToyDev& m, SlotState st, const 
     const int tj = argmax_of<VPL>(m, zf);
     if (lane == 0) truth[j] = tj;
     if (ee && ncomm0 + j != exempt) {  // one-round re-entry exemption (sdcore.cpp:118-119)
+      const int dj = d[j];
+      double zf_d = zf[0], zn_d = zn[0];
+#pragma unroll
+      for (int q = 1; q < VPL; ++q)
+        if (q == (dj >> 5)) {
+          zf_d = zf[q];
+          zn_d = zn[q];
+        }
+      zf_d = __shfl_sync(kFull, zf_d, dj & 31);
+      zn_d = __shfl_sync(kFull, zn_d, dj & 31);
+#pragma unroll 2
       for (int l = lo; l < hi; ++l) {
-        if (exit_test<VPL>(m, zf, zn, sm.wt[l].x, sm.wt[l].y, d[j], in->k_table[l]) && lane == 0)
+        if (exit_test<VPL>(m, zf, zn, zf_d, zn_d, sm.wt[l].x, sm.wt[l].y, dj, in->k_table[l]) && lane == 0)
           atomicOr(&failpos[l], 1u << j);
       }
     }
@@ -402,8 +413,8 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) verify_kernel(ToyDev m, Slo
   verify_one<VPL>(m, st, in, p, results, sm);
 }
 
-// One launch per round: block p drafts request p on warp 0 (the other warps wait at the
-// barrier) and then verifies + commits it with all warps — no grid-wide draft/verify boundary,
+// One launch per round: block p admits (when new) and drafts request p on warp 0 (the other
+// warps wait at the barrier) and then verifies + commits it with all warps — no grid-wide draft/verify boundary,
 // so a request with a short draft starts verifying while others still draft.
 template <int VPL>
 __global__ void __launch_bounds__(kVerifyWarps * 32) draft_verify_kernel(ToyDev m, SlotState st,
@@ -413,7 +424,14 @@ __global__ void __launch_bounds__(kVerifyWarps * 32) draft_verify_kernel(ToyDev 
   __shared__ int32_t dl[FASER_MAX_SPEC];
   const int p = blockIdx.x;
   if (p >= in->n_live) return;
-  if (threadIdx.x < 32) draft_one<VPL>(m, st, in, p, dl);
+  if (threadIdx.x < 32) {
+    // a request admitted this round: its slot state first (admit_kernel's work, same warp)
+    const int slot = in->live_slot()[p];
+    for (int e = 0; e < in->n_admit; ++e)
+      if (in->admit()[e].slot == slot) admit_one(m, st, in->admit()[e]);
+    __syncwarp();
+    draft_one<VPL>(m, st, in, p, dl);
+  }
   __syncthreads();  // the draft (global st.draft / draft_len / mh_at) is visible block-wide
   verify_one<VPL>(m, st, in, p, results, sm);
 }

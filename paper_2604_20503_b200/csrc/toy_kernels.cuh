@@ -55,6 +55,7 @@ struct StepIn {
   int32_t exempt_rule;
   int32_t total_bytes;
   int32_t off_live_slot, off_k, off_req_id, off_admit;  // byte offsets from `this`
+  int32_t off_tok;  // admitted prompts, concatenated (AdmitEntry::src may point here on the device)
   int32_t k_table[FASER_MAX_LAYERS + 1];
 
   __host__ __device__ const char* base() const { return reinterpret_cast<const char*>(this); }
@@ -67,9 +68,10 @@ struct StepIn {
   __host__ __device__ int32_t* k() { return reinterpret_cast<int32_t*>(base() + off_k); }
   __host__ __device__ int64_t* req_id() { return reinterpret_cast<int64_t*>(base() + off_req_id); }
   __host__ __device__ AdmitEntry* admit() { return reinterpret_cast<AdmitEntry*>(base() + off_admit); }
+  __host__ __device__ int32_t* tok() { return reinterpret_cast<int32_t*>(base() + off_tok); }
 
-  // Lays out the arrays for (n_live, n_admit); returns total bytes.
-  __host__ int32_t layout(int32_t live, int32_t admits) {
+  // Lays out the arrays for (n_live, n_admit, prompt tokens carried inline); returns total bytes.
+  __host__ int32_t layout(int32_t live, int32_t admits, int32_t tokens = 0) {
     auto al = [](int32_t x, int32_t a) { return (x + a - 1) / a * a; };
     n_live = live;
     n_admit = admits;
@@ -77,11 +79,13 @@ struct StepIn {
     off_k = off_live_slot + 4 * live;
     off_req_id = al(off_k + 4 * live, 8);
     off_admit = al(off_req_id + 8 * live, 16);
-    total_bytes = off_admit + static_cast<int32_t>(sizeof(AdmitEntry)) * admits;
+    off_tok = al(off_admit + static_cast<int32_t>(sizeof(AdmitEntry)) * admits, 16);
+    total_bytes = off_tok + 4 * tokens;
     return total_bytes;
   }
-  static constexpr size_t capacity(int32_t max_live) {
-    return sizeof(StepIn) + 64 + static_cast<size_t>(max_live) * (4 + 4 + 8 + sizeof(AdmitEntry));
+  static constexpr size_t capacity(int32_t max_live, int64_t max_tokens = 0) {
+    return sizeof(StepIn) + 96 + static_cast<size_t>(max_live) * (4 + 4 + 8 + sizeof(AdmitEntry)) +
+           4 * static_cast<size_t>(max_tokens);
   }
 };
 
