@@ -66,6 +66,20 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// cluster-pair split (GROUP mode): the two halves of a (request, kv head) merge through DSMEM
+__device__ __forceinline__ void pair_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sm100::smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_peer(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -91,7 +105,8 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
                                                    const __nv_bfloat16* __restrict__ qbuf,
                                                    __nv_bfloat16* __restrict__ obuf, float* __restrict__ part_o,
                                                    float2* __restrict__ part_ml, int* __restrict__ counters,
-                                                   int n_split, int rows_cap, int n_blocks, float scale_log2) {
+                                                   int n_split, int rows_cap, int n_blocks, float scale_log2,
+                                                   int pair) {
   constexpr int kStages = kAttnStages<HD>;
   constexpr int kChunks = HD / 8;          // 16-byte chunks per K/V row
   constexpr int kTileBytes = 64 * HD * 2;  // one K (or V) page
@@ -114,6 +129,8 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   const int gm = (1 << gs) - 1;
   const int G = 1 << gs;
   const int M = nr << gs;
+  // pair (cluster of 2 along z, GROUP mode): rank sp walks half of the pages (n_split = 2 page
+  // ranges) and rank 0 merges both halves from shared memory (no global partials / counters)
   const int blk = blockIdx.z / n_split, sp = blockIdx.z % n_split;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NT = 128 * MT;  // threads
@@ -419,6 +436,39 @@ __global__ void __launch_bounds__(128 * MT) attn_kernel(const __grid_constant__ 
   // each (packed row, dim) of this CTA: combine its warps -> final (n_split == 1) or partial
   const int ntiles = ROWS ? 4 : MT;
   const int wpt = ROWS ? 1 : nkg;  // warps per tile
+  if (!ROWS && pair) {
+    pair_sync();  // both halves' per-warp (m, l, O) are in their shared memory
+    if (sp == 0) {
+      const uint32_t p_so = peer_addr(so, 1), p_sm = peer_addr(sm, 1), p_sl = peer_addr(sl_, 1);
+      for (int e = threadIdx.x; e < ntiles * 16 * HD; e += NT) {
+        const int tl = e / (16 * HD), r = (e / HD) % 16, col = e % HD;
+        const int m = cta_m0 + tl * 16 + r;
+        if (m >= cta_m1) continue;
+        float mm = kNegBig;
+        for (int g = 0; g < wpt; ++g) {
+          const int w = tl * 4 + g;
+          mm = fmaxf(mm, fmaxf(sm[w * 16 + r], ld_peer(p_sm + 4u * (w * 16 + r))));
+        }
+        float l = 0.f, acc = 0.f;
+        for (int g = 0; g < wpt; ++g) {  // this half's warps, then the peer's (fixed order)
+          const int w = tl * 4 + g;
+          const float f = exp2f(sm[w * 16 + r] - mm);
+          l += sl_[w * 16 + r] * f;
+          acc += so[(w * 16 + r) * HD + col] * f;
+        }
+        for (int g = 0; g < wpt; ++g) {
+          const int w = tl * 4 + g;
+          const float f = exp2f(ld_peer(p_sm + 4u * (w * 16 + r)) - mm);
+          l += ld_peer(p_sl + 4u * (w * 16 + r)) * f;
+          acc += ld_peer(p_so + 4u * ((w * 16 + r) * HD + col)) * f;
+        }
+        const int row = first + (m >> gs), head = kvh * G + (m & gm);
+        obuf[(static_cast<int64_t>(row) * n_q + head) * HD + col] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
+      }
+    }
+    pair_sync();  // rank 1's shared memory stays alive until rank 0 has read it
+    return;
+  }
   for (int e = threadIdx.x; e < ntiles * 16 * HD; e += NT) {
     const int tl = e / (16 * HD), r = (e / HD) % 16, col = e % HD;
     const int m = cta_m0 + tl * 16 + r;
@@ -509,7 +559,8 @@ bool want_tma_env() {  // TMA page loads unless FASER_ATTN_TMA=0
 template <int HD, bool ROWS, int MT = 1, int PPS = 1>
 cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int n_split, KvDev kv,
                    int layer, const __nv_bfloat16* qbuf, __nv_bfloat16* obuf, float* part_o,
-                   float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s) {
+                   float2* part_ml, int* counters, int rows_cap, float scale_log2, cudaStream_t s,
+                   int pair = 0) {
   constexpr int kTile = 64 * HD * 2;
   constexpr int kMerge = (4 * MT * 16 * HD + 128 * MT) * 4;
   constexpr int kSmem = (PPS * 2 * kAttnStages<HD> * kTile > kMerge ? PPS * 2 * kAttnStages<HD> * kTile : kMerge) + 1024;
@@ -523,9 +574,26 @@ cudaError_t launch(const LlamaShape& m, RowsDev rows, int n_req, int blocks, int
   // cp.async path): the default whenever the pool has a TMA view (FASER_ATTN_TMA=0: cp.async)
   static const bool want_tma = want_tma_env();
   const bool use_tma = want_tma && kv.tma != nullptr && PPS == 1;
+  if (pair) {  // a cluster of two CTAs per (request, kv head, block): n_split = 2 page halves
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_req, m.n_kv, blocks * 2);
+    cfg.blockDim = dim3(128 * MT, 1, 1);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 2;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, attn_kernel<HD, ROWS, MT, PPS>, use_tma ? *kv.tma : dummy, use_tma ? 1 : 0, rows,
+                              kv, layer, m.n_q, m.n_kv, qbuf, obuf, part_o, part_ml, counters, 2, rows_cap, blocks,
+                              scale_log2, 1);
+  }
   attn_kernel<HD, ROWS, MT, PPS><<<grid, 128 * MT, kSmem, s>>>(use_tma ? *kv.tma : dummy, use_tma ? 1 : 0, rows, kv, layer,
                                                           m.n_q, m.n_kv, qbuf, obuf, part_o, part_ml, counters,
-                                                          n_split, rows_cap, blocks, scale_log2);
+                                                          n_split, rows_cap, blocks, scale_log2, 0);
   return cudaGetLastError();
 }
 
@@ -577,6 +645,12 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
     return lm_attention_tc(m, rows, n_req, max_rows_per_req, kv, layer, qbuf, obuf, s);
   if (rows_mode && attn_tc_rows_applies(m, max_ctx, kv))
     return lm_attention_tc(m, rows, n_req, max_rows_per_req, kv, layer, qbuf, obuf, s);
+  // cluster-pair split for GROUP rows (two CTAs per (request, kv head) walk half the pages each
+  // and merge through DSMEM, no global partials) when the doubled grid still leaves every CTA its
+  // own SM: two CTAs sharing an SM slow each other's instruction-bound page walk
+  // (profiles/r02_attn_pair_split.txt; FASER_ATTN_PAIR = minimum pages, 0 = off)
+  static const int pair_min = getenv("FASER_ATTN_PAIR") ? atoi(getenv("FASER_ATTN_PAIR")) : 6;
+  const int pair = (!rows_mode && n_split == 1 && pair_min > 0 && tiles >= pair_min && 2 * base <= target) ? 1 : 0;
   const size_t per_split = static_cast<size_t>(rows_cap) * m.n_q * (m.hd * 4 + 8);
   while (n_split > 1 && per_split * n_split > body_bytes) --n_split;
   float* part_o = body;
@@ -587,15 +661,15 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
     // two-page steps (PPS = 2, FASER_ATTN_WIDE=1)
     static const bool wide = getenv("FASER_ATTN_WIDE") && getenv("FASER_ATTN_WIDE")[0] == '1';
     if (wide && !(want_tma_env() && kv.tma)) {
-      if (mt == 2) return launch<64, false, 2, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
-      return launch<64, false, 1, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+      if (mt == 2) return launch<64, false, 2, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s, pair);
+      return launch<64, false, 1, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s, pair);
     }
-    if (mt == 2) return launch<64, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
-    return launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+    if (mt == 2) return launch<64, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s, pair);
+    return launch<64, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s, pair);
   }
   if (rows_mode) return launch<128, true>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
-  if (mt == 2) return launch<128, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
-  return launch<128, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s);
+  if (mt == 2) return launch<128, false, 2>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s, pair);
+  return launch<128, false>(m, rows, n_req, blocks, n_split, kv, layer, qbuf, obuf, part_o, part_ml, counters, rows_cap, scale_log2, s, pair);
 }
 
 }  // namespace faser

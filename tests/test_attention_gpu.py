@@ -67,7 +67,7 @@ BATCH_CTX = [4, 63, 64, 65, 127, 128, 129, 191, 192, 193, 255, 256, 257, 600, 64
 
 
 @pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (12, 12, 64), (32, 8, 128), (8, 8, 128)])
-@pytest.mark.parametrize("shape", ["decode", "verify", "prefill", "ragged", "batch", "long"])
+@pytest.mark.parametrize("shape", ["decode", "verify", "prefill", "ragged", "batch", "long", "pair"])
 def test_attention_matches_fp32(L, n_q, n_kv, hd, shape):
     rows, ctx = {
         "decode": ([1] * 6, [1, 63, 64, 65, 300, 1000]),
@@ -76,6 +76,7 @@ def test_attention_matches_fp32(L, n_q, n_kv, hd, shape):
         "ragged": ([2, 70, 1, 16], [2, 900, 129, 16]),
         "batch": (BATCH_ROWS, BATCH_CTX),
         "long": ([4, 4, 1], [1600, 2000, 1800]),  # few units, long contexts: the split-KV path
+        "pair": ([4] * 8, [600, 700, 400, 690, 500, 640, 385, 650]),  # cluster-pair split (DSMEM merge)
     }[shape]
     if shape == "batch" and n_q // n_kv * max(rows) > 64:
         rows = [min(r, 64 // (n_q // n_kv)) for r in rows]
