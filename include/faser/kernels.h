@@ -30,6 +30,10 @@ faser_status faser_k_gemm_bf16_plan(const void* w, const void* x, float* out, in
 /* The launch plan the engine uses for an [n_out x k] weight and t rows: out = {bn, splits, mc,
  * deep}. Host-only (no device needed). */
 faser_status faser_k_gemm_plan(int32_t n_out, int32_t t, int32_t k, int32_t* out4);
+/* The sweep-driven planner's plan for the same shape (out4 as above; score = the pick's mean log
+ * slowdown on its two nearest measured shapes), whatever FASER_GEMM_PLAN selects for the engine
+ * (tc_gemm.cu gemm_plan_table; CPU-callable). */
+faser_status faser_k_gemm_plan_table(int32_t n_out, int32_t t, int32_t k, int32_t* out4, double* score);
 /* faser_k_gemm_bf16_plan with a per-CTA timeline: trace[cta][8] globaltimer stamps (entry, after
  * griddepcontrol.wait, first stage landed, accumulators complete, split-K reduced, exit); the
  * grid is (weight tiles / mc, row tiles, splits), cta = (z * gy + y) * gx + x. */

@@ -28,7 +28,7 @@ def _stale(target, deps):
 
 def build_product(force=False, verbose=False):
     srcs = _sources()
-    deps = srcs + glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + glob.glob(
+    deps = srcs + glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + glob.glob(os.path.join(PKG, "csrc", "*.inc")) + glob.glob(
         os.path.join(ROOT, "include", "faser", "*.h"))
     if not force and not _stale(LIB, deps):
         return LIB

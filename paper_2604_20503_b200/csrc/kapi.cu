@@ -84,6 +84,16 @@ extern "C" faser_status faser_k_gemm_bf16_trace(const void* w, const void* x, fl
   return e == cudaSuccess ? FASER_OK : FASER_ECUDA;
 }
 
+extern "C" faser_status faser_k_gemm_plan_table(int32_t n_out, int32_t t, int32_t k, int32_t* out4, double* score) {
+  if (!out4 || n_out <= 0 || n_out % 128 || t <= 0 || k <= 0 || k % 64) return FASER_EINVAL;
+  const GemmPlan p = gemm_plan_table(n_out, t, k, score);
+  out4[0] = p.bn;
+  out4[1] = p.splits;
+  out4[2] = p.mc;
+  out4[3] = p.deep ? 1 : 0;
+  return FASER_OK;
+}
+
 extern "C" faser_status faser_k_gemm_plan(int32_t n_out, int32_t t, int32_t k, int32_t* out4) {
   if (!out4 || n_out <= 0 || n_out % 128 || t <= 0 || k <= 0 || k % 64) return FASER_EINVAL;
   int n = 0, dev = 0;

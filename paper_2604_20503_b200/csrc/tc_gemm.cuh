@@ -85,6 +85,9 @@ struct GemmPlan {
   int mc = 1;        // 128-row weight tiles per CTA sharing one rows tile (1, 2, 4)
 };
 GemmPlan gemm_plan(int n_out, int t, int k, int num_sms);
+// Sweep-driven plan (tc_gemm.cu, plan_table.inc); score (optional) = the pick's mean log slowdown
+// on its nearest measured shapes.
+GemmPlan gemm_plan_table(int n_out, int t, int k, double* score);
 // Plan for a prefill forward (one or a few prompts, 128..8192 rows, no logits): 128-row token
 // tiles from 256 rows up (the same-shape sweep's winners, which did not survive in the verify
 // stream but are measured here on prefill separately).
