@@ -67,7 +67,7 @@ BATCH_CTX = [4, 63, 64, 65, 127, 128, 129, 191, 192, 193, 255, 256, 257, 600, 64
 
 
 @pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (12, 12, 64), (32, 8, 128), (8, 8, 128)])
-@pytest.mark.parametrize("shape", ["decode", "verify", "prefill", "ragged", "batch", "long", "pair"])
+@pytest.mark.parametrize("shape", ["decode", "verify", "prefill", "ragged", "batch", "long", "pair", "decode_long"])
 def test_attention_matches_fp32(L, n_q, n_kv, hd, shape):
     rows, ctx = {
         "decode": ([1] * 6, [1, 63, 64, 65, 300, 1000]),
@@ -77,13 +77,14 @@ def test_attention_matches_fp32(L, n_q, n_kv, hd, shape):
         "batch": (BATCH_ROWS, BATCH_CTX),
         "long": ([4, 4, 1], [1600, 2000, 1800]),  # few units, long contexts: the split-KV path
         "pair": ([4] * 8, [600, 700, 400, 690, 500, 640, 385, 650]),  # cluster-pair split (DSMEM merge)
+        "decode_long": ([1] * 5, [1, 64, 257, 1300, 2000]),  # one row per request, 1..2000 keys
     }[shape]
     if shape == "batch" and n_q // n_kv * max(rows) > 64:
         rows = [min(r, 64 // (n_q // n_kv)) for r in rows]
     run_case(L, n_q, n_kv, hd, rows, ctx, seed=n_q + hd)
 
 
-@pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (32, 8, 128)])
+@pytest.mark.parametrize("n_q,n_kv,hd", [(32, 4, 64), (32, 8, 128), (12, 12, 64)])
 @pytest.mark.parametrize("kernels", ["tcgen05", "mma_sync"])
 def test_attention_dispatch_variants(n_q, n_kv, hd, kernels):
     """The non-default dispatches (env read once per process, so in a subprocess): tcgen05 for
@@ -92,7 +93,8 @@ def test_attention_dispatch_variants(n_q, n_kv, hd, kernels):
     import os
     import subprocess
     import sys
-    env = {"tcgen05": {"FASER_ATTN_TC": "1"}, "mma_sync": {"FASER_ATTN_TC": "0", "FASER_ATTN_TC_ROWS": "0"}}[kernels]
+    env = {"tcgen05": {"FASER_ATTN_TC": "1"},
+           "mma_sync": {"FASER_ATTN_TC": "0", "FASER_ATTN_TC_ROWS": "0"}}[kernels]
     code = ("import sys; sys.path.insert(0, 'tests'); import test_attention_gpu as t; "
             "from paper_2604_20503_b200 import engine; L = engine.lib(); "
             f"t.run_case(L, {n_q}, {n_kv}, {hd}, t.BATCH_ROWS, t.BATCH_CTX, seed=5); "
