@@ -426,6 +426,10 @@ void faser_drafter_default_cfg(faser_drafter_cfg* out);
 faser_status faser_drafter_create(const faser_drafter_cfg* cfg, const faser_latency_model* models,
                                   faser_drafter** out);
 void faser_drafter_destroy(faser_drafter* d);
+/* Installs refreshed stage-latency models (the online profiler's periodic refit, PAPER.md:575
+ * "refreshed every two hours in a separate process using runtime execution statistics"); the
+ * GP windows and acceptance books are kept. */
+faser_status faser_drafter_set_models(faser_drafter* d, const faser_latency_model* models);
 /* AdaptiveDrafter::assign_lengths (drafter.cpp:175-207) for the batch (req_ids[n]), batch size
  * b and draft SM share r -> k_out[n]. */
 faser_status faser_drafter_assign(faser_drafter* d, const int64_t* req_ids, int32_t n, int32_t b,

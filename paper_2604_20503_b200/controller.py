@@ -39,6 +39,10 @@ class AdaptiveDrafter:
 
     __del__ = close
 
+    def set_models(self, models):
+        """Installs refreshed stage-latency models (profiler.OnlineProfiler) for later rounds."""
+        _check(lib().faser_drafter_set_models(self.h, C.byref(models)))
+
     def assign_lengths(self, req_ids, b, r):
         ids = np.ascontiguousarray(req_ids, np.int64)
         out = np.zeros(max(len(ids), 1), np.int32)

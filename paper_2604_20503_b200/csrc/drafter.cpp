@@ -270,6 +270,12 @@ faser_status faser_drafter_create(const faser_drafter_cfg* cfg, const faser_late
 
 void faser_drafter_destroy(faser_drafter* d) { delete d; }
 
+faser_status faser_drafter_set_models(faser_drafter* d, const faser_latency_model* models) {
+  if (!d || !models) return FASER_EINVAL;
+  d->models = *models;
+  return FASER_OK;
+}
+
 double faser_drafter_beta(const faser_drafter_cfg* cfg, int32_t round) {
   return beta_of(cfg ? cfg->n_candidates : 8, round);
 }

@@ -97,12 +97,16 @@ class ModeController:
     r in (0,1)); FULL = + the overlap plan (plan_overlap, overlap.cpp:23-42). ``gate_layer`` > 0
     replaces make_gate_plan by a fixed single gated layer; ``chunk`` > 0 forces the overlap chunk."""
 
-    def __init__(self, mode, num_layers, fixed_k=4, models=None, gate_layer=0, chunk=0):
+    def __init__(self, mode, num_layers, fixed_k=4, models=None, gate_layer=0, chunk=0, profiler=None):
         from . import controller, engine
         self.mode, self.L, self.k, self.models = mode, num_layers, fixed_k, models
         self.gate_layer, self.chunk = gate_layer, chunk
         self.engine = engine
         self.drafter = controller.AdaptiveDrafter(models=models) if mode >= abi.MODE_VSD_AD else None
+        # online profiler (profiler.OnlineProfiler): runtime stage samples -> periodic refit of
+        # the latency models used below (PAPER.md:575)
+        self.profiler = profiler
+        self.ee_layers = 0
         self.overlap_on = False
         self.r = 1.0  # draft-lane SM share of the plan in force (1.0 = serial, overlap.hpp:14)
 
@@ -113,14 +117,17 @@ class ModeController:
         if self.mode >= abi.MODE_VSD_AD_EE:
             if self.gate_layer:
                 eng.set_gate(abi.GatePlan(self.gate_layer, self.gate_layer + 1, 1.0))
+                self.ee_layers = 1
             else:
                 # GateEntry.accept_estimate from the AcceptanceBook (drafter.cpp:151-161); the
                 # gate's r is the draft share of the overlap plan, 0.5 when serial because
                 # should_prune needs r in (0,1) (latmodel.cpp:45)
                 a_hat = self.drafter.estimate(live, ks, b, self.r)
                 r_gate = self.r if 0.0 < self.r < 1.0 else 0.5
-                eng.set_gate(self.engine.make_gate_plan(abi.ExitPolicy.default(), list(zip(ks, a_hat)),
-                                                        float(b), r_gate, self.L, self.models))
+                gp = self.engine.make_gate_plan(abi.ExitPolicy.default(), list(zip(ks, a_hat)),
+                                                float(b), r_gate, self.L, self.models)
+                eng.set_gate(gp)
+                self.ee_layers = max(0, min(gp.stop_layer, self.L) - gp.first_layer)
         self.overlap_on = False
         if self.mode == abi.MODE_FULL:
             if self.chunk:
@@ -134,13 +141,28 @@ class ModeController:
         self.r = float(eng.plan.overlap.r) if self.overlap_on else 1.0
         return ks
 
-    def observe(self, res, b, step_ms):
+    def observe(self, res, b, step_ms, ks=None, draft_ms=0.0, verify_ms=0.0):
         if self.drafter:
             self.drafter.observe_results(res, b, getattr(self, "r_used", 1.0), max(step_ms, 1e-3))
+        if self.profiler is not None and ks is not None:
+            serial = not self.overlap_on
+            self.profiler.record(b, ks, draft_ms, verify_ms, 1.0 if serial else self.r_used, self.ee_layers)
+            m = self.profiler.poll()
+            if m is not None:
+                self.install_models(m)
+
+    def install_models(self, models):
+        """A refreshed latency model: the drafter's GP-LCB objective, the Eq.10 gate and the
+        overlap planner use it from the next iteration on."""
+        self.models = models
+        if self.drafter:
+            self.drafter.set_models(models)
 
     def close(self):
         if self.drafter:
             self.drafter.close()
+        if self.profiler is not None:
+            self.profiler.close()
 
 
 MODE_NAMES = {abi.MODE_VSD: "VSD", abi.MODE_VSD_AD: "VSD_AD", abi.MODE_VSD_AD_EE: "VSD_AD_EE", abi.MODE_FULL: "FULL"}
@@ -196,7 +218,7 @@ def run_trace(eng: ServingEngine, trace, vocab, prompt_seed=1, fixed_k=4, id_of=
         d_ms, v_ms, s_ms = eng.last_step_timing()
         dt = s_ms if clock == "device" else (time.perf_counter() - w0) * 1e3
         if controller is not None:
-            controller.observe(res, len(live), s_ms)
+            controller.observe(res, len(live), s_ms, ks=ks, draft_ms=d_ms, verify_ms=v_ms)
             S.overlap_iterations += int(controller.overlap_on)
         t_clock += dt
         steps += 1

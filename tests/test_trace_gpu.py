@@ -1,6 +1,8 @@
 """GPU tier: arrival-trace replay (the missing serving loop) over the Llama
 path — bursty sine_segments arrivals (workload.cpp:73-114), iteration-boundary admission,
 every request completes and every output is the target's greedy decode (lossless)."""
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -64,3 +66,33 @@ def test_ablation_ladder_tiny(tmp_path):
     metrics.write_summary_csv(p, sums)
     rows = p.read_text().splitlines()
     assert [r.split(",")[0] for r in rows[1:]] == ["VSD", "VSD_AD", "VSD_AD_EE", "FULL"]
+
+
+@pytest.mark.gpu
+def test_online_profiler_refreshes_during_trace():
+    """The online profiler (profiler.OnlineProfiler) refits the stage-latency
+    models from the engine's own per-step device timings while the trace is served, and the
+    ModeController installs each refit in the AdaptiveDrafter; outputs stay the lossless ones."""
+    from paper_2604_20503_b200 import profiler
+    desc = llama.tiny()
+    V, L = desc.target.vocab, desc.target.layers
+    trace = serving.synth_trace(mean_rate_per_s=300.0, peak_to_valley=4.0, duration_ms=60.0, steps=4,
+                                in_range=(4, 20), out_range=(8, 24), seed=3)
+    outs = []
+    for online in (False, True):
+        with engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=96, mode=abi.MODE_VSD_AD, default_spec_length=4,
+                                  max_spec_length=16, prefill_rows=512) as eng:
+            m0 = abi.LatencyModel()
+            engine.lib().faser_default_latency_model(ctypes.byref(m0))
+            prof = profiler.OnlineProfiler(m0, prior=[], period_steps=6, min_buckets=3) if online else None
+            ctl = serving.ModeController(abi.MODE_VSD_AD, L, models=m0, profiler=prof)
+            m = serving.run_trace(eng, trace, V, controller=ctl, num_layers=L)
+            if online:
+                prof.flush()
+                assert prof.refreshes >= 1, "no refit from the runtime samples"
+                assert ctl.models is not m0
+                assert all(h["mape"].get("draft", 0.0) < 1.0 for h in prof.history)
+            ctl.close()
+            outs.append([eng.committed(j) for j in range(len(trace))])
+        assert m["completed"] == len(trace)
+    assert outs[1] == outs[0]

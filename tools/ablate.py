@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--out-range", default="64,256")
     ap.add_argument("--out", default="gpurun_out/ablation")
     ap.add_argument("--modes", default="VSD,VSD_AD,VSD_AD_EE,FULL")
+    ap.add_argument("--refresh-steps", type=int, default=0,
+                    help="online profiler: refit the latency models from runtime samples every N steps (0 = off)")
     args = ap.parse_args()
     desc = llama.PRESETS[args.workload]()
     V, L = desc.target.vocab, desc.target.layers
@@ -46,9 +48,16 @@ def main():
                 eng.submit(10 ** 9 + i, [1 + i, 2, 3, 4, 5], 8)
             while eng.pending_work() > 0:
                 eng.step()
+            prof = None
+            if args.refresh_steps and models is not None:
+                from paper_2604_20503_b200 import profiler
+                prof = profiler.OnlineProfiler(models, period_steps=args.refresh_steps)
             ctl = serving.ModeController(mode, L, fixed_k=args.k, models=models, gate_layer=args.gate_layer,
-                                         chunk=args.chunk)
+                                         chunk=args.chunk, profiler=prof)
             m = serving.run_trace(eng, trace, V, prompt_seed=1, controller=ctl, num_layers=L, seed=1)
+            if prof is not None:
+                print(json.dumps({"mode": mode, "online_refits": prof.refreshes, "history": prof.history[-3:]}),
+                      flush=True)
             ctl.close()
         s = m["summary"]
         summaries.append(s)

@@ -50,34 +50,10 @@ for b in ([] if REFIT else B_GRID):
 
 
 def fit(samples):
-    def lstsq(rows, y):
-        c, *_ = np.linalg.lstsq(np.array(rows, float), np.array(y, float), rcond=None)
-        return c
-
-    vs = [x for x in samples if x["mode"] == "vsd"]
-    ee = {(x["b"], x["s"]): x["verify_ms"] for x in samples if x["mode"] == "ee"}
-    cd = lstsq([[x["b"], x["s"], 1.0] for x in vs], [x["draft_ms"] for x in vs])
-    if cd[2] < 0:  # keep every prediction positive (eval_latency > 0): refit without intercept
-        c2 = lstsq([[x["b"], x["s"]] for x in vs], [x["draft_ms"] for x in vs])
-        cd = np.array([c2[0], c2[1], 0.0])
-    ct = lstsq([[x["b"] * x["s"], x["s"], 1.0] for x in vs], [x["verify_ms"] for x in vs])
-    eed = [(x["b"], x["s"], ee[(x["b"], x["s"])] - x["verify_ms"]) for x in vs if (x["b"], x["s"]) in ee]
-    ce = lstsq([[b * s, 1.0] for b, s, _ in eed], [max(d, 1e-3) for _, _, d in eed])
-    ce = np.maximum(ce, [0.0, 1e-3])
-    # share factor: the reference's piecewise-linear shape (knee 0.5), continuous, factor(1) = 1
-    shape = {"knee": 0.5, "a1": 1.575, "gamma1": 0.9, "a2": 1.25, "gamma2": 0.25}
-    model = {
-        "draft": {"stage": 0, **shape, "c0": cd[0], "c1": cd[1], "c2": cd[2]},
-        "target": {"stage": 1, **shape, "c0": ct[0], "c1": ct[1], "c2": ct[2]},
-        "ee_check": {"stage": 2, **shape, "c0": ce[0], "c1": ce[1], "c2": 0.0},
-        # row compaction is folded into the measured ee_check delta; pruning itself ~10% of it
-        "prune": {"stage": 3, **shape, "c0": ce[0] * 0.1, "c1": ce[1] * 0.1, "c2": 0.0},
-    }
-    pd = lambda x: cd[0] * x["b"] + cd[1] * x["s"] + cd[2]
-    pt = lambda x: (ct[0] * x["b"] + ct[1]) * x["s"] + ct[2]
-    mape = {"draft": float(np.mean([abs(pd(x) - x["draft_ms"]) / x["draft_ms"] for x in vs])),
-            "target": float(np.mean([abs(pt(x) - x["verify_ms"]) / x["verify_ms"] for x in vs]))}
-    return {k: {kk: float(vv) for kk, vv in v.items()} for k, v in model.items()}, mape
+    """The reference's load forms by least squares (the same fit the online profiler refreshes
+    at run time: paper_2604_20503_b200/profiler.py fit_serial)."""
+    from paper_2604_20503_b200 import profiler
+    return profiler.fit_serial(samples)
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--refit":
