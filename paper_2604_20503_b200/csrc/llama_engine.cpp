@@ -638,6 +638,7 @@ class LlamaEngine {
     int cls;
     cudaEvent_t a, b;
     double bytes, flops;
+    int n;  // launches between the event pair (a run of back-to-back same-class launches)
   };
   std::vector<KPend> kpend;
   std::vector<cudaEvent_t> kpool;
@@ -653,13 +654,16 @@ class LlamaEngine {
     kpool.pop_back();
     return e;
   }
+  // `n` > 1: `launch` enqueues a run of n back-to-back launches of the class; one event pair
+  // brackets the run, so the programmatic (PDL) overlap between them stays intact (an event
+  // record between two launches serialises them) and the run's time is split evenly.
   template <class F>
-  void timed(int cls, double bytes, F&& launch, double flops = 0.0) {
+  void timed(int cls, double bytes, F&& launch, double flops = 0.0, int n = 1) {
     if (!ktiming || capturing || cls < 0) {
       launch();
       return;
     }
-    KPend p{cls, kev(), kev(), bytes, flops};
+    KPend p{cls, kev(), kev(), bytes, flops, n};
     LCK(cudaEventRecord(p.a, fs));
     launch();
     LCK(cudaEventRecord(p.b, fs));
@@ -673,7 +677,7 @@ class LlamaEngine {
       k_ms[p.cls] += ms;
       k_bytes[p.cls] += p.bytes;
       k_flops[p.cls] += p.flops;
-      k_n[p.cls] += 1;
+      k_n[p.cls] += p.n;
       kpool.push_back(p.a);
       kpool.push_back(p.b);
     }
@@ -793,19 +797,28 @@ class LlamaEngine {
         LCK(tp_resid_add(tp_part.as<__nv_bfloat16>(), w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), T, s.d, fs));
         launches += 2;
       };
-      if (tp_rows)
-        row_parallel(m.op_o[l], w.op_ob, p_o);
-      else if (!(skip & 4))
-        timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); },
-              gflops(s.d, qd));
-      if (!(skip & 8))
-      timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); },
-            gflops(2 * s.ffn, s.d));
-      if (tp_rows)
-        row_parallel(m.op_d[l], w.op_h, p_d);
-      else if (!(skip & 16))
-        timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); },
-              gflops(s.d, s.ffn));
+      if (!tp_rows && !(skip & 28)) {
+        // o -> gate/up -> down run back to back: one event pair around the run
+        timed(gcls, gbytes(s.d, qd, s.d) + gbytes(2 * s.ffn, s.d, s.ffn) + gbytes(s.d, s.ffn, s.d), [&] {
+          LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs));
+          LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs));
+          LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs));
+        }, gflops(s.d, qd) + gflops(2 * s.ffn, s.d) + gflops(s.d, s.ffn), 3);
+      } else {
+        if (tp_rows)
+          row_parallel(m.op_o[l], w.op_ob, p_o);
+        else if (!(skip & 4))
+          timed(gcls, gbytes(s.d, qd, s.d), [&] { LCK(gemm_fused(m.op_o[l], w.op_ob, T, p_o, e_res, fs)); },
+                gflops(s.d, qd));
+        if (!(skip & 8))
+        timed(gcls, gbytes(2 * s.ffn, s.d, s.ffn), [&] { LCK(gemm_fused(m.op_gu[l], w.op_xb, T, p_gu, e_glu, fs)); },
+              gflops(2 * s.ffn, s.d));
+        if (tp_rows)
+          row_parallel(m.op_d[l], w.op_h, p_d);
+        else if (!(skip & 16))
+          timed(gcls, gbytes(s.d, s.ffn, s.d), [&] { LCK(gemm_fused(m.op_d[l], w.op_h, T, p_d, e_res, fs)); },
+                gflops(s.d, s.ffn));
+      }
       launches += 5;
       const int layer = l + 1;  // residual now holds the output of `layer` layers
       if (f.ee && layer >= f.gate_lo && layer < f.gate_hi && layer < s.layers) {

@@ -61,12 +61,15 @@ def to_model(d):
 
 
 def _lstsq(rows, y):
-    """Least squares; None when the design is rank-deficient (e.g. a serving load that only ever
-    ran one speculative length: the stage keeps its previous coefficients)."""
+    """Least squares in relative error (each row weighted by 1/y: stage times span 0.1-10 ms, and
+    the planners compare ratios); None when the design is rank-deficient (e.g. a serving load
+    that only ever ran one speculative length: the stage keeps its previous coefficients)."""
     A = np.array(rows, float)
     if np.linalg.matrix_rank(A) < A.shape[1]:
         return None
-    c, *_ = np.linalg.lstsq(A, np.array(y, float), rcond=None)
+    y = np.array(y, float)
+    w = 1.0 / np.maximum(np.abs(y), 1e-6)
+    c, *_ = np.linalg.lstsq(A * w[:, None], y * w, rcond=None)
     return c
 
 

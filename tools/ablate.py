@@ -56,8 +56,10 @@ def main():
                                          chunk=args.chunk, profiler=prof)
             m = serving.run_trace(eng, trace, V, prompt_seed=1, controller=ctl, num_layers=L, seed=1)
             if prof is not None:
-                print(json.dumps({"mode": mode, "online_refits": prof.refreshes, "history": prof.history[-3:]}),
-                      flush=True)
+                smp, n_rt = prof.samples()
+                print(json.dumps({"mode": mode, "online_refits": prof.refreshes, "history": prof.history[-3:],
+                                  "runtime_buckets": n_rt, "samples": smp[-n_rt:][:40],
+                                  "model": profiler.model_dict(ctl.models)}), flush=True)
             ctl.close()
         s = m["summary"]
         summaries.append(s)
