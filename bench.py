@@ -244,11 +244,14 @@ def make_engine(desc, args, local_rank, batch=None, **tp):
     from paper_2604_20503_b200 import engine
     mode = {"vsd": abi.MODE_VSD, "ad": abi.MODE_VSD_AD, "ee": abi.MODE_VSD_AD_EE,
             "ov": abi.MODE_FULL, "full": abi.MODE_FULL, "vsd_ee": abi.MODE_VSD_AD_EE}[args.mode]
-    return engine.ServingEngine(desc=desc, max_batch=batch or args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
-                                mode=mode, default_spec_length=args.k, max_spec_length=16,
-                                prefill_rows=8192, device=local_rank,
-                                prefill_lane=0 if (tp or args.no_prefill_lane) else 1,
-                                exempt_rule=2 if getattr(args, "recovery", False) else 1, **tp)
+    eng = engine.ServingEngine(desc=desc, max_batch=batch or args.batch, max_seq_len=IN_RANGE[1] + OUT_RANGE[1] + 8,
+                               mode=mode, default_spec_length=args.k, max_spec_length=16,
+                               prefill_rows=8192, device=local_rank,
+                               prefill_lane=0 if (tp or args.no_prefill_lane) else 1,
+                               exempt_rule=2 if getattr(args, "recovery", False) else 1, **tp)
+    if getattr(args, "temperature", 0.0) > 0.0:  # coupled Gumbel-max sampling acceptance
+        eng.set_sampling(args.temperature, 1)
+    return eng
 
 
 def tp_bootstrap(dist, rank, make_uid):
@@ -459,6 +462,8 @@ def llama_config(args, world, B):
     return {"workload": f"{WORKLOAD_NAMES.get(args.workload, args.workload)}, continuous batching "
                         f"B={B}/GPU, k={args.k}, mode={args.mode}, steady state (>= one request "
                         f"lifetime served before warm-up)",
+            **({"temperature": args.temperature, "acceptance_rule": "coupled Gumbel-max sampling"}
+               if getattr(args, "temperature", 0.0) > 0.0 else {}),
             "global_batch": B * world, "seq_len": f"in U{list(IN_RANGE)} out U{list(OUT_RANGE)}",
             "parallelism": f"replicas x{world} (request-sharded)",
             "l2": "target weights per verify >> 126 MB L2 (inputs larger than L2)"}
@@ -929,6 +934,8 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--mode", default="vsd", choices=["vsd", "ad", "ee", "ov", "full", "vsd_ee"])
+    ap.add_argument("--temperature", type=float, default=0.0,
+                    help="> 0: sampling acceptance (coupled Gumbel-max, faser_set_sampling); 0: greedy")
     ap.add_argument("--chunk", type=int, default=0, help="overlap chunk (0: plan_overlap decides)")
     ap.add_argument("--gate-layer", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)

@@ -487,6 +487,11 @@ faser_status faser_debug_set_skip_mask(faser_engine* e, int32_t mask) {
   return faser::llama_set_skip_mask(e->llama, mask);
 }
 
+faser_status faser_set_sampling(faser_engine* e, double temperature, uint64_t seed) {
+  if (!e || !e->llama) return FASER_EINVAL;
+  return faser::llama_set_sampling(e->llama, temperature, seed);
+}
+
 faser_status faser_set_prefill_lane(faser_engine* e, int32_t on) {
   if (!e) return FASER_EINVAL;
   if (!e->llama) return on ? FASER_EINVAL : FASER_OK;

@@ -341,6 +341,8 @@ class LlamaEngine {
   cudaEvent_t ev_pf_done[kBlobs] = {};  // per blob
   bool pf_lane = false;
   int skip_mask = -1;  // faser_debug_set_skip_mask (timing experiments); -1: FASER_SKIP
+  float samp_inv_tau = 0.f;  // faser_set_sampling: > 0 = coupled Gumbel-max sampling at 1 / tau
+  uint64_t samp_seed = 0;
   bool pf_defer = false;  // this step: new requests wait for the lane to drain
   int pf_in_flight_cap = 2;  // FASER_PF_INFLIGHT
   double pf_wait_ms = 0.0;  // host time blocked on a prefill (nothing runnable / blob ring full)
@@ -758,6 +760,12 @@ class LlamaEngine {
     e_lm.ss_in = w.ss.as<float>();
     e_lm.logits = w.logits.as<float>();
     e_lm.amax = w.amax.as<float2>();
+    if (samp_inv_tau > 0.f && f.logits) {  // draft steps and verify: sample, keyed by (request, position)
+      e_lm.rows = rows;
+      e_lm.req_ids = cur_q.req_id;
+      e_lm.samp_seed = samp_seed;
+      e_lm.inv_tau = samp_inv_tau;
+    }
 
     if (!f.pre_embedded) {
       LCK(lm_embed(s, m.emb, rows, T, w.x.as<float>(), w.xb.as<__nv_bfloat16>(), w.ss.as<float>(), fs));
@@ -1753,6 +1761,16 @@ faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev,
 float llama_last_step_prefill(const LlamaEngine* e) { return e->t_prefill; }
 faser_status llama_set_skip_mask(LlamaEngine* e, int mask) {
   return lguard(e, [&] { e->skip_mask = mask; });
+}
+faser_status llama_set_sampling(LlamaEngine* e, double temperature, uint64_t seed) {
+  return lguard(e, [&] {
+    if (!(temperature >= 0.0) || !std::isfinite(temperature)) throw LFail{FASER_EINVAL, "temperature must be >= 0"};
+    if (temperature > 0.0 && e->cfg.mode != FASER_MODE_VSD && e->cfg.mode != FASER_MODE_VSD_AD)
+      throw LFail{FASER_EINVAL, "sampling needs a full-verify mode (VSD / VSD_AD): the early-exit estimator "
+                                "and the chunked frontier rank raw logits"};
+    e->samp_inv_tau = temperature > 0.0 ? static_cast<float>(1.0 / temperature) : 0.f;
+    e->samp_seed = seed;
+  });
 }
 faser_status llama_set_prefill_lane(LlamaEngine* e, int on) {
   return lguard(e, [&] {

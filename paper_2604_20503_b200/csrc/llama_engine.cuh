@@ -33,6 +33,7 @@ float llama_last_step_prefill(const LlamaEngine* e);
 faser_status llama_join_lanes(LlamaEngine* e);
 faser_status llama_set_prefill_lane(LlamaEngine* e, int on);
 faser_status llama_set_skip_mask(LlamaEngine* e, int mask);
+faser_status llama_set_sampling(LlamaEngine* e, double temperature, uint64_t seed);
 void llama_last_step_bytes(const LlamaEngine* e, int64_t* h2d, int64_t* d2h);
 void* llama_stream(const LlamaEngine* e);
 faser_status llama_last_timeline(const LlamaEngine* e, faser_timeline_event* ev, int32_t cap, faser_timeline_info* info);

@@ -91,6 +91,31 @@ __device__ __forceinline__ void stamp(const EpiArgs& ea, int i) {
     ea.trace[cta * 8 + i] = gtimer();
   }
 }
+// Coupled Gumbel-max sampling noise (faser_set_sampling). The draft and the target perturb the
+// logits that predict absolute position `pos` of request `rid` with the SAME noise, so a drafted
+// token is accepted iff it equals the target's own sample: every committed token is the target's
+// Gumbel-max sample of softmax(z / tau) given its prefix (lossless in distribution, and identical
+// to non-speculative sampling with this noise whatever the drafter proposes). SplitMix64 mixing;
+// u = (23 random bits + 0.5) * 2^-23 in (0, 1) exactly, g = -log(-log(u)) in fp32.
+__device__ __forceinline__ uint64_t smix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t sample_key(uint64_t seed, int64_t rid, int pos) {
+  return smix64(smix64(seed) ^ (static_cast<uint64_t>(rid) * 0xd1b54a32d192ed03ull) ^
+                (static_cast<uint64_t>(pos) * 0x8cb92ba72f3d8dd7ull));
+}
+__device__ __forceinline__ float gumbel(uint64_t key, int id) {
+  const uint64_t h = smix64(key ^ (static_cast<uint64_t>(id) * 0x9e3779b97f4a7c15ull));
+  const float u = (static_cast<float>(static_cast<uint32_t>(h >> 41)) + 0.5f) * 0x1p-23f;
+  return -logf(-logf(u));
+}
+__device__ __forceinline__ float perturb(float z, float inv_tau, uint64_t key, int id) {
+  return __fadd_rn(__fmul_rn(z, inv_tau), gumbel(key, id));
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -114,6 +139,7 @@ __global__ void __launch_bounds__(128, 1)
   int* s_i0 = reinterpret_cast<int*>(s_red + 4 * 256);  // [4][BN] per-warp argmax ids
   int* s_pos = s_i0 + 4 * 256;  // [256] per-token position (QKV epilogue)
   int* s_page = s_pos + 256;    // [256] per-token KV page
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(s_pos);  // [256] sampling keys (kEpiLogits; aliases s_pos/s_page)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = blockIdx.x * MC * kBM;                       // first weight row of this CTA
@@ -236,6 +262,10 @@ __global__ void __launch_bounds__(128, 1)
         const int row = n0 + t;
         s_pos[t] = ea.row_d[row];
         s_page[t] = __float_as_int(ea.zd_src[static_cast<size_t>(row) * kBM + (row & (kBM - 1))]);
+      }
+      if (ea.mode == kEpiLogits && ea.inv_tau > 0.f) {  // the row's sampling key
+        const int row = n0 + t;
+        s_key[t] = sample_key(ea.samp_seed, ea.req_ids[ea.rows.row_req[row]], ea.rows.row_pos[row] + 1);
       }
       if (ea.mode == kEpiQkv) {
         const int row = n0 + t;
@@ -375,8 +405,13 @@ __global__ void __launch_bounds__(128, 1)
         } else {  // kEpiLogits
           a = make_float4(a.x * rs, a.y * rs, a.z * rs, a.w * rs);
           if (ea.logits) *reinterpret_cast<float4*>(ea.logits + idx) = a;  // validation / exit test only
-          float bv = a.x;
           const int id0 = ea.id_off + m0 + c4;
+          if (ea.inv_tau > 0.f) {  // Gumbel-max sampling: argmax of z / tau + g
+            const uint64_t key = s_key[t];
+            a = make_float4(perturb(a.x, ea.inv_tau, key, id0), perturb(a.y, ea.inv_tau, key, id0 + 1),
+                            perturb(a.z, ea.inv_tau, key, id0 + 2), perturb(a.w, ea.inv_tau, key, id0 + 3));
+          }
+          float bv = a.x;
           int bi = id0;
           if (a.y > bv) { bv = a.y; bi = id0 + 1; }
           if (a.z > bv) { bv = a.z; bi = id0 + 2; }

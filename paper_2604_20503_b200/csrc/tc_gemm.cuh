@@ -66,6 +66,13 @@ struct EpiArgs {
   const float* zd_src = nullptr;
   const int* row_d = nullptr;
   int* rank_cnt = nullptr;
+  // kEpiLogits sampling (faser_set_sampling): inv_tau > 0 perturbs the argmax operand of token t
+  // (row n0 + t) to logit * inv_tau + Gumbel(sample_key(samp_seed, req_ids[rows.row_req[row]],
+  // rows.row_pos[row] + 1), id): the per-tile (max, id) partials then hold a sample of
+  // softmax(logits / tau) (Gumbel-max); the logits written stay the raw ones. rows must be set.
+  const int64_t* req_ids = nullptr;
+  unsigned long long samp_seed = 0;
+  float inv_tau = 0.f;
   int t_begin = 0;                       // first token of this launch (token tiles start here)
   int w_after_wait = 0;                  // 1: the weights are written by the previous kernel (no
                                          // weight prefetch before griddepcontrol.wait)

@@ -341,6 +341,10 @@ class ServingEngine:
                                         C.c_double(r), int(num_layers), C.byref(tok), C.byref(rnd)), self.h)
         return tok.value, rnd.value
 
+    def set_sampling(self, temperature, seed=0):
+        """Coupled Gumbel-max sampling at `temperature` (0 = greedy); faser_set_sampling."""
+        _check(lib().faser_set_sampling(self.h, C.c_double(temperature), C.c_uint64(seed)), self.h)
+
     def debug_set_skip_mask(self, mask):
         """Timing experiments only: kernel classes the following steps skip (results invalid)."""
         _check(lib().faser_debug_set_skip_mask(self.h, int(mask)), self.h)
