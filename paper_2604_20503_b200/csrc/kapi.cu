@@ -18,13 +18,12 @@ __global__ void iota_kernel(int* a, int n, int* n_rows, int total) {
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
+  static const int n = [] {  // thread-safe one-time init (TP ranks call from several threads)
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (!n) n = 148;
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v ? v : 148;
+  }();
   return n;
 }
 

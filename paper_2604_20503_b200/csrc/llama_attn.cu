@@ -16,6 +16,7 @@
 // Few CTAs + long contexts split over KV (flash-decoding); the LAST split CTA to finish a
 // (request, kv head, block) merges the partial softmax states in split order (deterministic),
 // so there is no separate combine launch.
+#include <atomic>
 #include <mutex>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -632,9 +633,8 @@ cudaError_t lm_attention(const LlamaShape& m, RowsDev rows, int n_req, int max_r
     const int max_split = (tiles + 1) / 2 < 16 ? (tiles + 1) / 2 : 16;  // >= 2 pages per split
     if (n_split > max_split) n_split = max_split;
   }
-  static int dbg = getenv("FASER_ATTN_DEBUG") ? atoi(getenv("FASER_ATTN_DEBUG")) : 0;
-  if (dbg > 0) {
-    --dbg;
+  static std::atomic<int> dbg{getenv("FASER_ATTN_DEBUG") ? atoi(getenv("FASER_ATTN_DEBUG")) : 0};
+  if (dbg.load(std::memory_order_relaxed) > 0 && dbg.fetch_sub(1) > 0) {
     fprintf(stderr, "[attn] n_req %d max_rows %d max_ctx %d Mmax %d split %d tma %d group_tc %d rows_tc %d\n", n_req,
             max_rows_per_req, max_ctx, Mmax, n_split, kv.tma != nullptr,
             int(!rows_mode && attn_tc_applies(m, max_rows_per_req, max_ctx, kv)),
