@@ -288,15 +288,16 @@ faser_status faser_last_step_timing(const faser_engine* e, float* draft_ms, floa
  * next step drains it and admissions are prefilled in-step again) or back on (1). */
 faser_status faser_set_prefill_lane(faser_engine* e, int32_t on);
 /* Sampling acceptance (north-star K6 "greedy/rejection-sampling"; beyond the reference, which is
- * greedy only, sdcore.cpp:61-80). temperature > 0 (LLAMA engines, modes VSD /
- * VSD_AD): the draft and the target LM heads sample with coupled Gumbel-max noise - the token at
+ * greedy only, sdcore.cpp:61-80). temperature > 0 (LLAMA engines, every mode but
+ * FULL): the draft and the target LM heads sample with coupled Gumbel-max noise - the token at
  * absolute position p of request id r is argmax_v(z_v / temperature + G(seed, r, p, v)) for both
  * models - and the greedy match-and-commit kernel (K5) accepts drafted tokens while they equal
  * the target's sample, committing the target's sample at the first mismatch. Every committed
  * token is the target's sample of softmax(z / temperature) given its prefix: lossless in
  * distribution, and identical to non-speculative sampling with the same noise whatever the
- * drafter or k_i (drafter-invariant). temperature 0 restores greedy. Takes effect at the next
- * step; EINVAL for toy engines, EE / FULL modes, or temperature < 0. */
+ * drafter or k_i (drafter-invariant). In EE modes the fused exit-test estimator ranks the drafted
+ * token among the perturbed intermediate values (same noise). temperature 0 restores greedy.
+ * Takes effect at the next step; EINVAL for toy engines, FULL mode, or temperature < 0. */
 faser_status faser_set_sampling(faser_engine* e, double temperature, uint64_t seed);
 /* The serving loop of the missing sim.cpp as one call, for hosts that drive the
  * engine without per-step callbacks: up to n_rounds iterations of

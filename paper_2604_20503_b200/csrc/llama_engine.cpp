@@ -1765,9 +1765,8 @@ faser_status llama_set_skip_mask(LlamaEngine* e, int mask) {
 faser_status llama_set_sampling(LlamaEngine* e, double temperature, uint64_t seed) {
   return lguard(e, [&] {
     if (!(temperature >= 0.0) || !std::isfinite(temperature)) throw LFail{FASER_EINVAL, "temperature must be >= 0"};
-    if (temperature > 0.0 && e->cfg.mode != FASER_MODE_VSD && e->cfg.mode != FASER_MODE_VSD_AD)
-      throw LFail{FASER_EINVAL, "sampling needs a full-verify mode (VSD / VSD_AD): the early-exit estimator "
-                                "and the chunked frontier rank raw logits"};
+    if (temperature > 0.0 && e->cfg.mode == FASER_MODE_FULL)
+      throw LFail{FASER_EINVAL, "sampling is not wired into the chunked (FULL) verify lanes"};
     e->samp_inv_tau = temperature > 0.0 ? static_cast<float>(1.0 / temperature) : 0.f;
     e->samp_seed = seed;
   });

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(128, 1)
   int* s_i0 = reinterpret_cast<int*>(s_red + 4 * 256);  // [4][BN] per-warp argmax ids
   int* s_pos = s_i0 + 4 * 256;  // [256] per-token position (QKV epilogue)
   int* s_page = s_pos + 256;    // [256] per-token KV page
-  uint64_t* s_key = reinterpret_cast<uint64_t*>(s_pos);  // [256] sampling keys (kEpiLogits; aliases s_pos/s_page)
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(s_red);  // [256] sampling keys (kEpiLogits / kEpiRank)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = blockIdx.x * MC * kBM;                       // first weight row of this CTA
@@ -258,14 +258,18 @@ __global__ void __launch_bounds__(128, 1)
         rs = rsqrtf(((part[0] + part[1]) + (part[2] + part[3])) / ea.d_norm + ea.eps);
       }
       s_rs[t] = rs;
-      if (ea.mode == kEpiRank) {  // the row's drafted id and its z_d (s_pos / s_page reused)
-        const int row = n0 + t;
-        s_pos[t] = ea.row_d[row];
-        s_page[t] = __float_as_int(ea.zd_src[static_cast<size_t>(row) * kBM + (row & (kBM - 1))]);
-      }
-      if (ea.mode == kEpiLogits && ea.inv_tau > 0.f) {  // the row's sampling key
+      if ((ea.mode == kEpiLogits || ea.mode == kEpiRank) && ea.inv_tau > 0.f) {  // the row's sampling key
         const int row = n0 + t;
         s_key[t] = sample_key(ea.samp_seed, ea.req_ids[ea.rows.row_req[row]], ea.rows.row_pos[row] + 1);
+      }
+      if (ea.mode == kEpiRank) {  // the row's drafted id and its z_d (s_pos / s_page reused)
+        const int row = n0 + t;
+        const int dd = ea.row_d[row];
+        float zd = ea.zd_src[static_cast<size_t>(row) * kBM + (row & (kBM - 1))];
+        // sampling: rank d among the perturbed values, its own perturbed the same way
+        if (ea.inv_tau > 0.f && dd >= 0) zd = perturb(zd, ea.inv_tau, s_key[t], dd);
+        s_pos[t] = dd;
+        s_page[t] = __float_as_int(zd);
       }
       if (ea.mode == kEpiQkv) {
         const int row = n0 + t;
@@ -394,6 +398,11 @@ __global__ void __launch_bounds__(128, 1)
           const float zd = __int_as_float(s_page[t]);
           const int dd = s_pos[t];
           const int id0 = ea.id_off + m0 + c4;
+          if (ea.inv_tau > 0.f) {  // sampling: the exit test ranks the perturbed values
+            const uint64_t key = s_key[t];
+            a = make_float4(perturb(a.x, ea.inv_tau, key, id0), perturb(a.y, ea.inv_tau, key, id0 + 1),
+                            perturb(a.z, ea.inv_tau, key, id0 + 2), perturb(a.w, ea.inv_tau, key, id0 + 3));
+          }
           int c = 0;
           c += (id0 != dd) & ((a.x > zd) | ((a.x == zd) & (id0 < dd)));
           c += (id0 + 1 != dd) & ((a.y > zd) | ((a.y == zd) & (id0 + 1 < dd)));

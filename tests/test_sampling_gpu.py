@@ -26,7 +26,7 @@ def _gpu():
         pytest.skip("no GPU")
 
 
-def run(desc, prompts, max_out, tau, seed, kpat, mode=abi.MODE_VSD, rid0=1000):
+def run(desc, prompts, max_out, tau, seed, kpat, mode=abi.MODE_VSD, rid0=1000, gate=None, stats=None):
     eng = engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=160, mode=mode, default_spec_length=4,
                                max_spec_length=16, prefill_rows=1024)
     eng.set_sampling(tau, seed)
@@ -36,13 +36,37 @@ def run(desc, prompts, max_out, tau, seed, kpat, mode=abi.MODE_VSD, rid0=1000):
     while eng.live_requests():
         live = eng.live_requests()
         eng.set_spec_lengths(live, [kpat(r, s) for r in live])
+        if gate is not None:
+            eng.set_gate(gate)
         for r in eng.step():
             acc += r.outcome.accepted_count
             sub += r.outcome.submitted
+            if stats is not None:
+                stats["pruned"] = stats.get("pruned", 0) + r.outcome.has_pruned
         s += 1
     out = [eng.committed(rid0 + i) for i in range(len(prompts))]
     eng.close()
     return out, acc, sub
+
+
+def check_vs_oracle(desc, prompts, max_out, got, tau, seed):
+    V = desc.target.vocab
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
+    exact = differs_from_greedy = 0
+    for i, (p, m) in enumerate(zip(prompts, max_out)):
+        ref, rows = S.sampled_decode(tgt, p, m, V - 1, 1000 + i, seed, tau)
+        differs_from_greedy += ref != tgt.greedy(p, m, V - 1)
+        if got[i] == ref:
+            exact += 1
+            continue
+        j = next((q for q in range(min(len(got[i]), len(ref))) if got[i][q] != ref[q]), None)
+        assert j is not None, (i, got[i], ref)  # one is a prefix of the other: EOS / length bug
+        z, y = rows[j]
+        ys = np.sort(y)
+        # bf16 logits move each perturbed entry by <= LOGIT_TOL * range(z) / tau
+        assert ys[-1] - ys[-2] <= 2 * LOGIT_TOL * (z.max() - z.min()) / tau, (i, j, ys[-1] - ys[-2])
+    tgt.close()
+    return exact, differs_from_greedy
 
 
 KPATS = {"k1": lambda r, s: 1, "k4": lambda r, s: 4, "cycle": lambda r, s: (1, 2, 3, 4, 5, 6, 8, 10)[(r + s) % 8]}
@@ -59,25 +83,30 @@ def test_sampling_lossless_vs_oracle(preset, tau, kpat):
     max_out = [int(rng.integers(4, 24)) for _ in range(n)]
     seed = 20260417
     got, acc, sub = run(desc, prompts, max_out, tau, seed, KPATS[kpat])
-    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
-    exact = differs_from_greedy = 0
-    for i, (p, m) in enumerate(zip(prompts, max_out)):
-        ref, rows = S.sampled_decode(tgt, p, m, V - 1, 1000 + i, seed, tau)
-        differs_from_greedy += ref != tgt.greedy(p, m, V - 1)
-        if got[i] == ref:
-            exact += 1
-            continue
-        j = next((q for q in range(min(len(got[i]), len(ref))) if got[i][q] != ref[q]), None)
-        assert j is not None, (i, got[i], ref)  # one is a prefix of the other: EOS / length bug
-        z, y = rows[j]
-        ys = np.sort(y)
-        # bf16 logits move each perturbed entry by <= LOGIT_TOL * range(z) / tau
-        assert ys[-1] - ys[-2] <= 2 * LOGIT_TOL * (z.max() - z.min()) / tau, (i, j, ys[-1] - ys[-2])
-    tgt.close()
+    exact, differs_from_greedy = check_vs_oracle(desc, prompts, max_out, got, tau, seed)
     assert exact >= n // 2, f"only {exact}/{n} requests match the oracle's sampled decode exactly"
     assert differs_from_greedy >= 2, "sampling did not change the outputs"
     if kpat != "k1":
         assert 0 < acc < sub
+
+
+@pytest.mark.parametrize("exempt_rule", [1])
+def test_sampling_with_early_exit(exempt_rule):
+    """VSD_AD_EE with sampling: the fused exit-test estimator ranks the drafted token among the
+    perturbed intermediate values (the same noise the final sample uses); pruning only drops
+    rows, so the committed tokens stay the target's samples (lossless vs the oracle)."""
+    desc = llama.tiny()
+    V, L = desc.target.vocab, desc.target.layers
+    rng = np.random.default_rng(21)
+    n = 8
+    prompts = [rng.integers(0, V - 1, size=int(rng.integers(2, 40))).tolist() for _ in range(n)]
+    max_out = [int(rng.integers(6, 24)) for _ in range(n)]
+    st = {}
+    got, acc, sub = run(desc, prompts, max_out, 1.0, 7, KPATS["k4"], mode=abi.MODE_VSD_AD_EE,
+                        gate=abi.GatePlan(1, L, 1.0), stats=st)
+    exact, _ = check_vs_oracle(desc, prompts, max_out, got, 1.0, 7)
+    assert exact >= n // 2
+    assert st.get("pruned", 0) > 0, "the estimator never pruned"
 
 
 def test_sampling_drafter_invariant():
@@ -95,7 +124,7 @@ def test_sampling_drafter_invariant():
 
 def test_sampling_modes_and_arguments():
     desc = llama.tiny()
-    with engine.ServingEngine(desc=desc, max_batch=2, max_seq_len=64, mode=abi.MODE_VSD_AD_EE,
+    with engine.ServingEngine(desc=desc, max_batch=2, max_seq_len=64, mode=abi.MODE_FULL,
                               default_spec_length=4, max_spec_length=8, prefill_rows=256) as eng:
         with pytest.raises(engine.FaserError):
             eng.set_sampling(1.0, 1)
