@@ -26,9 +26,9 @@ def _gpu():
         pytest.skip("no GPU")
 
 
-def run(desc, prompts, max_out, tau, seed, kpat, mode=abi.MODE_VSD, rid0=1000, gate=None, stats=None):
+def run(desc, prompts, max_out, tau, seed, kpat, mode=abi.MODE_VSD, rid0=1000, gate=None, stats=None, **kw):
     eng = engine.ServingEngine(desc=desc, max_batch=4, max_seq_len=160, mode=mode, default_spec_length=4,
-                               max_spec_length=16, prefill_rows=1024)
+                               max_spec_length=16, prefill_rows=1024, **kw)
     eng.set_sampling(tau, seed)
     for i, (p, m) in enumerate(zip(prompts, max_out)):
         eng.submit(rid0 + i, p, m)
@@ -90,20 +90,23 @@ def test_sampling_lossless_vs_oracle(preset, tau, kpat):
         assert 0 < acc < sub
 
 
-@pytest.mark.parametrize("exempt_rule", [1])
+@pytest.mark.parametrize("exempt_rule", [1, 2])
 def test_sampling_with_early_exit(exempt_rule):
     """VSD_AD_EE with sampling: the fused exit-test estimator ranks the drafted token among the
     perturbed intermediate values (the same noise the final sample uses); pruning only drops
     rows, so the committed tokens stay the target's samples (lossless vs the oracle)."""
-    desc = llama.tiny()
-    V, L = desc.target.vocab, desc.target.layers
+    desc = llama.tiny(target_bigram=1.5)
+    V = desc.target.vocab
     rng = np.random.default_rng(21)
     n = 8
     prompts = [rng.integers(0, V - 1, size=int(rng.integers(2, 40))).tolist() for _ in range(n)]
     max_out = [int(rng.integers(6, 24)) for _ in range(n)]
     st = {}
+    # a small k_at (1 -> 4 -> 1) so the gated layers prune on this tiny pair (as in
+    # tests/test_llama_gpu.py test_early_exit_decisions_given_logits)
     got, acc, sub = run(desc, prompts, max_out, 1.0, 7, KPATS["k4"], mode=abi.MODE_VSD_AD_EE,
-                        gate=abi.GatePlan(1, L, 1.0), stats=st)
+                        gate=abi.GatePlan(1, 4, 1.0), stats=st, exit_policy=abi.ExitPolicy(1, 4, 1),
+                        exempt_rule=exempt_rule)
     exact, _ = check_vs_oracle(desc, prompts, max_out, got, 1.0, 7)
     assert exact >= n // 2
     assert st.get("pruned", 0) > 0, "the estimator never pruned"
