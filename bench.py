@@ -164,7 +164,7 @@ def llama_trace(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(DIST_BACKEND)
     from paper_2604_20503_b200 import serving
     desc = llama_desc(args.workload)
     V = desc.target.vocab
@@ -206,6 +206,10 @@ def llama_trace(args, rank, world, local_rank):
             "summary_rank0": m["summary"].as_json()}), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+# process-group backend of the N > 1 metric reduction (the data path has no collective)
+DIST_BACKEND = "gloo" if os.environ.get("FASER_BENCH_SHARE_GPU") == "1" else "nccl"
 
 
 def aggregate(stats, dist):
@@ -635,7 +639,7 @@ def llama_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(DIST_BACKEND)
     desc = llama_desc(args.workload)
     B = args.batch
     head = serve_point(args, desc, B, rank, world, local_rank, dist, want_e2e=True, want_kstats=True)
@@ -953,6 +957,11 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("FASER_BENCH_SHARE_GPU") == "1":
+        # functional check of the N > 1 launcher path on a one-GPU box: every rank's replica on
+        # cuda:0, metric reduction over gloo (NCCL refuses two ranks on one GPU). Not a
+        # performance number: the replicas share one GPU.
+        local_rank = 0
     if args.workload == "toy":
         (toy_reference if args.impl == "reference" else lambda a, r, w: toy_ours(a, r, w, local_rank))(args, rank, world)
     elif args.impl == "reference":

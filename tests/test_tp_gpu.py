@@ -85,3 +85,49 @@ def test_tensor_parallel_rejects_bad_configs():
     with pytest.raises(engine.FaserError):  # tiny's target (4q/2kv heads) does not split 4 ways
         make(llama.tiny(), tp_size=4, tp_rank=0, tp_group=engine.TpGroup.local(4))
     g2.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tensor_parallel_sampling(tp):
+    """Sampling acceptance under TP: every vocab shard perturbs its logits with the noise of its
+    GLOBAL token ids, so the all-gathered (max, id) is the same Gumbel-max sample as unsharded;
+    ranks agree bit-exactly and the outputs are the fp32 oracle's coupled-Gumbel samples."""
+    from oracle import sampling as S
+    desc = llama.tp_tiny()
+    V = desc.target.vocab
+    rng = np.random.default_rng(40 + tp)
+    prompts = [rng.integers(0, V - 1, size=int(rng.integers(3, 40))).tolist() for _ in range(6)]
+    max_out = [int(rng.integers(4, 24)) for _ in range(6)]
+    ks = [1, 2, 4, 6]
+    group = engine.TpGroup.local(tp)
+    engines = [make(desc, tp_size=tp, tp_rank=r, tp_group=group) for r in range(tp)]
+    for e in engines:
+        e.set_sampling(1.0, 31337)
+    outs = [None] * tp
+    th = [threading.Thread(target=serve, args=(engines[r], prompts, max_out, ks, outs, r)) for r in range(tp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for e in engines:
+        e.close()
+    group.close()
+    assert all(o is not None for o in outs), "a TP rank failed"
+    for r in range(1, tp):
+        assert outs[r] == outs[0]
+    got = outs[0][0]
+    tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b, threads=2)
+    try:
+        exact = 0
+        for i, (p, m) in enumerate(zip(prompts, max_out)):
+            ref, rows = S.sampled_decode(tgt, p, m, V - 1, i, 31337, 1.0)
+            if got[i] == ref:
+                exact += 1
+                continue
+            q = next(q for q in range(min(len(got[i]), len(ref))) if got[i][q] != ref[q])
+            z, y = rows[q]
+            ys = np.sort(y)
+            assert ys[-1] - ys[-2] <= 2 * LOGIT_TOL * (z.max() - z.min()), (i, q)
+        assert exact >= 3
+    finally:
+        tgt.close()
