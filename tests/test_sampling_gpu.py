@@ -147,3 +147,18 @@ def test_sampling_modes_and_arguments():
     tgt = lmoracle.Model(desc.target, desc.bigram_a, desc.bigram_b)
     assert got == tgt.greedy(p, 12, desc.target.vocab - 1)
     tgt.close()
+
+
+def test_sampling_config3_shapes():
+    """The benchmarked shapes (config 3: 32000-entry vocabulary = 250 LM-head tiles, llama-68m
+    draft / TinyLlama-1.1B target) at tau = 0.5, k = 4: outputs are the fp32 oracle's
+    coupled-Gumbel samples (near-tie rule as above)."""
+    desc = llama.config3()
+    V = desc.target.vocab
+    rng = np.random.default_rng(8)
+    prompts = [rng.integers(0, V - 1, size=int(rng.integers(8, 24))).tolist() for _ in range(3)]
+    max_out = [6, 5, 6]
+    tau, seed = 0.5, 4242
+    got, acc, sub = run(desc, prompts, max_out, tau, seed, KPATS["k4"])
+    exact, _ = check_vs_oracle(desc, prompts, max_out, got, tau, seed)
+    assert exact >= 1
