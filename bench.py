@@ -10,7 +10,9 @@ verify forward (+ early exit) -> fused accept/commit for every live request.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--batch B] [--k K]
                   [--mode vsd|ad|ee|vsd_ee|full] [--workload cfg3|cfg4|cfg5|toy] [--no-sweep]
-                  [--trace SECONDS] [--tp]
+                  [--trace SECONDS] [--tp] [--temperature TAU] [--recovery --gate-layer L]
+FASER_BENCH_SHARE_GPU=1 (under torchrun): every rank's replica on cuda:0 with a gloo metric
+reduction — a functional check of the N > 1 path on a one-GPU box, not a performance number.
 
 Measurement window: before the W warm-up steps every point serves until at least B requests
 have finished (<= FILL_CAP untimed steps), so the K timed steps see the steady-state mix of
