@@ -137,8 +137,10 @@ class OnlineProfiler:
     kept per (b, s) bucket (the newest win); a bucket's sample is its median."""
 
     def __init__(self, base_model, prior=None, period_steps=256, period_s=0.0, window=16, min_buckets=3):
+        """``prior``: the offline grid of the SAME model pair (e.g. offline_samples() for config
+        3, whose grid profiles/r01_latency_model.json holds); None = runtime samples only."""
         self.base = model_dict(base_model) if not isinstance(base_model, dict) else base_model
-        self.prior = offline_samples() if prior is None else list(prior)
+        self.prior = list(prior) if prior is not None else []
         self.period_steps, self.period_s, self.window, self.min_buckets = period_steps, period_s, window, min_buckets
         self.buckets = {}
         self.lock = threading.Lock()

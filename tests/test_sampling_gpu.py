@@ -162,3 +162,19 @@ def test_sampling_config3_shapes():
     got, acc, sub = run(desc, prompts, max_out, tau, seed, KPATS["k4"])
     exact, _ = check_vs_oracle(desc, prompts, max_out, got, tau, seed)
     assert exact >= 1
+
+
+def test_sampling_with_prefill_lane():
+    """Sampling with the admission-prefill lane (the bench configuration): requests join the
+    batch at different steps than without the lane, but the noise is keyed by (request,
+    position) only, so the committed sequences are the oracle's samples either way."""
+    desc = llama.tiny()
+    V = desc.target.vocab
+    rng = np.random.default_rng(17)
+    n = 8
+    prompts = [rng.integers(0, V - 1, size=int(rng.integers(2, 60))).tolist() for _ in range(n)]
+    max_out = [int(rng.integers(4, 24)) for _ in range(n)]
+    got, acc, sub = run(desc, prompts, max_out, 1.0, 555, KPATS["cycle"], prefill_lane=1)
+    exact, _ = check_vs_oracle(desc, prompts, max_out, got, 1.0, 555)
+    assert exact >= n // 2
+    assert 0 < acc < sub

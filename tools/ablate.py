@@ -51,7 +51,9 @@ def main():
             prof = None
             if args.refresh_steps and models is not None:
                 from paper_2604_20503_b200 import profiler
-                prof = profiler.OnlineProfiler(models, period_steps=args.refresh_steps)
+                # the offline grid is config 3's (tools/profile_latency.py): a prior only for it
+                prior = profiler.offline_samples() if args.workload == "cfg3" else None
+                prof = profiler.OnlineProfiler(models, prior=prior, period_steps=args.refresh_steps)
             ctl = serving.ModeController(mode, L, fixed_k=args.k, models=models, gate_layer=args.gate_layer,
                                          chunk=args.chunk, profiler=prof)
             m = serving.run_trace(eng, trace, V, prompt_seed=1, controller=ctl, num_layers=L, seed=1)
