@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -27,6 +28,7 @@
 #include "faser/engine.h"
 #include "oracle.h"
 #include "specsim/exitctl.hpp"
+#include "specsim/drafter.hpp"
 #include "specsim/latmodel.hpp"
 #ifdef SPECREF_METRICS
 #include "specsim/metrics.hpp"
@@ -428,6 +430,116 @@ int specref_acceptance_window_replay(const int32_t* s, const int32_t* submitted,
     for (int j = 0; j < nq; ++j) out[static_cast<size_t>(i) * (nq + 1) + j] = w.rate_for(qs[j]);
     out[static_cast<size_t>(i) * (nq + 1) + nq] = w.overall();
   }
+  return 0;
+}
+
+// ------------------------------------------------------------------ AdaptiveDrafter
+// The reference's own AdaptiveDrafter / GpPosterior / AcceptanceBook (drafter.cpp, compiled in
+// place against oracle/eigen_shim for its three Eigen calls) behind the same glue the product's
+// faser_drafter_* applies for the missing sim loop (include/faser/engine.h): per round each
+// request's (spec, submitted, accepted) is pushed into its AcceptanceWindow (W = window_request),
+// rounds with submitted > 0 record their ratio in the AcceptanceBook under the round number
+// rounds_in(key) + 1, and observe_round gets the mean ratio per distinct spec length.
+namespace {
+specsim::PiecewiseLatencyParams to_params(const faser_latency_params& p) {
+  specsim::PiecewiseLatencyParams q;
+  q.stage = static_cast<specsim::StageKind>(p.stage);
+  q.knee = p.knee;
+  q.a1 = p.a1;
+  q.gamma1 = p.gamma1;
+  q.a2 = p.a2;
+  q.gamma2 = p.gamma2;
+  q.c0 = p.c0;
+  q.c1 = p.c1;
+  q.c2 = p.c2;
+  return q;
+}
+struct RefDrafter {
+  specsim::LatencyModel models;
+  specsim::DrafterConfig cfg;
+  specsim::AcceptanceBook book;
+  specsim::AdaptiveDrafter drafter;
+  std::map<int64_t, specsim::Request> reqs;
+  RefDrafter(const specsim::DrafterConfig& c, const specsim::LatencyModel& m)
+      : models(m), cfg(c), book(c.window_ctx, c.cold_start_accept), drafter(c, &models) {}
+};
+}  // namespace
+
+void* specref_drafter_create(const faser_drafter_cfg* c, const faser_latency_model* m) {
+  specsim::DrafterConfig cfg;
+  cfg.candidates.assign(c->candidates, c->candidates + c->n_candidates);
+  cfg.epsilon = c->epsilon;
+  cfg.window_ctx = c->window_ctx;
+  cfg.window_request = c->window_request;
+  cfg.kernel_len = c->kernel_len;
+  cfg.kernel_var = c->kernel_var;
+  cfg.noise_var = c->noise_var;
+  cfg.cold_start_accept = c->cold_start_accept;
+  specsim::LatencyModel lm = specsim::LatencyModel::default_ground_truth();
+  if (m) {
+    lm.draft = to_params(m->draft);
+    lm.target = to_params(m->target);
+    lm.ee_check = to_params(m->ee_check);
+    lm.prune = to_params(m->prune);
+  }
+  return new RefDrafter(cfg, lm);
+}
+void specref_drafter_destroy(void* h) { delete static_cast<RefDrafter*>(h); }
+
+int specref_drafter_assign(void* h, const int64_t* ids, int32_t n, int32_t b, double r, int32_t* out) {
+  auto* d = static_cast<RefDrafter*>(h);
+  std::vector<const specsim::Request*> batch;
+  for (int i = 0; i < n; ++i) {
+    specsim::Request& q = d->reqs[ids[i]];
+    q.id = static_cast<int>(ids[i]);
+    batch.push_back(&q);
+  }
+  try {
+    const std::vector<int> k = d->drafter.assign_lengths(batch, b, r, d->book);
+    for (int i = 0; i < n; ++i) out[i] = k[i];
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
+int specref_drafter_observe(void* h, int32_t b, double r, double t_obs_ms, const int64_t* ids, const int32_t* spec,
+                            const int32_t* submitted, const int32_t* accepted, int32_t n) {
+  auto* d = static_cast<RefDrafter*>(h);
+  const specsim::ContextKey key = specsim::ContextKey::of(b, r);
+  const int round = d->drafter.rounds_in(key) + 1;
+  std::map<int, std::pair<double, int>> by_s;
+  for (int i = 0; i < n; ++i) {
+    specsim::Request& q = d->reqs[ids[i]];
+    q.accept_window.push({spec[i], submitted[i], accepted[i]}, d->cfg.window_request);
+    if (submitted[i] > 0) {
+      const double ratio = static_cast<double>(accepted[i]) / submitted[i];
+      d->book.record(key, round, spec[i], ratio);
+      auto& e = by_s[spec[i]];
+      e.first += ratio;
+      e.second += 1;
+    }
+  }
+  std::vector<std::pair<int, double>> acc;
+  for (const auto& [s, e] : by_s) acc.emplace_back(s, e.first / e.second);
+  try {
+    d->drafter.observe_round(b, r, t_obs_ms, acc);
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
+int specref_drafter_posterior(void* h, int32_t b, double r, double* mu, double* sigma, int32_t* rounds) {
+  auto* d = static_cast<RefDrafter*>(h);
+  const specsim::ContextKey key = specsim::ContextKey::of(b, r);
+  const specsim::GpPosterior* gp = d->drafter.find_posterior(key);
+  for (size_t i = 0; i < d->cfg.candidates.size(); ++i) {
+    const int s = d->cfg.candidates[i];
+    mu[i] = gp ? gp->mu(s, d->cfg) : 0.0;
+    sigma[i] = gp ? gp->sigma(s, d->cfg) : std::sqrt(d->cfg.kernel_var);
+  }
+  *rounds = d->drafter.rounds_in(key);
   return 0;
 }
 

@@ -152,3 +152,62 @@ def test_estimate_fallback_chain():
     assert a[2] == 0.5           # request 1 has no s = 2 round: the context's rate for s = 2
     assert a[3] == (0.75 + 0.5) / 2  # nobody ran s = 5: the context overall
     d.close()
+
+
+def test_drafter_matches_reference_translation_unit():
+    """The native AdaptiveDrafter (csrc/drafter.cpp) against the REFERENCE's own drafter.cpp,
+    compiled in place into oracle/_ref with oracle/eigen_shim standing in for its three Eigen
+    calls (MatrixXd / VectorXd / LLT solve): same k_i assignments round by round (cold-start
+    sweep, then GP-LCB with the AcceptanceBook estimates and the latency lanes) and the same GP
+    posterior to rounding, over a random serving history in two (b, r) contexts."""
+    import ctypes as C
+    import os
+
+    import pytest
+
+    from oracle import pyoracle as po
+    from paper_2604_20503_b200 import llama
+    if not os.path.exists(po.REF_SO):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    L = C.CDLL(po.REF_SO)
+    if not hasattr(L, "specref_drafter_create"):
+        pytest.skip("oracle/_ref predates the drafter export")
+    L.specref_drafter_create.restype = C.c_void_p
+    L.specref_drafter_create.argtypes = [C.c_void_p, C.c_void_p]
+    L.specref_drafter_destroy.argtypes = [C.c_void_p]
+    L.specref_drafter_assign.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_void_p]
+    L.specref_drafter_observe.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_int32]
+    L.specref_drafter_posterior.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    cfg = controller.DrafterCfg.default()
+    for models in (None, llama.fitted_latency_model()):
+        nat = controller.AdaptiveDrafter(cfg, models=models)
+        ref = L.specref_drafter_create(C.byref(cfg), C.byref(models) if models is not None else None)
+        rng = np.random.default_rng(7)
+        pool = np.arange(100, 140, dtype=np.int64)
+        mism = 0
+        for rnd in range(160):
+            b = int(rng.choice([4, 16]))
+            r = float(rng.choice([1.0, 0.5]))
+            live = np.sort(rng.choice(pool, size=b, replace=False)).astype(np.int64)
+            kn = np.array(nat.assign_lengths(live, b, r), np.int32)
+            kr = np.zeros(b, np.int32)
+            assert L.specref_drafter_assign(ref, P(live), b, b, r, P(kr)) == 0
+            mism += int((kn != kr).sum())
+            spec = kn
+            sub = np.minimum(spec, rng.integers(1, 11, size=b)).astype(np.int32)
+            acc = np.array([rng.integers(0, s + 1) for s in sub], np.int32)
+            t = float(rng.uniform(1.0, 6.0))
+            nat.observe_round(b, r, t, live, spec, sub, acc)
+            assert L.specref_drafter_observe(ref, b, r, t, P(live), P(spec), P(sub), P(acc), b) == 0
+            mu_n, sd_n, rn = nat.posterior(b, r)
+            mu_r, sd_r = np.zeros(cfg.n_candidates), np.zeros(cfg.n_candidates)
+            rr = C.c_int32()
+            L.specref_drafter_posterior(ref, b, r, P(mu_r), P(sd_r), C.byref(rr))
+            assert rn == rr.value
+            np.testing.assert_allclose(mu_n, mu_r, rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(sd_n, sd_r, rtol=1e-9, atol=1e-9)
+        assert mism == 0, f"{mism} k_i assignments differ from the reference drafter"
+        L.specref_drafter_destroy(ref)
+        nat.close()
