@@ -294,9 +294,13 @@ def llama_tp(args, rank, world, local_rank):
     dist.barrier()
     torch.cuda.synchronize()
     dev_ms, tokens, first, last, clock = 0.0, 0, {}, {}, 0.0
+    ph = [0.0, 0.0]  # draft (+ admission) / verify + accept device ms over the timed steps
     for _ in range(args.steps):
         res = eng.step()
-        dt = eng.last_step_timing()[2]
+        tm = eng.last_step_timing()
+        dt = tm[2]
+        ph[0] += tm[0]
+        ph[1] += tm[1]
         dev_ms += dt
         clock += dt
         for r in res:
@@ -317,7 +321,11 @@ def llama_tp(args, rank, world, local_rank):
             "p50_tpot_ms": tp50[len(tp50) // 2] if tp50 else 0.0,
             "config": {"workload": f"{args.workload}: TP={world} verification (NCCL all-reduce after O/down, "
                        f"vocab-parallel argmax), replicated draft, B={B}, k={args.k}", "global_batch": B,
-                       "parallelism": f"tp{world}"}}), flush=True)
+                       "parallelism": f"tp{world}"},
+            "device_ms_per_step": {"draft": ph[0] / args.steps, "verify_accept": ph[1] / args.steps},
+            # per rank: each streams 1/world of the target's weights (and KV heads) per verify
+            "verify_forward_roofline": tp_rank_roofline(llama_roofline(desc, B, args.k, ph[1] / args.steps), world)}),
+              flush=True)
     eng.close()
     group.close()
     dist.destroy_process_group()
@@ -799,6 +807,18 @@ def llama_roofline(desc, B, k, verify_ms):
             "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": src,
             "kernel": "target verify forward (tcgen05 GEMMs + paged attention + accept), per step",
             "algorithmic_bytes": bytes_, "rows_per_verify": B * k}
+
+
+def tp_rank_roofline(roof, world):
+    """A TP rank streams 1/world of the verify's algorithmic bytes in the same time."""
+    if world <= 1:
+        return roof
+    r = dict(roof)
+    r["algorithmic_bytes"] = roof["algorithmic_bytes"] / world
+    r["achieved"] = roof["achieved"] / world
+    r["frac"] = roof["frac"] / world
+    r["note"] = f"per rank: 1/{world} of the target's weights and KV"
+    return r
 
 
 def llama_cpu_sample(desc, args, budget_s=20.0):
