@@ -127,7 +127,10 @@ struct LmModel {
     s.n_q /= tp;
     s.n_kv /= tp;
     s.ffn /= tp;
-    s.vocab /= tp;
+    // vocab-parallel LM head: ceil(V / tp) rows per rank rounded up to the 128-row tile; rank r
+    // holds global ids [r * Vs, r * Vs + Vs), rows past V are zero padding masked out of the
+    // argmax (EpiArgs::id_limit), so any V splits (config 5: 128256 over 8 ranks)
+    if (tp > 1) s.vocab = ((full.vocab + tp - 1) / tp + 127) / 128 * 128;
     sh = s;
     const int64_t d = s.d, qkv = s.qkv_out(), qd = static_cast<int64_t>(s.n_q) * s.hd, F = s.ffn, V = s.vocab;
     const int64_t Vf = full.vocab, hd = s.hd;
@@ -146,7 +149,10 @@ struct LmModel {
       full_lm.alloc(static_cast<size_t>(Vf) * d * 2);
       LCK(lm_init_matrix(full_lm.as<__nv_bfloat16>(), Vf * d, s.seed, kTagLm * 4096u, s.init_std, st));
       LCK(lm_init_embedding(emb, full_lm.as<__nv_bfloat16>(), full, ga, gb, st));
-      LCK(cudaMemcpyAsync(lm, full_lm.as<__nv_bfloat16>() + rank * V * d, V * d * 2, cudaMemcpyDeviceToDevice, st));
+      const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(V, Vf - rank * V));  // rows < full vocab
+      if (valid > 0)
+        LCK(cudaMemcpyAsync(lm, full_lm.as<__nv_bfloat16>() + rank * V * d, valid * d * 2, cudaMemcpyDeviceToDevice, st));
+      if (valid < V) LCK(cudaMemsetAsync(lm + valid * d, 0, (V - valid) * d * 2, st));
       LCK(cudaStreamSynchronize(st));
     }
     const int64_t nqf = full.n_q, nkvf = full.n_kv;
@@ -533,7 +539,7 @@ class LlamaEngine {
         throw LFail{FASER_EINVAL, "tensor-parallel verification supports modes VSD and VSD_AD"};
       if (cfg.debug_capture) throw LFail{FASER_EINVAL, "debug_capture is not available with tp_size > 1"};
       const faser_llama_shape& t = m->target;
-      if (t.n_heads % tp || t.n_kv_heads % tp || t.ffn % (64 * tp) || t.vocab % (128 * tp) ||
+      if (t.n_heads % tp || t.n_kv_heads % tp || t.ffn % (64 * tp) ||
           ((t.n_heads + 2 * t.n_kv_heads) / tp * t.head_dim) % 128 || (t.n_heads / tp * t.head_dim) % 128)
         throw LFail{FASER_EINVAL, "target shape does not split over tp_size ranks"};
     }
@@ -755,7 +761,10 @@ class LlamaEngine {
     e_part.mode = kEpiStore;
     e_part.out_bf16 = tp_part.as<__nv_bfloat16>();
     EpiArgs e_lm = base;
-    if (is_tp_target) e_lm.id_off = tp_rank * s.vocab;  // global token ids of this vocab shard
+    if (is_tp_target) {
+      e_lm.id_off = tp_rank * s.vocab;  // global token ids of this vocab shard
+      e_lm.id_limit = tsh.vocab;        // padding rows of the last shard(s) never win the argmax
+    }
     e_lm.mode = kEpiLogits;
     e_lm.ss_in = w.ss.as<float>();
     e_lm.logits = w.logits.as<float>();

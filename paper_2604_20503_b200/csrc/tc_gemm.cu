@@ -420,6 +420,12 @@ __global__ void __launch_bounds__(128, 1)
             a = make_float4(perturb(a.x, ea.inv_tau, key, id0), perturb(a.y, ea.inv_tau, key, id0 + 1),
                             perturb(a.z, ea.inv_tau, key, id0 + 2), perturb(a.w, ea.inv_tau, key, id0 + 3));
           }
+          if (ea.id_limit && id0 + 3 >= ea.id_limit) {  // vocab padding of a TP shard
+            if (id0 >= ea.id_limit) a.x = -FLT_MAX;
+            if (id0 + 1 >= ea.id_limit) a.y = -FLT_MAX;
+            if (id0 + 2 >= ea.id_limit) a.z = -FLT_MAX;
+            if (id0 + 3 >= ea.id_limit) a.w = -FLT_MAX;
+          }
           float bv = a.x;
           int bi = id0;
           if (a.y > bv) { bv = a.y; bi = id0 + 1; }

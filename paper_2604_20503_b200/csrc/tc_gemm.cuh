@@ -60,6 +60,7 @@ struct EpiArgs {
   float* logits = nullptr;               // kEpiLogits [t][n_out]; nullptr: argmax partials only
   float2* amax = nullptr;                // kEpiLogits [n_out/128][t_stride] (value, idx bits)
   int id_off = 0;                        // kEpiLogits: id of output row 0 (vocab-parallel shard)
+  int id_limit = 0;                      // kEpiLogits: ids >= id_limit are padding (0 = none)
   // kEpiRank: z_d of token t = zd_src[t * 128 + t % 128] (a [t][128] block-diagonal GEMM over the
   // gathered rows W[d_t], same accumulation order as this LM head), d_t = row_d[t] (-1: no test);
   // counts -> rank_cnt[n_out/128][t_stride]. logits (optional) are written as in kEpiLogits.

@@ -34,9 +34,22 @@ def make(desc, **kw):
                                 max_spec_length=8, prefill_rows=1024, **kw)
 
 
-@pytest.mark.parametrize("preset,tp", [("tp_tiny", 2), ("tp_tiny", 4), ("tp_tiny", 8), ("tiny128", 2)])
+def tp_tiny_v1152():
+    """tp_tiny with a 1152-entry vocabulary: 1152 / tp is not a multiple of the 128-row LM-head
+    tile for tp = 2, 4, 8 (config 5's 128256 over 8 ranks has the same property), so the
+    vocab-parallel shards are padded and at tp = 8 three ranks hold padding only."""
+    return llama._pair(llama.shape(128, 2, 2, 2, 64, 256, 1152, seed=41, bigram=llama.DRAFT_BIGRAM),
+                       llama.shape(256, 3, 16, 8, 64, 512, 1152, seed=42, bigram=llama.TARGET_BIGRAM["tiny"],
+                                   hard=0.0))
+
+
+PRESETS = {**llama.PRESETS, "tp_tiny_v1152": tp_tiny_v1152}
+
+
+@pytest.mark.parametrize("preset,tp", [("tp_tiny", 2), ("tp_tiny", 4), ("tp_tiny", 8), ("tiny128", 2),
+                                       ("tp_tiny_v1152", 2), ("tp_tiny_v1152", 4), ("tp_tiny_v1152", 8)])
 def test_tensor_parallel_verify_matches_unsharded(preset, tp):
-    desc = llama.PRESETS[preset]()
+    desc = PRESETS[preset]()
     V = desc.target.vocab
     rng = np.random.default_rng(tp)
     prompts = [rng.integers(0, V - 1, size=int(rng.integers(3, 40))).tolist() for _ in range(7)]
