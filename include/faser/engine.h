@@ -211,7 +211,9 @@ typedef struct faser_engine_cfg {
   /* Tensor-parallel verification (config 5): the TARGET is split over tp_size
    * ranks (column-parallel QKV / gate-up, row-parallel O / down + all-reduce, vocab-parallel LM
    * head + all-gathered argmax); the draft is replicated. tp_size <= 1: no TP. Modes VSD and
-   * VSD_AD only. Every rank drives its own engine with the same submits and plans. */
+   * VSD_AD only. Every rank drives its own engine with the same submits and plans. Heads and
+   * ffn / 64 must divide by tp_size; the vocabulary need not (each rank's LM-head shard is
+   * ceil(vocab / tp_size) rounded up to 128 rows, the padding masked out of the argmax). */
   int32_t tp_size;
   int32_t tp_rank;
   struct faser_tp_group* tp_group; /* from faser_tp_*_group_create; not owned by the engine */
